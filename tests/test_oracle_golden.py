@@ -1,0 +1,157 @@
+"""Pin the CPU oracle (oracle/flash_oracle.py) to the reference.
+
+CPU-only. Three kinds of evidence:
+1. golden vectors produced by the unmodified reference (tests/golden/*.npz):
+   quantize codes/scales/zeros/wire bytes and dequantize outputs; flash
+   all-reduce outputs; the reference's own per-piece wire messages;
+2. the known-answer tests of the reference test-suite (cited file:line);
+3. the reference's reported error numbers (reports.json).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import flash_oracle as orc
+from tests import golden_io as gio
+
+
+# ---------------------------------------------------------------- codec goldens
+
+@pytest.mark.parametrize("i", range(len(gio.codec_meta())))
+def test_codec_matches_reference(i):
+    z = gio.codec_npz()
+    meta = gio.codec_meta()[i]
+    codec = gio.oracle_codec(meta)
+    x = z[f"x{i}"]
+    q = orc.quantize(x, codec)
+    assert q.wire_bytes() == bytes(z[f"wire{i}"])
+    if codec.kind != "fp16":
+        assert np.array_equal(q.codes, z[f"codes{i}"])
+        assert np.array_equal(q.scales.view(np.uint16), z[f"scales{i}"].view(np.uint16))
+        if not codec.symmetric:
+            assert np.array_equal(q.zeros, z[f"zeros{i}"])
+    d = orc.dequantize(q)
+    assert np.array_equal(d.view(np.uint32), z[f"deq{i}"].view(np.uint32))
+
+
+# ---------------------------------------------------------------- flash goldens
+
+@pytest.mark.parametrize("i", range(len(gio.flash_meta())))
+def test_flash_matches_reference(i):
+    meta, xs, ref_out, ref_exact = gio.flash_case(i)
+    s1, s2 = gio.oracle_stage(meta["stage1"]), gio.oracle_stage(meta["stage2"])
+    res = orc.flash_all_reduce(xs, s1, s2, meta["chunk"])
+    for o in res.outputs:
+        assert np.array_equal(o.view(np.uint32), ref_out.view(np.uint32))
+    assert np.array_equal(orc.all_reduce_exact(xs), ref_exact)
+    n = meta["n"]
+    assert res.wire_bytes_per_rank == meta["wire_bytes_per_rank"]
+    # the reference's own wire messages, per (src, dst), in send order:
+    # per piece, stage-1 piece (collectives.py:367) then stage-2 (:379-381)
+    piece = meta["resolved_chunk"] // n
+    for src in range(n):
+        for dst in range(n):
+            if src == dst:
+                continue
+            st1 = orc.piece_messages(res.stage1[dst][src], piece)
+            st2 = orc.piece_messages(res.stage2[src], piece)
+            expect = [m for pair in zip(st1, st2) for m in pair]
+            assert gio.flash_wire(i, src, dst) == expect
+
+
+# ---------------------------------------------------------------- known answers
+
+def test_known_group_params():
+    # test_codec.py:50-68: [0,3,6,15] int4 -> scale 1, zero 0; [-2,2] -> 4/15, 8
+    q = orc.quantize(np.array([0, 3, 6, 15], np.float32), orc.Codec(bits=4, group_size=4))
+    assert float(q.scales[0]) == 1.0 and q.zeros[0] == 0
+    q = orc.quantize(np.array([-2, 2], np.float32), orc.Codec(bits=4, group_size=2))
+    assert q.zeros[0] == 8 and q.codes.tolist() == [0, 15]  # test_codec.py:78-90
+    # zeros -> scale floor 1e-8 snapped up to fp16 grid (> 0), zero 0
+    q = orc.quantize(np.zeros(3, np.float32), orc.Codec(bits=8, group_size=3))
+    assert float(q.scales[0]) > 0 and q.zeros[0] == 0
+
+
+def test_identity_ramp():
+    # test_codec.py:72-78
+    x = np.arange(16, dtype=np.float32)
+    q = orc.quantize(x, orc.Codec(bits=4, group_size=16))
+    assert q.codes.tolist() == list(range(16))
+    assert np.array_equal(orc.dequantize(q), x)
+
+
+def test_symmetric_decode():
+    # test_codec.py:92-102: codes -8 and 7 at scale 0.5 -> [-4.0, 3.5]
+    q = orc.QSeg(np.array([(-8) & 0xF, 7], np.uint8), np.array([0.5], np.float16), None, 2,
+                 orc.Codec(bits=4, group_size=2, symmetric=True))
+    assert orc.dequantize(q).tolist() == [-4.0, 3.5]
+
+
+def test_pack_layout():
+    # bitpack tests test_bitpack.py:32-55
+    assert orc.pack(np.array([1, 2]), 4).tobytes() == bytes([0x21])
+    assert orc.pack(np.array([0xA, 0xB, 0xC]), 4).tobytes() == bytes([0xBA, 0x0C])
+    for lo in range(16):
+        for hi in range(16):
+            b = orc.pack(np.array([lo, hi]), 4)
+            assert b.tobytes() == bytes([(hi << 4) | lo])
+            assert orc.unpack(b, 2, 4).tolist() == [lo, hi]
+
+
+def test_wire_lengths():
+    # test_codec.py:138-150
+    assert orc.Codec(bits=4).wire_len(256) == 128 + 2 * 3
+    assert orc.Codec(bits=4, symmetric=True).wire_len(256) == 128 + 2 * 2
+    assert orc.Codec(bits=6).wire_len(128) == 128 + 3
+
+
+def test_accumulation_order():
+    # test_collectives.py:56-65: ((1e8 + -1e8) + 1) == 1 in fp32
+    xs = [np.array([1e8], np.float32), np.array([-1e8], np.float32), np.array([1.0], np.float32)]
+    assert orc.all_reduce_exact(xs)[0] == 1.0
+
+
+def test_zero_point_clamp_quirk():
+    # codec.py:261,321 clamp z to [0, 2^b-1]: all-positive groups collapse
+    q = orc.quantize(np.array([1.0, 2.0], np.float32), orc.Codec(bits=4, group_size=2))
+    d = orc.dequantize(q)
+    assert q.codes.tolist() == [15, 15] and d[0] == d[1] and abs(d[0] - 1.0) < 1e-3
+
+
+def test_chunking_transparent():
+    # test_collectives.py:164-174 through the segment restatement
+    rng = np.random.default_rng(9)
+    xs = [rng.standard_normal(50000).astype(np.float32) for _ in range(4)]
+    c = orc.Codec(bits=4, group_size=32)
+    outs = [orc.flash_all_reduce(xs, c, c, ch).outputs[0] for ch in (128, 4 * 32 * 7, None)]
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+def test_reports_reproduced():
+    # workload.py:176-200 numbers recorded from the reference
+    rep = gio.reports()
+    for key, (half_ref, full_ref) in rep["rs_vs_ag"].items():
+        n = int(key.split("_")[0][1:])
+        bits = int(key.split("_")[1][1:])
+        xs = orc.gen_rank_activations(4096, 16, 0, n)
+        exact = orc.all_reduce_exact(xs)
+        # quirk kept: bits=6 makes stage 1 of the half run a true INT6 codec
+        # (workload.py:437), while the full run is the int4->int8 preset (:441-442)
+        half = orc.flash_all_reduce(xs, orc.Codec(bits=bits), orc.FP16).outputs[0]
+        s1 = orc.Codec(bits=4 if bits == 6 else bits)
+        s2 = orc.Codec(bits=8) if bits == 6 else s1
+        full = orc.flash_all_reduce(xs, s1, s2).outputs[0]
+        assert orc.mse(half, exact) == pytest.approx(half_ref, rel=1e-12)
+        assert orc.mse(full, exact) == pytest.approx(full_ref, rel=1e-12)
+
+
+def test_snap_scale_edges():
+    # codec.py:235-248: overflow clamps to 65504, underflow bumps to 2^-24
+    s = orc.snap_scale_f16(np.array([1e9, 1e-30, 0.0, 1.0]), 1e-8)
+    assert float(s[0]) == 65504.0
+    assert float(s[1]) == float(np.float16(2.0 ** -24))
+    assert float(s[2]) == float(np.float16(2.0 ** -24))
+    assert float(s[3]) == 1.0
