@@ -1,0 +1,417 @@
+"""Benchmark of the B200 Flash All-Reduce (BASELINE.json metric:
+"all-reduce latency & effective GB/s at TP=2/4/8 vs NCCL bf16; roofline
+fraction").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c1|c4]
+
+N=1 (the driver default): the headline workload C2 — INT4 asym g128 flash
+all-reduce of bf16 [8,1024,8192] per rank at TP=8 — with all 8 TP ranks
+emulated on one B200 (8 logical ranks, the reference's list-of-tensors call;
+peer stores land in local HBM instead of crossing NVLink). One step = one
+all-reduce of all 8 ranks' tensors = one launch of the fused persistent
+kernel. N>1 (torchrun): one rank per GPU over CUDA IPC / NVLink with
+NCCL bf16 all_reduce timed beside it.
+
+value = sum over TP ranks of the bf16 input bytes all-reduced per second
+(whole job); algbw (nccl-tests convention, e*M/t) and latency are reported
+too. Inputs (1 GiB at N=1) exceed the 126 MB L2, so no flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (tp, tokens-per-rank shape, bits, dtype)
+    "c2": dict(tp=8, shape=(8, 1024, 8192), bits=4, group=128, dtype="bf16",
+               desc="INT4 asym g128 flash all-reduce of bf16 [8,1024,8192] per rank at TP=8 (Llama-3-70B prefill)"),
+    "c1": dict(tp=4, shape=(1024, 8192), bits=8, group=128, dtype="fp16",
+               desc="INT8 asym g128 flash all-reduce of fp16 [1024,8192] per rank at TP=4"),
+    "c4": dict(tp=8, shape=(64, 8192), bits=4, group=128, dtype="bf16",
+               desc="decode: INT4 g128 flash all-reduce of bf16 [64,8192] per rank at TP=8 (latency-bound)"),
+}
+
+
+def load_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sms.append(float(parts[1]))
+                    maxes.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def wire_len(bits: int, group: int, n: int) -> int:
+    packed = (n * (4 if bits <= 4 else 8) + 7) // 8
+    return packed + (-(-n // group)) * 3
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference itself (baseline/_ref) if installed, else the oracle port
+
+
+def cpu_reference_step(tp: int, elems: int, bits: int, group: int, seed: int = 0):
+    import numpy as np
+
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    rng = np.random.default_rng(seed)
+    xs = [rng.standard_normal(elems).astype(np.float32) for _ in range(tp)]
+    if os.path.isdir(os.path.join(ref_dir, "qcollectives")):
+        sys.path.insert(0, ref_dir)
+        import qcollectives as qc  # the unmodified reference, installed offline
+
+        cfg = qc.FlashConfig.from_bits(bits, group_size=group)
+        t0 = time.perf_counter()
+        qc.flash_all_reduce(xs, cfg)
+        return time.perf_counter() - t0, "reference", tp, "qcollectives.flash_all_reduce (one Python thread per rank, GIL-bound)"
+    from oracle import flash_oracle as orc  # port (test infrastructure), only as the CPU baseline
+
+    c = orc.Codec(bits=bits, group_size=group)
+    t0 = time.perf_counter()
+    orc.flash_all_reduce(xs, c, c)
+    return time.perf_counter() - t0, "port", 1, "oracle/flash_oracle.py numpy restatement (single thread)"
+
+
+def cpu_sample_elems(cfg: dict) -> int:
+    # bounded sample: 1/64 of the C2 per-rank tensor (1,048,576 elements), ~few s of CPU
+    m = math.prod(cfg["shape"])
+    return max(cfg["tp"] * 1024, min(m, 1 << 20))
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    elems = cpu_sample_elems(cfg)
+    e = 2
+    times = []
+    kind = cores = note = None
+    for i in range(args.warmup + args.steps):
+        dt, kind, cores, note = cpu_reference_step(cfg["tp"], elems, cfg["bits"], cfg["group"], seed=i)
+        if i >= args.warmup:
+            times.append(dt)
+    t = statistics.mean(times)
+    val = cfg["tp"] * e * elems / t / 1e9
+    sample = f"{cfg['tp']} ranks x {elems} elements (fp32 arrays of bf16-sized work; {elems / math.prod(cfg['shape']):.4f} of the per-rank tensor)"
+    line = {"impl": "reference", "metric": args.metric, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "tp": cfg["tp"], "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
+                             "host_cpus": os.cpu_count(), "note": note},
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def _dtype(name):
+    import torch
+
+    return {"bf16": torch.bfloat16, "fp16": torch.float16}[name]
+
+
+def bench_local(args, cfg, peaks):
+    """N=1: all TP ranks as logical ranks of one B200."""
+    import torch
+
+    import paper_2412_04964_b200 as fc
+    from paper_2412_04964_b200 import _lib
+    from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    tp, dt = cfg["tp"], _dtype(cfg["dtype"])
+    m = math.prod(cfg["shape"])
+    e = 2
+    seg = -(-m // tp)
+    fcfg = fc.FlashConfig.from_bits(cfg["bits"], group_size=cfg["group"])
+    comm = FlashComm.local([0] * tp, slot_bytes_for(seg, fcfg.stage1_codec, fcfg.stage2_codec))
+    if args.ctas:
+        comm.set_option(_lib.OPT_CTAS, args.ctas)
+    if args.lag:
+        comm.set_option(_lib.OPT_LAG, args.lag)
+    if args.split:
+        comm.set_option(_lib.OPT_FUSED, 0)
+    g = torch.Generator(device=dev).manual_seed(1234)
+    ins = [torch.randn(m, device=dev, generator=g).to(dt) for _ in range(tp)]
+    outs = [torch.empty(m, device=dev, dtype=dt) for _ in range(tp)]
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        comm.all_reduce_local(ins, fcfg, outs=outs, check=False)
+    comm.check()
+    launches_per_step = comm.get_option(_lib.OPT_LAST_LAUNCHES)
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    t0.record(stream)
+    evs[0].record(stream)
+    for i in range(args.steps):
+        comm.all_reduce_local(ins, fcfg, outs=outs, check=False)
+        evs[i + 1].record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    comm.check()
+    total_ms = t0.elapsed_time(t1)
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    ms = total_ms / args.steps
+    # algorithmic HBM bytes of one step (all TP ranks on this GPU), SURVEY §8(d):
+    # per rank 2*e*M + 2*(N-1)*(W1(seg)+W2(seg))
+    w = wire_len(cfg["bits"], cfg["group"], seg)
+    alg_bytes = tp * (2 * e * m + 2 * (tp - 1) * 2 * w)
+    kernel_ms = total_ms / (args.steps * launches_per_step)
+    achieved = alg_bytes / launches_per_step / (kernel_ms * 1e-3) / 1e9
+    value = tp * e * m / (ms * 1e-3) / 1e9
+
+    # ---- e2e: reference-facing call with HOST buffers (pinned), H2D + D2H inside the timed region
+    host_in = [t.cpu().pin_memory() for t in ins]
+    host_out = torch.empty(m, dtype=dt).pin_memory()
+    e2e_steps = max(1, min(args.steps, 5))
+    fc.flash_all_reduce(host_in, fcfg, comm=comm)  # warm
+    torch.cuda.synchronize()
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(e2e_steps):
+        run = fc.flash_all_reduce(host_in, fcfg, comm=comm)
+        host_out.copy_(run.outputs[0], non_blocking=True)
+    a1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = a0.elapsed_time(a1) / e2e_steps
+    e2e = {"value": tp * e * m / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+           "h2d_bytes_per_step": tp * e * m, "d2h_bytes_per_step": e * m,
+           "path": "flash_all_reduce(list of pinned host bf16 tensors) -> C-ABI fc_flash_all_reduce_local -> D2H of rank 0"}
+
+    # ---- CPU baseline on the host cores (bounded sample)
+    cpu = None
+    if not args.no_cpu:
+        elems = cpu_sample_elems(cfg)
+        dts = []
+        for i in range(2):
+            d, kind, cores, note = cpu_reference_step(tp, elems, cfg["bits"], cfg["group"], seed=i)
+            dts.append(d)
+        cv = tp * e * elems / min(dts) / 1e9
+        cpu = {"value": cv, "unit": "GB/s", "cores": cores, "kind": kind, "host_cpus": os.cpu_count(),
+               "sample": f"{tp} ranks x {elems} elements per rank ({elems / m:.4f} of the per-rank tensor), best of 2",
+               "note": note, "gpu_speedup": value / cv}
+
+    traffic = None
+    tp_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp_path):
+        with open(tp_path) as fh:
+            traffic = json.load(fh).get(f"{args.config}_fused")
+    line = {
+        "metric": args.metric, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (torch.randn, seed 1234)",
+        "config": {"workload": cfg["desc"] + f"; all {tp} TP ranks emulated as logical ranks on 1 GPU",
+                   "tp": tp, "bits": cfg["bits"], "group_size": cfg["group"], "elems_per_rank": m,
+                   "value_def": "sum over TP ranks of bf16 input bytes all-reduced per second",
+                   "l2": "inputs (%.0f MiB) exceed L2; no flush" % (tp * e * m / 2**20),
+                   "mode": "split" if args.split else "fused"},
+        "latency_us": ms * 1e3, "latency_us_median": statistics.median(per) * 1e3,
+        "algbw_gbs": e * m / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "alg_bytes_per_launch": alg_bytes / launches_per_step, "kernel_ms": kernel_ms,
+                     "peak_source": peaks["source"]},
+        "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(args.steps * launches_per_step),
+        "clocks": clk, "nccl_bf16": None,
+    }
+    comm.close()
+    return line
+
+
+def bench_dist(args, cfg, peaks):
+    """N>1 under torchrun: one rank per GPU, CUDA IPC over NVLink, NCCL beside it."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2412_04964_b200 as fc
+    from paper_2412_04964_b200 import _lib
+    from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    tp, dt = world, _dtype(cfg["dtype"])
+    m = math.prod(cfg["shape"])
+    e = 2
+    seg = -(-m // tp)
+    fcfg = fc.FlashConfig.from_bits(cfg["bits"], group_size=cfg["group"])
+    comm = FlashComm.from_process_group(device=local, slot_bytes=slot_bytes_for(seg, fcfg.stage1_codec, fcfg.stage2_codec))
+    if args.ctas:
+        comm.set_option(_lib.OPT_CTAS, args.ctas)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn(m, device=dev, generator=g).to(dt)
+    out = torch.empty_like(x)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([a.elapsed_time(b) / args.steps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms = timed(lambda: comm.all_reduce(x, fcfg, out=out))
+    clk = clocks.stop()
+    comm.check()
+    launches = comm.get_option(_lib.OPT_LAST_LAUNCHES)
+    y = x.clone()
+    nccl_ms = timed(lambda: dist.all_reduce(y))
+    w = wire_len(cfg["bits"], cfg["group"], seg)
+    nvl_bytes = (tp - 1) * 2 * w
+    hbm_bytes = 2 * e * m + 2 * (tp - 1) * 2 * w
+    t_nvl, t_hbm = nvl_bytes / (NVLINK_GBS * 1e9), hbm_bytes / (peaks["hbm_gbs"] * 1e9)
+    bound = "nvlink" if t_nvl >= t_hbm else "hbm"
+    achieved = (nvl_bytes if bound == "nvlink" else hbm_bytes) / (ms * 1e-3) / 1e9
+    peak = NVLINK_GBS if bound == "nvlink" else peaks["hbm_gbs"]
+    # e2e: pinned host buffer -> device -> all-reduce -> host
+    host = x.cpu().pin_memory()
+    hout = torch.empty_like(host).pin_memory()
+
+    def e2e_step():
+        d = host.to(dev, non_blocking=True)
+        comm.all_reduce(d, fcfg, out=d)
+        hout.copy_(d, non_blocking=True)
+
+    e2e_ms = timed(e2e_step)
+    line = {
+        "metric": args.metric, "value": tp * e * m / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (torch.randn)",
+        "config": {"workload": cfg["desc"].replace("TP=8", f"TP={tp}").replace("TP=4", f"TP={tp}"), "tp": tp,
+                   "bits": cfg["bits"], "group_size": cfg["group"], "elems_per_rank": m,
+                   "parallelism": f"tp{tp} (one rank per GPU, CUDA IPC over NVLink)",
+                   "value_def": "sum over ranks of bf16 input bytes all-reduced per second"},
+        "latency_us": ms * 1e3, "algbw_gbs": e * m / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "t_roof_us": max(t_nvl, t_hbm) * 1e6},
+        "nccl_bf16": {"ms_per_step": nccl_ms, "algbw_gbs": e * m / (nccl_ms * 1e-3) / 1e9,
+                      "speedup_of_flash": nccl_ms / ms},
+        "e2e": {"value": tp * e * m / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": e * m, "d2h_bytes_per_step": e * m},
+        "gpu_launches": int(args.steps * launches), "clocks": clk, "cpu_baseline": None,
+    }
+    comm.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--lag", type=int, default=0)
+    ap.add_argument("--split", action="store_true", help="phase-split kernels instead of the fused kernel")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    args.metric = "flash all-reduce effective GB/s (sum over TP ranks), latency and roofline fraction"
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    peaks = load_peaks()
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        bench_dist(args, cfg, peaks)
+    else:
+        print(json.dumps(bench_local(args, cfg, peaks)), flush=True)
+
+
+if __name__ == "__main__":
+    main()

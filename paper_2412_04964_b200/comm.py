@@ -1,0 +1,291 @@
+"""Communicator: the B200 replacement of the reference's simulated fabric
+(/root/reference/pkg/src/qcollectives/fabric.py:111-246).
+
+A `FlashComm` owns, per rank, one device block holding N stage-1 receive
+slots, N stage-2 gather slots, per-tile arrival flags and an error word
+(layout: include/flashcomm.h, csrc/fc_flash.cuh). Peers write into it
+directly over NVLink: P2P between the GPUs of one process (`local`), or CUDA
+IPC between one process per GPU (`from_process_group`; handles are exchanged
+over torch.distributed). What the reference fabric guaranteed is kept: a
+rank that never arrives surfaces as ProtocolError naming the stuck pair
+(fabric.py:158-178, timeout default 5 s), and per-link wire bytes follow the
+reference ledger formula (collectives.py:152-157, costmodel.py:122-128).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from .codec import CodecConfig, QuantizedTensor, fc_dtype
+from .errors import ConfigError, DomainError, ProtocolError
+
+DEFAULT_TIMEOUT_S = 5.0  # fabric.py:132
+
+
+@dataclass(frozen=True)
+class FabricTopology:
+    """Signature-compatible stand-in for fabric.py:33-48 (flat homogeneous
+    topology). On B200 the link model is NVLink 5 through NVSwitch; the
+    measured topology is `FlashComm.topology()`."""
+
+    world_size: int
+    link_bandwidth: float = 900e9
+    base_latency: float = 2e-6
+    qdq_cost: float = 0.0
+
+    def __post_init__(self) -> None:
+        if int(self.world_size) < 1:
+            raise ConfigError(f"world_size must be >= 1, got {self.world_size}")
+        if not self.link_bandwidth > 0:
+            raise ConfigError("link_bandwidth must be positive")
+        if self.base_latency < 0 or self.qdq_cost < 0:
+            raise ConfigError("latencies must be nonnegative")
+
+
+@dataclass
+class TrafficLedger:
+    """Per-link byte/message counters (fabric.py:51-91). Filled analytically
+    from the call's piece layout; GPU kernels move exactly these bytes."""
+
+    bytes_sent: list
+    messages: list
+    steps: int = 0
+
+    @classmethod
+    def zeros(cls, n: int) -> "TrafficLedger":
+        return cls([[0] * n for _ in range(n)], [[0] * n for _ in range(n)])
+
+    @property
+    def world_size(self) -> int:
+        return len(self.bytes_sent)
+
+    def rank_bytes_sent(self, rank: int) -> int:
+        return sum(self.bytes_sent[rank])
+
+    def total_bytes(self) -> int:
+        return sum(map(sum, self.bytes_sent))
+
+    def to_json_dict(self) -> dict:
+        return {"bytes_sent": self.bytes_sent, "messages": self.messages, "steps": self.steps}
+
+
+def piece_layout(seg: int, piece: int):
+    """(offset, length) pieces of one rank segment (collectives.py:152-157)."""
+    off = 0
+    while off < seg:
+        yield off, min(piece, seg - off)
+        off += piece
+
+
+def flash_ledger(n_ranks: int, seg: int, piece: int, stage1: CodecConfig, stage2: CodecConfig) -> TrafficLedger:
+    """Bytes/messages each directed pair carries in flash_all_reduce: per piece
+    one stage-1 and one stage-2 message (collectives.py:359-385)."""
+    per_pair = 0
+    msgs = 0
+    for _, plen in piece_layout(seg, piece):
+        per_pair += stage1.wire_byte_len(plen) + stage2.wire_byte_len(plen)
+        msgs += 2
+    led = TrafficLedger.zeros(n_ranks)
+    for s in range(n_ranks):
+        for r in range(n_ranks):
+            if s != r:
+                led.bytes_sent[s][r] = per_pair
+                led.messages[s][r] = msgs
+    led.steps = 2
+    return led
+
+
+def slot_bytes_for(seg: int, *codecs: CodecConfig) -> int:
+    """Smallest slot capacity holding one round of a whole segment."""
+    need = 4096
+    for c in codecs:
+        need = max(need, int(c.device_layout(seg).total_bytes))
+    return int(math.ceil(need / 4096.0) * 4096)
+
+
+def exchange_handles(my_handle: bytes, group=None) -> bytes:
+    """All-gather every rank's IPC handle in rank order over torch.distributed
+    (any backend: gloo for CPU tests, nccl on the box)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    got: list = [None] * world
+    dist.all_gather_object(got, bytes(my_handle), group=group)
+    for r, h in enumerate(got):
+        if not isinstance(h, (bytes, bytearray)) or len(h) != len(my_handle):
+            raise ProtocolError(f"rank {r} sent a malformed IPC handle")
+    return b"".join(bytes(h) for h in got)
+
+
+def _device_index(d) -> int:
+    if isinstance(d, torch.device):
+        return d.index if d.index is not None else torch.cuda.current_device()
+    if isinstance(d, str):
+        return _device_index(torch.device(d))
+    return int(d)
+
+
+class FlashComm:
+    """Peer-buffer manager + topology + flag protocol (see module doc)."""
+
+    def __init__(self, handle: C.c_void_p, world: int, devices: list, rank: Optional[int], slot_bytes: int):
+        self._h = handle
+        self.world_size = world
+        self.devices = devices
+        self.rank = rank  # None for a local (one-process) communicator
+        self.slot_bytes = slot_bytes
+
+    # ---------------------------------------------------------------- creation
+    @classmethod
+    def local(cls, devices: Sequence, slot_bytes: int) -> "FlashComm":
+        devs = [_device_index(d) for d in devices]
+        n = len(devs)
+        if not 1 <= n <= _lib.FC_MAX_RANKS:
+            raise ConfigError(f"world_size must be in 1..{_lib.FC_MAX_RANKS}, got {n}")
+        arr = (C.c_int32 * n)(*devs)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().fc_comm_create_local(n, arr, int(slot_bytes), C.byref(h)))
+        return cls(h, n, devs, None, int(slot_bytes))
+
+    @classmethod
+    def from_process_group(cls, group=None, device=None, slot_bytes: int = 64 << 20) -> "FlashComm":
+        """One process per GPU (torchrun): allocate, exchange IPC handles, map peers."""
+        import torch.distributed as dist
+
+        rank = dist.get_rank(group)
+        world = dist.get_world_size(group)
+        dev = _device_index(device if device is not None else torch.cuda.current_device())
+        h = C.c_void_p()
+        _lib.check(_lib.lib().fc_comm_create_ipc(world, rank, dev, int(slot_bytes), C.byref(h)))
+        comm = cls(h, world, [dev] * world, rank, int(slot_bytes))
+        try:
+            mine = (C.c_uint8 * _lib.FC_IPC_HANDLE_BYTES)()
+            _lib.check(_lib.lib().fc_comm_ipc_handle(h, mine))
+            allh = exchange_handles(bytes(mine), group)
+            buf = (C.c_uint8 * len(allh)).from_buffer_copy(allh)
+            _lib.check(_lib.lib().fc_comm_ipc_open(h, buf))
+            dist.barrier(group)
+        except Exception:
+            comm.close()
+            raise
+        return comm
+
+    def close(self) -> None:
+        if self._h:
+            _lib.lib().fc_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- options
+    def set_option(self, option: int, value: int) -> None:
+        _lib.check(_lib.lib().fc_comm_set_option(self._h, int(option), int(value)))
+
+    def get_option(self, option: int) -> int:
+        v = C.c_int64()
+        _lib.check(_lib.lib().fc_comm_get_option(self._h, int(option), C.byref(v)))
+        return v.value
+
+    def set_timeout(self, seconds: float) -> None:
+        self.set_option(_lib.OPT_TIMEOUT_MS, max(1, int(round(seconds * 1000))))
+
+    # ---------------------------------------------------------------- calls
+    @staticmethod
+    def _cfg(cfg) -> _lib.fc_flash_cfg:
+        return _lib.fc_flash_cfg(cfg.stage1_codec.to_fc(), cfg.stage2_codec.to_fc(),
+                                 int(cfg.chunk_size) if cfg.chunk_size is not None else 0)
+
+    def all_reduce_local(self, ins: Sequence[torch.Tensor], cfg, outs: Optional[Sequence[torch.Tensor]] = None,
+                         out_dtype: Optional[torch.dtype] = None, check: bool = True) -> list:
+        """One process, all ranks: ins[r] lives on devices[r] (flat, contiguous)."""
+        if self.rank is not None:
+            raise ConfigError("all_reduce_local needs a local communicator")
+        if len(ins) != self.world_size:
+            raise ProtocolError(f"expected {self.world_size} rank tensors, got {len(ins)}")
+        n = ins[0].numel()
+        dt = ins[0].dtype
+        for r, t in enumerate(ins):
+            if t.numel() != n:
+                raise ProtocolError(f"rank {r} tensor length {t.numel()} != rank 0 length {n}")
+            if t.dtype != dt:
+                raise ProtocolError(f"rank {r} dtype {t.dtype} != rank 0 dtype {dt}")
+            if not t.is_cuda or t.device.index != self.devices[r]:
+                raise DomainError(f"rank {r} tensor must live on cuda:{self.devices[r]}")
+            if not t.is_contiguous():
+                raise DomainError(f"rank {r} tensor must be contiguous")
+        odt = out_dtype or dt
+        if outs is None:
+            outs = [torch.empty(n, dtype=odt, device=t.device) for t in ins]
+        N = self.world_size
+        pin = (C.c_void_p * N)(*[t.data_ptr() for t in ins])
+        pout = (C.c_void_p * N)(*[o.data_ptr() for o in outs])
+        pst = (C.c_void_p * N)(*[torch.cuda.current_stream(t.device).cuda_stream for t in ins])
+        c = self._cfg(cfg)
+        _lib.check(_lib.lib().fc_flash_all_reduce_local(self._h, pin, pout, n, fc_dtype(dt), fc_dtype(odt),
+                                                        C.byref(c), pst))
+        if check:
+            self.check()
+        return list(outs)
+
+    def all_reduce(self, tensor: torch.Tensor, cfg, out: Optional[torch.Tensor] = None,
+                   out_dtype: Optional[torch.dtype] = None, check: bool = False) -> torch.Tensor:
+        """Per-rank form (IPC world): every rank calls with equal numel/cfg.
+        out may be `tensor` (in place). Asynchronous unless check=True."""
+        if self.rank is None:
+            raise ConfigError("all_reduce needs an IPC communicator (from_process_group)")
+        if not tensor.is_contiguous():
+            raise DomainError("tensor must be contiguous")
+        odt = out_dtype or tensor.dtype
+        if out is None:
+            out = torch.empty_like(tensor, dtype=odt)
+        c = self._cfg(cfg)
+        st = torch.cuda.current_stream(tensor.device).cuda_stream
+        _lib.check(_lib.lib().fc_flash_all_reduce(self._h, tensor.data_ptr(), out.data_ptr(), tensor.numel(),
+                                                  fc_dtype(tensor.dtype), fc_dtype(odt), C.byref(c), st))
+        if check:
+            self.check()
+        return out
+
+    def check(self, rank: int = -1) -> None:
+        """Synchronize and raise the device-side error of `rank` (all if -1)."""
+        _lib.check(_lib.lib().fc_comm_check(self._h, int(rank)))
+
+    # ---------------------------------------------------------------- debug / parity
+    def slot(self, rank: int, stage: int, src: int, config: CodecConfig) -> QuantizedTensor:
+        """Stage-1 receive slot [src] or stage-2 gather slot [src] of `rank`
+        as a QuantizedTensor (the last round of the last call)."""
+        L = _lib.fc_layout()
+        _lib.check(_lib.lib().fc_comm_slot(self._h, rank, stage, src, None, C.byref(L)))
+        dev = torch.device("cuda", self.devices[rank] if self.rank is None else self.devices[self.rank])
+        raw = torch.empty(int(L.total_bytes), dtype=torch.uint8, device=dev)
+        _lib.check(_lib.lib().fc_comm_slot(self._h, rank, stage, src, raw.data_ptr(), C.byref(L)))
+        qt = QuantizedTensor.__new__(QuantizedTensor)
+        qt.config = config
+        qt.element_count = int(L.elements)
+        qt._buf = raw
+        qt._layout = L
+        qt.codes = raw[: L.codes_bytes]
+        qt.scales = (raw[L.scales_offset: L.scales_offset + 2 * L.groups].view(torch.float16)
+                     if not config.is_passthrough else torch.empty(0, dtype=torch.float16, device=dev))
+        qt.zeros = raw[L.zeros_offset: L.zeros_offset + L.groups] if (config.is_int and not config.symmetric) else None
+        return qt
+
+    def topology(self) -> dict:
+        N = self.world_size
+        acc = (C.c_int32 * (N * N))()
+        mc = C.c_int32()
+        _lib.check(_lib.lib().fc_comm_topology(self._h, acc, C.byref(mc)))
+        names = sorted({torch.cuda.get_device_name(d) for d in set(self.devices)})
+        return {"world_size": N, "devices": list(self.devices), "device_names": names,
+                "peer_access": [[int(acc[a * N + b]) for b in range(N)] for a in range(N)],
+                "multicast_supported": bool(mc.value), "ipc": self.rank is not None}

@@ -1,0 +1,752 @@
+// C ABI of the B200 Flash All-Reduce: codec entry points, the communicator
+// (CUDA-IPC / P2P peer-buffer manager + topology discovery) and the
+// flash_all_reduce orchestration. See include/flashcomm.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "fc_flash.cuh"
+#include "fc_host.h"
+
+namespace fc {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_launch_count = 0;  // kernels launched by the current call
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+static fc_status fail(fc_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+// codec.py:61-73
+fc_status validate_codec(const fc_codec* c) {
+  if (!c) return fail(FC_ERR_CONFIG, "codec is NULL");
+  if (c->kind == FC_KIND_FP16) return FC_OK;
+  if (c->kind != FC_KIND_INT) return fail(FC_ERR_CONFIG, "unknown codec kind %d", c->kind);
+  if (c->bits < 2 || c->bits > 8) return fail(FC_ERR_CONFIG, "bits must be in 2..8, got %d", c->bits);
+  if (c->group_size < 1) return fail(FC_ERR_CONFIG, "group_size must be >= 1");
+  if (c->rounding != FC_ROUND_NEAREST_EVEN && c->rounding != FC_ROUND_CEIL)
+    return fail(FC_ERR_CONFIG, "rounding must be one of ('nearest-even', 'ceil')");
+  if (!(c->scale_floor > 0)) return fail(FC_ERR_CONFIG, "scale_floor must be positive");
+  return FC_OK;
+}
+
+static int64_t group_of(const fc_codec& c) { return c.kind == FC_KIND_FP16 ? 1 : c.group_size; }
+
+// collectives.py:56-75
+static fc_status resolve_chunk(const fc_flash_cfg* cfg, int world, int64_t* out) {
+  const int64_t mult = std::lcm(group_of(cfg->stage1), group_of(cfg->stage2));
+  const int64_t unit = (int64_t)world * mult;
+  const int64_t dflt = 64 * 1024;
+  if (cfg->chunk_elems <= 0) {
+    *out = std::max<int64_t>(1, ceil_div(dflt, unit)) * unit;
+    return FC_OK;
+  }
+  if (cfg->chunk_elems % unit != 0)
+    return fail(FC_ERR_CONFIG, "chunk_size %lld must be a multiple of world_size*group lcm = %lld",
+                (long long)cfg->chunk_elems, (long long)unit);
+  *out = cfg->chunk_elems;
+  return FC_OK;
+}
+
+}  // namespace fc
+
+using namespace fc;
+
+// ============================================================================
+// communicator
+
+struct fc_comm {
+  int world = 0;
+  bool ipc = false;
+  int my_rank = 0;  // ipc
+  int devices[kMaxRanks] = {0};
+  int64_t slot_bytes = 0;
+  int64_t flags_cap = 0;
+  int64_t block_bytes = 0;
+  uint8_t* blk[kMaxRanks] = {nullptr};
+  bool owned[kMaxRanks] = {false};
+  bool opened[kMaxRanks] = {false};
+  float* scratch[kMaxRanks] = {nullptr};
+  int64_t scratch_elems[kMaxRanks] = {0};
+  cudaEvent_t ev[kMaxRanks] = {nullptr};
+  uint32_t epoch = 0;
+  // options
+  int64_t fused = 1, ctas = 0, timeout_ms = 5000, lag = 0, fast = 1;
+  int64_t launches = 0, last_launches = 0;  // kernels launched by the last call
+  // last call (debug export)
+  fc_codec last_c1{}, last_c2{};
+  int64_t last_R = 0, last_sub_len = 0;
+};
+
+static int64_t block_bytes_for(int world, int64_t slot_bytes, int64_t flags_cap) {
+  return blk_misc_off(world, slot_bytes, flags_cap) + kMiscBytes;
+}
+
+static fc_status comm_init_common(fc_comm* c, int world, int64_t slot_bytes) {
+  if (world < 1 || world > kMaxRanks) return fail(FC_ERR_CONFIG, "world_size must be in 1..%d, got %d", kMaxRanks, world);
+  if (slot_bytes < 4096) return fail(FC_ERR_CONFIG, "slot_bytes must be >= 4096");
+  c->world = world;
+  c->slot_bytes = align_up(slot_bytes, 256);
+  c->flags_cap = align_up(c->slot_bytes / 2048 + 16, 64);
+  c->block_bytes = block_bytes_for(world, c->slot_bytes, c->flags_cap);
+  return FC_OK;
+}
+
+static fc_status alloc_block(fc_comm* c, int r) {
+  FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+  void* p = nullptr;
+  FC_CUDA_TRY(cudaMalloc(&p, (size_t)c->block_bytes));
+  FC_CUDA_TRY(cudaMemset(p, 0, (size_t)c->block_bytes));
+  FC_CUDA_TRY(cudaDeviceSynchronize());
+  c->blk[r] = (uint8_t*)p;
+  c->owned[r] = true;
+  FC_CUDA_TRY(cudaEventCreateWithFlags(&c->ev[r], cudaEventDisableTiming));
+  return FC_OK;
+}
+
+extern "C" {
+
+const char* fc_version(void) { return "flashcomm 0.1.0 (sm_100a)"; }
+const char* fc_last_error(void) { return g_err.c_str(); }
+
+fc_status fc_codec_validate(const fc_codec* codec) { return validate_codec(codec); }
+
+fc_status fc_codec_layout(const fc_codec* codec, int64_t n, fc_layout* out) {
+  FC_TRY(validate_codec(codec));
+  if (n < 0 || !out) return fail(FC_ERR_DOMAIN, "invalid element count");
+  *out = layout_of(*codec, n);
+  return FC_OK;
+}
+
+fc_status fc_flash_resolve_chunk(const fc_flash_cfg* cfg, int32_t world, int64_t* chunk_out) {
+  if (!cfg || !chunk_out) return fail(FC_ERR_CONFIG, "NULL argument");
+  FC_TRY(validate_codec(&cfg->stage1));
+  FC_TRY(validate_codec(&cfg->stage2));
+  if (world < 1) return fail(FC_ERR_CONFIG, "world_size must be >= 1");
+  return resolve_chunk(cfg, world, chunk_out);
+}
+
+fc_status fc_quantize(const void* x, int32_t in_dtype, int64_t n, const fc_codec* codec, void* dst,
+                      uint32_t* err_word, void* stream) {
+  FC_TRY(validate_codec(codec));
+  if (!dtype_ok(in_dtype)) return fail(FC_ERR_CONFIG, "unsupported dtype %d", in_dtype);
+  if (n <= 0) return fail(FC_ERR_DOMAIN, "input tensor is empty");
+  if (!x || !dst) return fail(FC_ERR_DOMAIN, "NULL buffer");
+  return launch_quantize(x, in_dtype, n, *codec, dst, err_word, (cudaStream_t)stream, true);
+}
+
+fc_status fc_dequantize(const void* src, int64_t n, const fc_codec* codec, void* out, int32_t out_dtype,
+                        void* stream) {
+  FC_TRY(validate_codec(codec));
+  if (!dtype_ok(out_dtype)) return fail(FC_ERR_CONFIG, "unsupported dtype %d", out_dtype);
+  if (n <= 0) return fail(FC_ERR_DOMAIN, "input tensor is empty");
+  if (!src || !out) return fail(FC_ERR_DOMAIN, "NULL buffer");
+  return launch_dequantize(src, n, *codec, out, out_dtype, (cudaStream_t)stream, true);
+}
+
+static fc_status decode_err_word(uint32_t w) {
+  if (w == 0) return FC_OK;
+  const uint32_t kind = w >> 28, phase = (w >> 20) & 0xFF, peer = (w >> 10) & 0x3FF, rank = w & 0x3FF;
+  static const char* names[] = {"?", "scatter", "reduce", "gather", "barrier"};
+  if (kind == kErrNonFinite) return fail(FC_ERR_DOMAIN, "input contains NaN or infinity (rank %u)", rank);
+  if (kind == kErrTimeout)
+    return fail(FC_ERR_PROTOCOL, "deadlock: rank %u timed out waiting on rank %u (%s)", rank, peer,
+                names[phase < 5 ? phase : 0]);
+  return fail(FC_ERR_PROTOCOL, "device error word 0x%08x", w);
+}
+
+fc_status fc_error_word_check(const uint32_t* err_word, void* stream) {
+  FC_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  if (!err_word) return FC_OK;
+  uint32_t w = 0;
+  FC_CUDA_TRY(cudaMemcpy(&w, err_word, 4, cudaMemcpyDeviceToHost));
+  return decode_err_word(w);
+}
+
+fc_status fc_comm_create_local(int32_t world, const int32_t* devices, int64_t slot_bytes, fc_comm** out) {
+  if (!out || !devices) return fail(FC_ERR_CONFIG, "NULL argument");
+  fc_comm* c = new fc_comm();
+  fc_status s = comm_init_common(c, world, slot_bytes);
+  if (s != FC_OK) {
+    delete c;
+    return s;
+  }
+  c->ipc = false;
+  for (int r = 0; r < world; ++r) c->devices[r] = devices[r];
+  for (int r = 0; r < world; ++r) {
+    s = alloc_block(c, r);
+    if (s != FC_OK) {
+      fc_comm_destroy(c);
+      return s;
+    }
+  }
+  // P2P between distinct devices (NVLink through NVSwitch on one B200 box)
+  for (int a = 0; a < world; ++a)
+    for (int b = 0; b < world; ++b) {
+      if (c->devices[a] == c->devices[b]) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, c->devices[a], c->devices[b]);
+      if (!can) {
+        fc_comm_destroy(c);
+        return fail(FC_ERR_CONFIG, "device %d cannot access peer device %d", c->devices[a], c->devices[b]);
+      }
+      cudaSetDevice(c->devices[a]);
+      cudaError_t e = cudaDeviceEnablePeerAccess(c->devices[b], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        fc_comm_destroy(c);
+        return fail(FC_ERR_CUDA, "cudaDeviceEnablePeerAccess(%d->%d): %s", c->devices[a], c->devices[b],
+                    cudaGetErrorString(e));
+      }
+      cudaGetLastError();
+    }
+  *out = c;
+  return FC_OK;
+}
+
+fc_status fc_comm_create_ipc(int32_t world, int32_t rank, int32_t device, int64_t slot_bytes, fc_comm** out) {
+  if (!out) return fail(FC_ERR_CONFIG, "NULL argument");
+  if (rank < 0 || rank >= world) return fail(FC_ERR_CONFIG, "rank %d outside world of size %d", rank, world);
+  fc_comm* c = new fc_comm();
+  fc_status s = comm_init_common(c, world, slot_bytes);
+  if (s != FC_OK) {
+    delete c;
+    return s;
+  }
+  c->ipc = true;
+  c->my_rank = rank;
+  for (int r = 0; r < world; ++r) c->devices[r] = device;
+  s = alloc_block(c, rank);
+  if (s != FC_OK) {
+    fc_comm_destroy(c);
+    return s;
+  }
+  *out = c;
+  return FC_OK;
+}
+
+fc_status fc_comm_ipc_handle(fc_comm* c, void* handle_out) {
+  if (!c || !c->ipc || !handle_out) return fail(FC_ERR_CONFIG, "not an IPC communicator");
+  FC_CUDA_TRY(cudaSetDevice(c->devices[c->my_rank]));
+  cudaIpcMemHandle_t h;
+  FC_CUDA_TRY(cudaIpcGetMemHandle(&h, c->blk[c->my_rank]));
+  static_assert(sizeof(h) == FC_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &h, sizeof h);
+  return FC_OK;
+}
+
+fc_status fc_comm_ipc_open(fc_comm* c, const void* handles) {
+  if (!c || !c->ipc || !handles) return fail(FC_ERR_CONFIG, "not an IPC communicator");
+  FC_CUDA_TRY(cudaSetDevice(c->devices[c->my_rank]));
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->my_rank || c->opened[p]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, (const uint8_t*)handles + (size_t)p * FC_IPC_HANDLE_BYTES, sizeof h);
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(FC_ERR_PROTOCOL, "rank %d cannot map rank %d's buffers: %s", c->my_rank, p, cudaGetErrorString(e));
+    c->blk[p] = (uint8_t*)ptr;
+    c->opened[p] = true;
+  }
+  return FC_OK;
+}
+
+fc_status fc_comm_destroy(fc_comm* c) {
+  if (!c) return FC_OK;
+  for (int r = 0; r < kMaxRanks; ++r) {
+    if (c->owned[r] && c->blk[r]) {
+      cudaSetDevice(c->devices[r]);
+      cudaDeviceSynchronize();
+      cudaFree(c->blk[r]);
+    }
+    if (c->opened[r] && c->blk[r]) cudaIpcCloseMemHandle(c->blk[r]);
+    if (c->scratch[r]) cudaFree(c->scratch[r]);
+    if (c->ev[r]) cudaEventDestroy(c->ev[r]);
+  }
+  cudaGetLastError();
+  delete c;
+  return FC_OK;
+}
+
+fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
+  if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
+  switch (option) {
+    case FC_OPT_FUSED: c->fused = value != 0; break;
+    case FC_OPT_CTAS: c->ctas = std::max<int64_t>(0, value); break;
+    case FC_OPT_TIMEOUT_MS:
+      if (value <= 0) return fail(FC_ERR_CONFIG, "timeout must be positive");
+      c->timeout_ms = value;
+      break;
+    case FC_OPT_LAG: c->lag = std::max<int64_t>(0, value); break;
+    case FC_OPT_FAST: c->fast = value != 0; break;
+    default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
+  }
+  return FC_OK;
+}
+
+fc_status fc_comm_get_option(fc_comm* c, int32_t option, int64_t* value) {
+  if (!c || !value) return fail(FC_ERR_CONFIG, "NULL argument");
+  switch (option) {
+    case FC_OPT_FUSED: *value = c->fused; break;
+    case FC_OPT_CTAS: *value = c->ctas; break;
+    case FC_OPT_TIMEOUT_MS: *value = c->timeout_ms; break;
+    case FC_OPT_LAG: *value = c->lag; break;
+    case FC_OPT_FAST: *value = c->fast; break;
+    case FC_OPT_LAST_LAUNCHES: *value = c->last_launches; break;
+    default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
+  }
+  return FC_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// flash all-reduce orchestration
+
+namespace {
+
+struct Plan {
+  int64_t seg = 0, R = 0, rounds = 0;
+  bool fast = false;
+  fc_layout L1{}, L2{};
+};
+
+fc_status make_plan(const fc_comm* c, const fc_flash_cfg* cfg, int64_t n, bool aligned, Plan* p) {
+  const int N = c->world;
+  p->seg = ceil_div(n, N);
+  p->fast = c->fast && fast_group(cfg->stage1) && fast_group(cfg->stage2) && (p->seg % 8 == 0) && aligned;
+  int64_t unit = std::lcm(group_of(cfg->stage1), group_of(cfg->stage2));
+  if (p->fast) unit = std::lcm(unit, (int64_t)kTileElems);
+  // largest multiple of `unit` whose two slot layouts fit and whose tiles fit the flags
+  const int sbmax = std::max(storage_bits(cfg->stage1), storage_bits(cfg->stage2));
+  int64_t rmax = (c->slot_bytes * 8 / sbmax) / unit * unit;
+  while (rmax > 0 && (layout_of(cfg->stage1, rmax).total_bytes > c->slot_bytes ||
+                      layout_of(cfg->stage2, rmax).total_bytes > c->slot_bytes ||
+                      ceil_div(rmax, kTileElems) > c->flags_cap))
+    rmax -= unit;
+  if (rmax <= 0 && p->seg > 0) {
+    // a single round of the whole segment may still fit (seg < unit)
+    if (layout_of(cfg->stage1, p->seg).total_bytes <= c->slot_bytes &&
+        layout_of(cfg->stage2, p->seg).total_bytes <= c->slot_bytes && ceil_div(p->seg, kTileElems) <= c->flags_cap)
+      rmax = p->seg;
+    else
+      return fail(FC_ERR_CONFIG, "communicator slots (%lld B) too small for group lcm %lld",
+                  (long long)c->slot_bytes, (long long)unit);
+  }
+  p->R = std::min(p->seg, rmax);
+  p->rounds = ceil_div(p->seg, p->R);
+  p->L1 = layout_of(cfg->stage1, p->R);
+  p->L2 = layout_of(cfg->stage2, p->R);
+  return FC_OK;
+}
+
+uint8_t* h_recv_slot(const fc_comm* c, int owner, int src) { return c->blk[owner] + (int64_t)src * c->slot_bytes; }
+uint8_t* h_gath_slot(const fc_comm* c, int owner, int src) {
+  return c->blk[owner] + (int64_t)(c->world + src) * c->slot_bytes;
+}
+
+template <typename Tin, typename Tout>
+fc_status launch_fused(const fc_comm* c, FlashArgs a, int rank_lo, int rank_hi, int device, cudaStream_t st) {
+  auto kern = k_flash_fused<Tin, Tout>;
+  int occ = 0;
+  FC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
+  const int cap = std::max(1, occ) * num_sms(device);
+  const int nr = rank_hi - rank_lo;
+  int C = c->ctas > 0 ? (int)c->ctas : cap / nr;
+  C = std::max(1, std::min(C, cap / nr));
+  a.rank_lo = rank_lo;
+  a.rank_hi = rank_hi;
+  a.ctas_per_rank = C;
+  const int per_step = 2 * (a.world - 1) + 1;
+  a.lag = c->lag > 0 ? (int)c->lag : (C + per_step - 1) / per_step + 1;
+  void* args[] = {&a};
+  FC_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nr * C), dim3(kThreads), args, 0, st));
+  ++g_launch_count;
+  return FC_OK;
+}
+
+unsigned grid_for(int device, int64_t items) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)num_sms(device) * 8));
+}
+
+// order every rank's stream after every other rank's work so far (one process, several GPUs)
+fc_status cross_sync(fc_comm* c, cudaStream_t* st) {
+  for (int r = 0; r < c->world; ++r) {
+    FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+    FC_CUDA_TRY(cudaEventRecord(c->ev[r], st[r]));
+  }
+  for (int r = 0; r < c->world; ++r) {
+    FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+    for (int q = 0; q < c->world; ++q)
+      if (q != r) FC_CUDA_TRY(cudaStreamWaitEvent(st[r], c->ev[q], 0));
+  }
+  return FC_OK;
+}
+
+fc_status ensure_scratch(fc_comm* c, int r, int64_t elems) {
+  if (c->scratch_elems[r] >= elems) return FC_OK;
+  FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+  if (c->scratch[r]) {
+    FC_CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(c->scratch[r]);
+  }
+  FC_CUDA_TRY(cudaMalloc(&c->scratch[r], (size_t)elems * 4));
+  c->scratch_elems[r] = elems;
+  return FC_OK;
+}
+
+// generic (any group size) phases for rank r ------------------------------------
+template <typename Tin>
+fc_status gen_phase_scatter(fc_comm* c, const FlashArgs& a, int r, cudaStream_t st) {
+  const int dev = c->devices[r];
+  for (int j = 0; j < c->world; ++j) {
+    SrcSeg<Tin> src{reinterpret_cast<const Tin*>(a.in[r]), (int64_t)j * a.seg + a.sub_off, a.M};
+    uint8_t* dst = h_recv_slot(c, j, r);
+    uint32_t* ew = reinterpret_cast<uint32_t*>(c->blk[r] + blk_misc_off(c->world, c->slot_bytes, c->flags_cap));
+    if (a.c1.kind == FC_KIND_INT) {
+      k_gen_params<<<grid_for(dev, ceil_div(ceil_div(a.sub_len, a.c1.g), 256)), 256, 0, st>>>(src, a.sub_len, a.c1, dst,
+                                                                                            ew, r);
+      ++g_launch_count;
+    }
+    k_gen_codes<<<grid_for(dev, ceil_div(gen_code_units(a.c1, a.sub_len), 256)), 256, 0, st>>>(src, a.sub_len, a.c1,
+                                                                                             dst, ew, r);
+    ++g_launch_count;
+  }
+  FC_CUDA_TRY(cudaGetLastError());
+  return FC_OK;
+}
+
+fc_status gen_phase_reduce(fc_comm* c, const FlashArgs& a, int j, cudaStream_t st, int64_t L2_bytes) {
+  const int dev = c->devices[j];
+  FC_TRY(ensure_scratch(c, j, a.sub_len));
+  FC_CUDA_TRY(cudaSetDevice(dev));
+  uint32_t* ew = reinterpret_cast<uint32_t*>(c->blk[j] + blk_misc_off(c->world, c->slot_bytes, c->flags_cap));
+  k_gen_sum<<<grid_for(dev, ceil_div(a.sub_len, 256)), 256, 0, st>>>(a, j, c->scratch[j]); ++g_launch_count;
+  SrcF32 src{c->scratch[j]};
+  uint8_t* dst = h_gath_slot(c, j, j);
+  if (a.c2.kind == FC_KIND_INT) {
+    k_gen_params<<<grid_for(dev, ceil_div(ceil_div(a.sub_len, a.c2.g), 256)), 256, 0, st>>>(src, a.sub_len, a.c2, dst,
+                                                                                          ew, j);
+    ++g_launch_count;
+  }
+  k_gen_codes<<<grid_for(dev, ceil_div(gen_code_units(a.c2, a.sub_len), 256)), 256, 0, st>>>(src, a.sub_len, a.c2, dst,
+                                                                                           ew, j);
+  ++g_launch_count;
+  k_gen_bcast<<<grid_for(dev, ceil_div(L2_bytes / 16, 256)), 256, 0, st>>>(a, j, L2_bytes); ++g_launch_count;
+  FC_CUDA_TRY(cudaGetLastError());
+  return FC_OK;
+}
+
+template <typename Tout>
+fc_status gen_phase_gather(fc_comm* c, const FlashArgs& a, int r, cudaStream_t st) {
+  const int dev = c->devices[r];
+  for (int j = 0; j < c->world; ++j) {
+    k_gen_dequant<Tout><<<grid_for(dev, ceil_div(a.sub_len, 256)), 256, 0, st>>>(
+        h_gath_slot(c, r, j), a.sub_len, a.c2, reinterpret_cast<Tout*>(a.out[r]), (int64_t)j * a.seg + a.sub_off, a.M);
+    ++g_launch_count;
+  }
+  FC_CUDA_TRY(cudaGetLastError());
+  return FC_OK;
+}
+
+// IPC barrier between phases
+fc_status ipc_barrier(fc_comm* c, const FlashArgs& a, int rank, int phase, cudaStream_t st) {
+  k_barrier<<<1, 32, 0, st>>>(a, rank, phase); ++g_launch_count;
+  FC_CUDA_TRY(cudaGetLastError());
+  return FC_OK;
+}
+
+template <typename Tin, typename Tout>
+fc_status run_typed(fc_comm* c, const void* const* ins, void* const* outs, int64_t n, const fc_flash_cfg* cfg,
+                    cudaStream_t* st, int only_rank /* -1: local world */) {
+  const int N = c->world;
+  bool aligned = true;
+  for (int r = 0; r < N; ++r) {
+    if (only_rank >= 0 && r != only_rank) continue;
+    aligned &= ((uintptr_t)ins[r] % 16 == 0) && ((uintptr_t)outs[r] % 16 == 0);
+  }
+  Plan p;
+  FC_TRY(make_plan(c, cfg, n, aligned, &p));
+  g_launch_count = 0;
+  FlashArgs a{};
+  a.world = N;
+  a.M = n;
+  a.seg = p.seg;
+  a.slot_bytes = c->slot_bytes;
+  a.flags_cap = c->flags_cap;
+  a.timeout_ns = (uint64_t)c->timeout_ms * 1000000ull;
+  a.c1 = dev_codec(cfg->stage1, p.L1);
+  a.c2 = dev_codec(cfg->stage2, p.L2);
+  for (int r = 0; r < N; ++r) {
+    a.in[r] = ins[r];
+    a.out[r] = outs[r];
+    a.blk[r] = c->blk[r];
+  }
+  bool single_dev = true;
+  for (int r = 1; r < N; ++r) single_dev &= c->devices[r] == c->devices[0];
+
+  for (int64_t k = 0; k < p.rounds; ++k) {
+    a.sub_off = k * p.R;
+    a.sub_len = std::min(p.R, p.seg - a.sub_off);
+    a.tiles = (int)ceil_div(a.sub_len, kTileElems);
+    a.epoch = ++c->epoch;
+    if (only_rank >= 0) {
+      // ---------------- IPC world: this process is rank `only_rank`
+      const int r = only_rank;
+      const int dev = c->devices[r];
+      FC_CUDA_TRY(cudaSetDevice(dev));
+      cudaStream_t s = st[r];
+      if (p.fast && c->fused) {
+        FC_TRY((launch_fused<Tin, Tout>(c, a, r, r + 1, dev, s)));
+      } else if (p.fast) {
+        a.rank_lo = r;
+        a.rank_hi = r + 1;
+        k_scatter<Tin><<<grid_for(dev, (int64_t)(N - 1) * a.tiles), kThreads, 0, s>>>(a); ++g_launch_count;
+        FC_TRY(ipc_barrier(c, a, r, 0, s));
+        k_reduce<Tin, Tout><<<grid_for(dev, a.tiles), kThreads, 0, s>>>(a); ++g_launch_count;
+        FC_TRY(ipc_barrier(c, a, r, 1, s));
+        k_gather<Tout><<<grid_for(dev, (int64_t)(N - 1) * a.tiles), kThreads, 0, s>>>(a); ++g_launch_count;
+      } else {
+        FC_TRY(gen_phase_scatter<Tin>(c, a, r, s));
+        FC_TRY(ipc_barrier(c, a, r, 0, s));
+        FC_TRY(gen_phase_reduce(c, a, r, s, p.L2.total_bytes));
+        FC_TRY(ipc_barrier(c, a, r, 1, s));
+        FC_TRY(gen_phase_gather<Tout>(c, a, r, s));
+      }
+      FC_CUDA_TRY(cudaGetLastError());
+      continue;
+    }
+    // ---------------- local world: this process drives every rank
+    if (p.fast && c->fused) {
+      if (single_dev) {
+        FC_CUDA_TRY(cudaSetDevice(c->devices[0]));
+        FC_TRY((launch_fused<Tin, Tout>(c, a, 0, N, c->devices[0], st[0])));
+      } else {
+        for (int r = 0; r < N; ++r) {
+          FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+          FC_TRY((launch_fused<Tin, Tout>(c, a, r, r + 1, c->devices[r], st[r])));
+        }
+      }
+    } else if (p.fast && single_dev) {
+      const int dev = c->devices[0];
+      FC_CUDA_TRY(cudaSetDevice(dev));
+      a.rank_lo = 0;
+      a.rank_hi = N;
+      k_scatter<Tin><<<grid_for(dev, (int64_t)N * (N - 1) * a.tiles), kThreads, 0, st[0]>>>(a); ++g_launch_count;
+      k_reduce<Tin, Tout><<<grid_for(dev, (int64_t)N * a.tiles), kThreads, 0, st[0]>>>(a); ++g_launch_count;
+      k_gather<Tout><<<grid_for(dev, (int64_t)N * (N - 1) * a.tiles), kThreads, 0, st[0]>>>(a); ++g_launch_count;
+    } else if (p.fast) {
+      for (int r = 0; r < N; ++r) {
+        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+        a.rank_lo = r;
+        a.rank_hi = r + 1;
+        k_scatter<Tin><<<grid_for(c->devices[r], (int64_t)(N - 1) * a.tiles), kThreads, 0, st[r]>>>(a); ++g_launch_count;
+      }
+      FC_TRY(cross_sync(c, st));
+      for (int r = 0; r < N; ++r) {
+        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+        a.rank_lo = r;
+        a.rank_hi = r + 1;
+        k_reduce<Tin, Tout><<<grid_for(c->devices[r], a.tiles), kThreads, 0, st[r]>>>(a); ++g_launch_count;
+      }
+      FC_TRY(cross_sync(c, st));
+      for (int r = 0; r < N; ++r) {
+        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+        a.rank_lo = r;
+        a.rank_hi = r + 1;
+        k_gather<Tout><<<grid_for(c->devices[r], (int64_t)(N - 1) * a.tiles), kThreads, 0, st[r]>>>(a); ++g_launch_count;
+      }
+    } else {
+      for (int r = 0; r < N; ++r) {
+        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+        FC_TRY(gen_phase_scatter<Tin>(c, a, r, single_dev ? st[0] : st[r]));
+      }
+      if (!single_dev) FC_TRY(cross_sync(c, st));
+      for (int r = 0; r < N; ++r) {
+        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+        FC_TRY(gen_phase_reduce(c, a, r, single_dev ? st[0] : st[r], p.L2.total_bytes));
+      }
+      if (!single_dev) FC_TRY(cross_sync(c, st));
+      for (int r = 0; r < N; ++r) {
+        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+        FC_TRY(gen_phase_gather<Tout>(c, a, r, single_dev ? st[0] : st[r]));
+      }
+    }
+    FC_CUDA_TRY(cudaGetLastError());
+  }
+  c->last_launches = g_launch_count;
+  c->last_c1 = cfg->stage1;
+  c->last_c2 = cfg->stage2;
+  c->last_R = p.R;
+  c->last_sub_len = std::min(p.R, p.seg - (p.rounds - 1) * p.R);
+  return FC_OK;
+}
+
+template <typename Tin, typename Tout>
+fc_status identity_typed(const void* in, void* out, int64_t n, int device, cudaStream_t st) {
+  FC_CUDA_TRY(cudaSetDevice(device));
+  k_convert<Tin, Tout><<<grid_for(device, ceil_div(n, 256)), 256, 0, st>>>(reinterpret_cast<const Tin*>(in),
+                                                                          reinterpret_cast<Tout*>(out), n);
+  FC_CUDA_TRY(cudaGetLastError());
+  return FC_OK;
+}
+
+#define FC_DISPATCH2(IN_DT, OUT_DT, FN, ...)                                                     \
+  [&]() -> fc_status {                                                                           \
+    switch ((IN_DT) * 3 + (OUT_DT)) {                                                            \
+      case FC_DTYPE_F32 * 3 + FC_DTYPE_F32: return FN<float, float>(__VA_ARGS__);                \
+      case FC_DTYPE_F32 * 3 + FC_DTYPE_F16: return FN<float, __half>(__VA_ARGS__);               \
+      case FC_DTYPE_F32 * 3 + FC_DTYPE_BF16: return FN<float, __nv_bfloat16>(__VA_ARGS__);       \
+      case FC_DTYPE_F16 * 3 + FC_DTYPE_F32: return FN<__half, float>(__VA_ARGS__);               \
+      case FC_DTYPE_F16 * 3 + FC_DTYPE_F16: return FN<__half, __half>(__VA_ARGS__);              \
+      case FC_DTYPE_F16 * 3 + FC_DTYPE_BF16: return FN<__half, __nv_bfloat16>(__VA_ARGS__);      \
+      case FC_DTYPE_BF16 * 3 + FC_DTYPE_F32: return FN<__nv_bfloat16, float>(__VA_ARGS__);       \
+      case FC_DTYPE_BF16 * 3 + FC_DTYPE_F16: return FN<__nv_bfloat16, __half>(__VA_ARGS__);      \
+      default: return FN<__nv_bfloat16, __nv_bfloat16>(__VA_ARGS__);                              \
+    }                                                                                            \
+  }()
+
+fc_status check_call(const fc_comm* c, int64_t n, int in_dt, int out_dt, const fc_flash_cfg* cfg) {
+  if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
+  if (!cfg) return fail(FC_ERR_CONFIG, "flash method needs a FlashConfig");
+  FC_TRY(validate_codec(&cfg->stage1));
+  FC_TRY(validate_codec(&cfg->stage2));
+  if (!dtype_ok(in_dt) || !dtype_ok(out_dt)) return fail(FC_ERR_CONFIG, "unsupported dtype");
+  if (n <= 0) return fail(FC_ERR_DOMAIN, "rank tensors must be nonempty");
+  int64_t chunk = 0;
+  return resolve_chunk(cfg, c->world, &chunk);
+}
+
+}  // namespace
+
+extern "C" {
+
+fc_status fc_flash_all_reduce_local(fc_comm* c, const void* const* ins, void* const* outs, int64_t n, int32_t in_dtype,
+                                    int32_t out_dtype, const fc_flash_cfg* cfg, void* const* streams) {
+  FC_TRY(check_call(c, n, in_dtype, out_dtype, cfg));
+  if (c->ipc) return fail(FC_ERR_CONFIG, "fc_flash_all_reduce_local needs a local communicator");
+  if (!ins || !outs) return fail(FC_ERR_DOMAIN, "NULL buffer list");
+  for (int r = 0; r < c->world; ++r)
+    if (!ins[r] || !outs[r]) return fail(FC_ERR_DOMAIN, "NULL buffer for rank %d", r);
+  cudaStream_t st[kMaxRanks];
+  for (int r = 0; r < c->world; ++r) st[r] = streams ? (cudaStream_t)streams[r] : (cudaStream_t)0;
+  if (c->world == 1) return FC_DISPATCH2(in_dtype, out_dtype, identity_typed, ins[0], outs[0], n, c->devices[0], st[0]);
+  return FC_DISPATCH2(in_dtype, out_dtype, run_typed, c, ins, outs, n, cfg, st, -1);
+}
+
+fc_status fc_flash_all_reduce(fc_comm* c, const void* in, void* out, int64_t n, int32_t in_dtype, int32_t out_dtype,
+                              const fc_flash_cfg* cfg, void* stream) {
+  FC_TRY(check_call(c, n, in_dtype, out_dtype, cfg));
+  if (!c->ipc) return fail(FC_ERR_CONFIG, "fc_flash_all_reduce needs an IPC communicator");
+  if (!in || !out) return fail(FC_ERR_DOMAIN, "NULL buffer");
+  const int r = c->my_rank;
+  if (c->world == 1) return FC_DISPATCH2(in_dtype, out_dtype, identity_typed, in, out, n, c->devices[r], (cudaStream_t)stream);
+  for (int p = 0; p < c->world; ++p)
+    if (!c->blk[p]) return fail(FC_ERR_PROTOCOL, "rank %d has not mapped rank %d (call fc_comm_ipc_open)", r, p);
+  const void* ins[kMaxRanks] = {nullptr};
+  void* outs[kMaxRanks] = {nullptr};
+  cudaStream_t st[kMaxRanks] = {nullptr};
+  ins[r] = in;
+  outs[r] = out;
+  st[r] = (cudaStream_t)stream;
+  return FC_DISPATCH2(in_dtype, out_dtype, run_typed, c, ins, outs, n, cfg, st, r);
+}
+
+fc_status fc_comm_check(fc_comm* c, int32_t rank) {
+  if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
+  fc_status first = FC_OK;
+  std::string msg;
+  for (int r = 0; r < c->world; ++r) {
+    if (rank >= 0 && r != rank) continue;
+    if (c->ipc && r != c->my_rank) continue;
+    FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+    FC_CUDA_TRY(cudaDeviceSynchronize());
+    uint32_t* ew = reinterpret_cast<uint32_t*>(c->blk[r] + blk_misc_off(c->world, c->slot_bytes, c->flags_cap));
+    uint32_t w = 0;
+    FC_CUDA_TRY(cudaMemcpy(&w, ew, 4, cudaMemcpyDeviceToHost));
+    if (w) {
+      FC_CUDA_TRY(cudaMemset(ew, 0, 4));  // latch consumed; the comm stays usable
+      fc_status s = decode_err_word(w);
+      if (first == FC_OK) {
+        first = s;
+        msg = g_err;
+      }
+    }
+  }
+  if (first != FC_OK) g_err = msg;
+  return first;
+}
+
+fc_status fc_comm_slot(fc_comm* c, int32_t rank, int32_t stage, int32_t src, void* dst, fc_layout* layout) {
+  if (!c || !layout) return fail(FC_ERR_CONFIG, "NULL argument");
+  if (rank < 0 || rank >= c->world || src < 0 || src >= c->world || !c->blk[rank])
+    return fail(FC_ERR_DOMAIN, "rank/src out of range");
+  if (stage != 1 && stage != 2) return fail(FC_ERR_DOMAIN, "stage must be 1 or 2");
+  if (c->last_R <= 0) return fail(FC_ERR_PROTOCOL, "no flash_all_reduce has run on this communicator");
+  const fc_codec& cc = stage == 1 ? c->last_c1 : c->last_c2;
+  fc_layout L = layout_of(cc, c->last_R);
+  const fc_layout Ln = layout_of(cc, c->last_sub_len);
+  L.elements = Ln.elements;  // offsets follow the round capacity, counts the last round
+  L.groups = Ln.groups;
+  L.codes_bytes = Ln.codes_bytes;
+  L.wire_bytes = Ln.wire_bytes;
+  *layout = L;
+  if (dst) {
+    const uint8_t* p = stage == 1 ? h_recv_slot(c, rank, src) : h_gath_slot(c, rank, src);
+    FC_CUDA_TRY(cudaSetDevice(c->devices[c->ipc ? c->my_rank : rank]));
+    FC_CUDA_TRY(cudaDeviceSynchronize());
+    FC_CUDA_TRY(cudaMemcpy(dst, p, (size_t)L.total_bytes, cudaMemcpyDefault));
+  }
+  return FC_OK;
+}
+
+fc_status fc_comm_topology(fc_comm* c, int32_t* can_access, int32_t* multicast) {
+  if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
+  const int N = c->world;
+  if (can_access) {
+    for (int a = 0; a < N; ++a)
+      for (int b = 0; b < N; ++b) {
+        int v = 1;
+        if (c->devices[a] != c->devices[b]) cudaDeviceCanAccessPeer(&v, c->devices[a], c->devices[b]);
+        can_access[a * N + b] = v;
+      }
+  }
+  if (multicast) {
+    *multicast = 0;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &fn, cudaEnableDefault, &q) == cudaSuccess && fn &&
+        q == cudaDriverEntryPointSuccess) {
+      typedef CUresult (*GetAttr)(int*, CUdevice_attribute, CUdevice);
+      int v = 0;
+      if (((GetAttr)fn)(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, c->devices[c->ipc ? c->my_rank : 0]) ==
+          CUDA_SUCCESS)
+        *multicast = v;
+    }
+    cudaGetLastError();
+  }
+  return FC_OK;
+}
+
+}  // extern "C"

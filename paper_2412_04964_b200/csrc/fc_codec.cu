@@ -1,0 +1,131 @@
+// Single-GPU group codec kernels: quantize (codec.py:292-329) and dequantize
+// (codec.py:354-384), plus the generic (any group size) kernels that the
+// flash path reuses for group sizes outside {32, 64, 128, 256}.
+#include <algorithm>
+
+#include "fc_codec_dev.cuh"
+#include "fc_host.h"
+
+namespace fc {
+
+// --------------------------------------------------------------------------
+// fast path: one 32-element chunk per thread, groups of g/32 lanes
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_quant_fast(const T* __restrict__ x, int64_t n, DevCodec c,
+                                                         uint8_t* __restrict__ dst, uint32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t tiles = (n + kTileElems - 1) / kTileElems;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t p0 = t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+    const int nvalid = (int)max((int64_t)0, min(n - p0, (int64_t)kLaneElems));
+    float v[kLaneElems];
+    load_chunk(x, p0, n, nvalid, v);
+    LaneQuant q;
+    const bool bad = lane_quantize(c, v, nvalid, q);
+    store_lane(c, dst, p0, nvalid, q, lane);
+    if (bad && err) atomicOr(err, make_err(kErrNonFinite, 0, 0, 0));
+  }
+}
+
+template <typename To>
+__global__ void __launch_bounds__(kThreads) k_dequant_fast(const uint8_t* __restrict__ src, int64_t n, DevCodec c,
+                                                           To* __restrict__ out) {
+  const int64_t tiles = (n + kTileElems - 1) / kTileElems;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t p0 = t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+    const int nvalid = (int)max((int64_t)0, min(n - p0, (int64_t)kLaneElems));
+    if (nvalid <= 0) continue;
+    LaneCodes L;
+    load_lane(c, src, p0, L);
+    float v[kLaneElems];
+#pragma unroll
+    for (int k = 0; k < kLaneElems; ++k) v[k] = lane_value(c, L, k);
+    store_chunk(out, p0, n, nvalid, v);
+  }
+}
+
+// --------------------------------------------------------------------------
+// launchers
+
+int num_sms(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = 148;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+static int cur_sms() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return num_sms(d);
+}
+
+template <typename T>
+static void quant_generic(const T* x, int64_t n, const DevCodec& dc, uint8_t* dst, uint32_t* err, cudaStream_t st) {
+  SrcSeg<T> src{x, 0, n};
+  if (dc.kind == FC_KIND_INT) {
+    const int64_t groups = (n + dc.g - 1) / dc.g;
+    k_gen_params<<<(unsigned)((groups + 255) / 256), 256, 0, st>>>(src, n, dc, dst, err, 0u);
+  }
+  const int64_t units = gen_code_units(dc, n);
+  k_gen_codes<<<(unsigned)((units + 255) / 256), 256, 0, st>>>(src, n, dc, dst, err, 0u);
+}
+
+fc_status launch_quantize(const void* x, int in_dtype, int64_t n, const fc_codec& c, void* dst, uint32_t* err,
+                          cudaStream_t st, bool allow_fast) {
+  const fc_layout L = layout_of(c, n);
+  const DevCodec dc = dev_codec(c, L);
+  const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)dst % 16 == 0);
+  if (allow_fast && fast_group(c) && aligned) {
+    const int64_t tiles = (n + kTileElems - 1) / kTileElems;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)cur_sms() * 8);
+    uint8_t* d = (uint8_t*)dst;
+    switch (in_dtype) {
+      case FC_DTYPE_F32: k_quant_fast<float><<<grid, kThreads, 0, st>>>((const float*)x, n, dc, d, err); break;
+      case FC_DTYPE_F16: k_quant_fast<__half><<<grid, kThreads, 0, st>>>((const __half*)x, n, dc, d, err); break;
+      default: k_quant_fast<__nv_bfloat16><<<grid, kThreads, 0, st>>>((const __nv_bfloat16*)x, n, dc, d, err); break;
+    }
+  } else {
+    uint8_t* d = (uint8_t*)dst;
+    switch (in_dtype) {
+      case FC_DTYPE_F32: quant_generic((const float*)x, n, dc, d, err, st); break;
+      case FC_DTYPE_F16: quant_generic((const __half*)x, n, dc, d, err, st); break;
+      default: quant_generic((const __nv_bfloat16*)x, n, dc, d, err, st); break;
+    }
+  }
+  FC_CUDA_TRY(cudaGetLastError());
+  return FC_OK;
+}
+
+fc_status launch_dequantize(const void* src, int64_t n, const fc_codec& c, void* out, int out_dtype,
+                            cudaStream_t st, bool allow_fast) {
+  const fc_layout L = layout_of(c, n);
+  const DevCodec dc = dev_codec(c, L);
+  const uint8_t* s = (const uint8_t*)src;
+  const bool aligned = ((uintptr_t)src % 16 == 0) && ((uintptr_t)out % 16 == 0);
+  if (allow_fast && fast_group(c) && aligned) {
+    const int64_t tiles = (n + kTileElems - 1) / kTileElems;
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)cur_sms() * 8);
+    switch (out_dtype) {
+      case FC_DTYPE_F32: k_dequant_fast<float><<<grid, kThreads, 0, st>>>(s, n, dc, (float*)out); break;
+      case FC_DTYPE_F16: k_dequant_fast<__half><<<grid, kThreads, 0, st>>>(s, n, dc, (__half*)out); break;
+      default: k_dequant_fast<__nv_bfloat16><<<grid, kThreads, 0, st>>>(s, n, dc, (__nv_bfloat16*)out); break;
+    }
+  } else {
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    switch (out_dtype) {
+      case FC_DTYPE_F32: k_gen_dequant<float><<<grid, 256, 0, st>>>(s, n, dc, (float*)out, 0); break;
+      case FC_DTYPE_F16: k_gen_dequant<__half><<<grid, 256, 0, st>>>(s, n, dc, (__half*)out, 0); break;
+      default: k_gen_dequant<__nv_bfloat16><<<grid, 256, 0, st>>>(s, n, dc, (__nv_bfloat16*)out, 0); break;
+    }
+  }
+  FC_CUDA_TRY(cudaGetLastError());
+  return FC_OK;
+}
+
+}  // namespace fc

@@ -1,0 +1,345 @@
+// Flash All-Reduce device code (Alg. 1 of arXiv 2412.04964; reference
+// collectives.py:321-402), B200 form.
+//
+// Per rank r and round (a sub-range [sub_off, sub_off+sub_len) of every rank
+// segment; rounds are result-transparent, collectives.py:14-16):
+//   scatter(r->j, t): quantize tile t of r's segment j with stage 1 and store
+//                     it straight into rank j's receive slot [r] (NVLink P2P /
+//                     IPC-mapped stores), then raise rflag[j][r][t].
+//   reduce(j, t):     wait rflag[j][*][t]; dequantize the N-1 peer tiles and
+//                     QDQ the own tile in registers; fp32 sum in ascending
+//                     source rank (collectives.py:182-187); stage-2 quantize;
+//                     store to every peer's gather slot [j]; decode the own
+//                     output; raise gflag[p][j][t].
+//   gather(r, j, t):  wait gflag[r][j][t]; decode into out[j*seg + ...].
+// Own pieces never touch HBM as codes (collectives.py:364-365,378 are done in
+// registers).
+#pragma once
+
+#include "fc_codec_dev.cuh"
+
+namespace fc {
+
+struct FlashArgs {
+  int world;
+  int rank_lo, rank_hi;     // ranks handled by this launch
+  int ctas_per_rank;        // fused kernel
+  int lag;                  // fused schedule lag (steps)
+  int tiles;                // ceil(sub_len / kTileElems)
+  uint32_t epoch;
+  int64_t M;                // elements per rank (unpadded)
+  int64_t seg;              // ceil(M / world)
+  int64_t sub_off, sub_len; // this round's sub-range of every segment
+  int64_t slot_bytes;
+  int64_t flags_cap;
+  uint64_t timeout_ns;
+  DevCodec c1, c2;
+  const void* in[kMaxRanks];
+  void* out[kMaxRanks];
+  uint8_t* blk[kMaxRanks];  // every rank's block, addressable from the launching device
+};
+
+// block layout (host mirror in fc_api.cu)
+__host__ __device__ inline int64_t blk_flags_off(int world, int64_t slot_bytes) { return 2 * (int64_t)world * slot_bytes; }
+__host__ __device__ inline int64_t blk_misc_off(int world, int64_t slot_bytes, int64_t flags_cap) {
+  return blk_flags_off(world, slot_bytes) + 2 * (int64_t)world * flags_cap * 4;
+}
+constexpr int64_t kMiscBytes = 512;  // err word @0, barrier flags @64: [2][kMaxRanks] u32
+
+__device__ __forceinline__ uint8_t* recv_slot(const FlashArgs& a, int owner, int src) {
+  return a.blk[owner] + (int64_t)src * a.slot_bytes;
+}
+__device__ __forceinline__ uint8_t* gath_slot(const FlashArgs& a, int owner, int src) {
+  return a.blk[owner] + (int64_t)(a.world + src) * a.slot_bytes;
+}
+__device__ __forceinline__ uint32_t* rflag(const FlashArgs& a, int owner, int src) {
+  return reinterpret_cast<uint32_t*>(a.blk[owner] + blk_flags_off(a.world, a.slot_bytes)) + (int64_t)src * a.flags_cap;
+}
+__device__ __forceinline__ uint32_t* gflag(const FlashArgs& a, int owner, int src) {
+  return reinterpret_cast<uint32_t*>(a.blk[owner] + blk_flags_off(a.world, a.slot_bytes)) +
+         (int64_t)(a.world + src) * a.flags_cap;
+}
+__device__ __forceinline__ uint32_t* errw(const FlashArgs& a, int owner) {
+  return reinterpret_cast<uint32_t*>(a.blk[owner] + blk_misc_off(a.world, a.slot_bytes, a.flags_cap));
+}
+__device__ __forceinline__ uint32_t* barflag(const FlashArgs& a, int owner, int phase, int src) {
+  return errw(a, owner) + 16 + phase * kMaxRanks + src;
+}
+
+enum Phase : uint32_t { kPhScatter = 1, kPhReduce = 2, kPhGather = 3, kPhBarrier = 4 };
+
+__device__ __forceinline__ void lane_codes_from(const LaneQuant& q, LaneCodes& L) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) L.w[i] = q.w[i];
+  L.s = q.s;
+  L.zf = q.zf;
+}
+
+// ---------------------------------------------------------------- work items
+
+template <typename Tin>
+__device__ __forceinline__ void do_scatter(const FlashArgs& a, int r, int j, int t) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+  const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+  float v[kLaneElems];
+  load_chunk(reinterpret_cast<const Tin*>(a.in[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, v);
+  LaneQuant q;
+  const bool bad = lane_quantize(a.c1, v, nvalid, q);
+  store_lane(a.c1, recv_slot(a, j, r), p0, nvalid, q, lane);
+  if (bad) atomicOr(errw(a, r), make_err(kErrNonFinite, kPhScatter, j, r));
+}
+
+template <typename Tin, typename Tout>
+__device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+  const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+  const int64_t idx0 = (int64_t)j * a.seg + a.sub_off + p0;
+  bool bad = false;
+  float acc[kLaneElems];
+  for (int s = 0; s < a.world; ++s) {
+    LaneCodes L;
+    if (s == j) {
+      float v[kLaneElems];
+      load_chunk(reinterpret_cast<const Tin*>(a.in[j]), idx0, a.M, nvalid, v);
+      LaneQuant q;
+      bad |= lane_quantize(a.c1, v, nvalid, q);  // own piece: QDQ in registers (collectives.py:364-365)
+      lane_codes_from(q, L);
+    } else if (nvalid > 0) {
+      load_lane(a.c1, recv_slot(a, j, s), p0, L);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) L.w[i] = 0;
+      L.s = 0.0f;
+      L.zf = 0.0f;
+    }
+    if (s == 0) {
+#pragma unroll
+      for (int k = 0; k < kLaneElems; ++k) acc[k] = lane_value(a.c1, L, k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kLaneElems; ++k) acc[k] += lane_value(a.c1, L, k);
+    }
+  }
+  LaneQuant q2;
+  bad |= lane_quantize(a.c2, acc, nvalid, q2);
+  for (int pp = 1; pp < a.world; ++pp) {
+    const int p = (j + pp) % a.world;
+    store_lane(a.c2, gath_slot(a, p, j), p0, nvalid, q2, lane);
+  }
+  LaneCodes L2;
+  lane_codes_from(q2, L2);
+  float o[kLaneElems];
+#pragma unroll
+  for (int k = 0; k < kLaneElems; ++k) o[k] = lane_value(a.c2, L2, k);  // owner decodes too (collectives.py:378)
+  if (nvalid > 0) store_chunk(reinterpret_cast<Tout*>(a.out[j]), idx0, a.M, nvalid, o);
+  if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
+}
+
+template <typename Tout>
+__device__ __forceinline__ void do_gather(const FlashArgs& a, int r, int j, int t) {
+  const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+  const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+  if (nvalid <= 0) return;
+  LaneCodes L;
+  load_lane(a.c2, gath_slot(a, r, j), p0, L);
+  float o[kLaneElems];
+#pragma unroll
+  for (int k = 0; k < kLaneElems; ++k) o[k] = lane_value(a.c2, L, k);
+  store_chunk(reinterpret_cast<Tout*>(a.out[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, o);
+}
+
+// ---------------------------------------------------------------- flags
+
+// Threads [0, nflags) each wait for one flag to reach the epoch. Returns true
+// if the CTA must abort (timeout here -> error word; or an error elsewhere).
+__device__ __forceinline__ bool wait_flags(const FlashArgs& a, int rank, uint32_t* const* flags, const int* peers,
+                                           int nflags, uint32_t phase, int* s_abort) {
+  if ((int)threadIdx.x < nflags) {
+    const uint32_t* f = flags[threadIdx.x];
+    const uint64_t t0 = globaltimer();
+    volatile uint32_t* ew = errw(a, rank);
+    uint32_t spins = 0;
+    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+      if ((*ew >> 28) == kErrTimeout) {  // another CTA of this rank gave up
+        *s_abort = 1;
+        break;
+      }
+      if ((++spins & 63u) == 0 && globaltimer() - t0 > a.timeout_ns) {
+        atomicCAS(errw(a, rank), 0u, make_err(kErrTimeout, phase, peers[threadIdx.x], rank));
+        *s_abort = 1;
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  return *s_abort != 0;
+}
+
+// All threads' prior stores (incl. to peer memory) are published before the
+// flag: bar.sync orders them before thread 0's system-scope fence.
+__device__ __forceinline__ void raise_flags(uint32_t* const* flags, int nflags, uint32_t epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int i = 0; i < nflags; ++i) st_relaxed_sys(flags[i], epoch);
+  }
+}
+
+// ---------------------------------------------------------------- kernels
+
+// One persistent kernel per rank (or all ranks of one GPU in one grid):
+// item i -> CTA i % ctas_per_rank, items in increasing order. Schedule step k
+// holds P scatter items for tile k, the reduce of tile k-lag and P gathers of
+// tile k-2*lag. Every wait targets an item of a strictly earlier position, so
+// with all CTAs resident the schedule cannot deadlock.
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
+  __shared__ int s_abort;
+  __shared__ uint32_t* s_flags[kMaxRanks];
+  __shared__ int s_peers[kMaxRanks];
+  const int rank = a.rank_lo + (int)(blockIdx.x / a.ctas_per_rank);
+  const int cta = (int)(blockIdx.x % a.ctas_per_rank);
+  const int P = a.world - 1;
+  const int per_step = 2 * P + 1;
+  const int64_t total = (int64_t)(a.tiles + 2 * a.lag) * per_step;
+  if (threadIdx.x == 0) s_abort = 0;
+  __syncthreads();
+  for (int64_t i = cta; i < total; i += a.ctas_per_rank) {
+    const int64_t k = i / per_step;
+    const int slot = (int)(i % per_step);
+    if (slot < P) {
+      const int64_t t = k;
+      if (t >= a.tiles) continue;
+      const int j = (rank + 1 + slot) % a.world;
+      do_scatter<Tin>(a, rank, j, (int)t);
+      if (threadIdx.x == 0) s_flags[0] = rflag(a, j, rank) + t;
+      raise_flags(s_flags, 1, a.epoch);
+    } else if (slot == P) {
+      const int64_t t = k - a.lag;
+      if (t < 0 || t >= a.tiles) continue;
+      if (threadIdx.x < P) {
+        const int s = (rank + 1 + threadIdx.x) % a.world;
+        s_flags[threadIdx.x] = rflag(a, rank, s) + t;
+        s_peers[threadIdx.x] = s;
+      }
+      __syncthreads();
+      if (wait_flags(a, rank, s_flags, s_peers, P, kPhReduce, &s_abort)) return;
+      __syncthreads();
+      do_reduce<Tin, Tout>(a, rank, (int)t);
+      __syncthreads();
+      if (threadIdx.x < P) s_flags[threadIdx.x] = gflag(a, (rank + 1 + threadIdx.x) % a.world, rank) + t;
+      raise_flags(s_flags, P, a.epoch);
+    } else {
+      const int64_t t = k - 2 * a.lag;
+      if (t < 0 || t >= a.tiles) continue;
+      const int j = (rank + 1 + (slot - P - 1)) % a.world;
+      if (threadIdx.x == 0) {
+        s_flags[0] = gflag(a, rank, j) + t;
+        s_peers[0] = j;
+      }
+      __syncthreads();
+      if (wait_flags(a, rank, s_flags, s_peers, 1, kPhGather, &s_abort)) return;
+      do_gather<Tout>(a, rank, j, (int)t);
+    }
+    __syncthreads();
+  }
+}
+
+// Phase-split kernels (no flags): ordering comes from kernel boundaries
+// (one GPU), stream events (several GPUs, one process) or k_barrier (IPC).
+template <typename Tin>
+__global__ void __launch_bounds__(kThreads) k_scatter(FlashArgs a) {
+  const int P = a.world - 1;
+  const int64_t per_rank = (int64_t)P * a.tiles;
+  const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * per_rank;
+  for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
+    const int r = a.rank_lo + (int)(i / per_rank);
+    const int64_t rem = i % per_rank;
+    const int t = (int)(rem / P);
+    const int j = (r + 1 + (int)(rem % P)) % a.world;
+    do_scatter<Tin>(a, r, j, t);
+  }
+}
+
+template <typename Tin, typename Tout>
+__global__ void __launch_bounds__(kThreads, 2) k_reduce(FlashArgs a) {
+  const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * a.tiles;
+  for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
+    const int j = a.rank_lo + (int)(i / a.tiles);
+    do_reduce<Tin, Tout>(a, j, (int)(i % a.tiles));
+  }
+}
+
+template <typename Tout>
+__global__ void __launch_bounds__(kThreads) k_gather(FlashArgs a) {
+  const int P = a.world - 1;
+  const int64_t per_rank = (int64_t)P * a.tiles;
+  const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * per_rank;
+  for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
+    const int r = a.rank_lo + (int)(i / per_rank);
+    const int64_t rem = i % per_rank;
+    const int t = (int)(rem / P);
+    const int j = (r + 1 + (int)(rem % P)) % a.world;
+    do_gather<Tout>(a, r, j, t);
+  }
+}
+
+// Cross-process barrier between phases (IPC world, phase-split/generic):
+// one warp; lane p != rank raises barflag[p][phase][rank], then waits on its own.
+__global__ void k_barrier(FlashArgs a, int rank, int phase) {
+  const int p = threadIdx.x;
+  __threadfence_system();
+  __syncwarp();
+  if (p < a.world && p != rank) st_relaxed_sys(barflag(a, p, phase, rank), a.epoch);
+  if (p < a.world && p != rank) {
+    const uint32_t* f = barflag(a, rank, phase, p);
+    const uint64_t t0 = globaltimer();
+    volatile uint32_t* ew = errw(a, rank);
+    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+      if ((*ew >> 28) == kErrTimeout) break;
+      if (globaltimer() - t0 > a.timeout_ns) {
+        atomicCAS(errw(a, rank), 0u, make_err(kErrTimeout, kPhBarrier, p, rank));
+        break;
+      }
+      __nanosleep(100);
+    }
+  }
+  __syncwarp();
+  __threadfence_system();
+}
+
+// ---------------------------------------------------------------- generic path
+
+// scratch[i] = sum_s dequant(recv_slot[owner][s])[i], ascending s
+__global__ void k_gen_sum(FlashArgs a, int owner, float* scratch) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.sub_len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.0f;
+    for (int s = 0; s < a.world; ++s) {
+      const float d = gen_value_at(a.c1, recv_slot(a, owner, s), i);
+      acc = (s == 0) ? d : acc + d;
+    }
+    scratch[i] = acc;
+  }
+}
+
+// copy owner's own gather slot [owner] to every peer's gather slot [owner]
+__global__ void k_gen_bcast(FlashArgs a, int owner, int64_t bytes) {
+  const uint8_t* src = gath_slot(a, owner, owner);
+  const int64_t n16 = bytes / 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = ld_v4(src + 16 * i);
+    for (int pp = 1; pp < a.world; ++pp) st_v4(gath_slot(a, (owner + pp) % a.world, owner) + 16 * i, v);
+  }
+}
+
+template <typename Tin, typename Tout>
+__global__ void k_convert(const Tin* __restrict__ in, Tout* __restrict__ out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = DT<Tout>::from_f(DT<Tin>::to_f(in[i]));
+}
+
+}  // namespace fc

@@ -1,0 +1,104 @@
+// Host-side helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/flashcomm.h"
+#include "fc_common.cuh"
+
+namespace fc {
+
+void set_error(const char* fmt, ...);
+
+#define FC_CUDA_TRY(expr)                                                             \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      ::fc::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return FC_ERR_CUDA;                                                             \
+    }                                                                                 \
+  } while (0)
+
+#define FC_TRY(expr)                  \
+  do {                                \
+    fc_status s_ = (expr);            \
+    if (s_ != FC_OK) return s_;       \
+  } while (0)
+
+inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline int storage_bits(const fc_codec& c) {
+  if (c.kind == FC_KIND_FP16) return 16;
+  return c.bits <= 4 ? 4 : 8;
+}
+
+// Device layout of `n` quantized elements (see fc_layout in flashcomm.h).
+// The codes region holds whole 32-element lane chunks so vector stores of a
+// ragged tail stay inside the region.
+inline fc_layout layout_of(const fc_codec& c, int64_t n) {
+  fc_layout L{};
+  const int sb = storage_bits(c);
+  L.elements = n;
+  L.groups = (c.kind == FC_KIND_FP16) ? 0 : ceil_div(n, c.group_size);
+  L.codes_bytes = (n * sb + 7) / 8;
+  const int64_t code_cap = align_up(align_up(n, kLaneElems) * sb / 8, 16);
+  L.scales_offset = code_cap;
+  L.zeros_offset = L.scales_offset + align_up(L.groups * 2, 16);
+  const bool has_zero = c.kind == FC_KIND_INT && !c.symmetric;
+  L.total_bytes = L.zeros_offset + (has_zero ? align_up(L.groups, 16) : 0);
+  if (L.total_bytes == 0) L.total_bytes = 16;
+  const int meta = (c.kind == FC_KIND_FP16) ? 0 : (c.symmetric ? 2 : 3);
+  L.wire_bytes = L.codes_bytes + L.groups * meta;
+  return L;
+}
+
+inline bool fast_group(const fc_codec& c) {
+  if (c.kind == FC_KIND_FP16) return true;
+  return c.group_size == 32 || c.group_size == 64 || c.group_size == 128 || c.group_size == 256;
+}
+
+inline DevCodec dev_codec(const fc_codec& c, const fc_layout& L) {
+  DevCodec d{};
+  d.kind = c.kind;
+  d.bits = c.bits;
+  d.g = c.group_size;
+  d.sym = c.symmetric;
+  d.ceil_mode = c.rounding == FC_ROUND_CEIL;
+  d.sb = storage_bits(c);
+  d.lpg = (c.kind == FC_KIND_INT && fast_group(c)) ? c.group_size / kLaneElems : 1;
+  if (c.kind == FC_KIND_INT) {
+    if (c.symmetric) {
+      d.qmax_f = (float)((1 << (c.bits - 1)) - 1);
+      d.qmin_f = -(float)(1 << (c.bits - 1));
+      d.qdiv = (double)((1 << (c.bits - 1)) - 1);
+    } else {
+      d.qmax_f = (float)((1 << c.bits) - 1);
+      d.qmin_f = 0.0f;
+      d.qdiv = (double)((1 << c.bits) - 1);
+    }
+  }
+  d.floor = c.scale_floor;
+  d.scales_off = L.scales_offset;
+  d.zeros_off = L.zeros_offset;
+  return d;
+}
+
+inline int dtype_size(int dt) { return dt == FC_DTYPE_F32 ? 4 : 2; }
+inline bool dtype_ok(int dt) { return dt == FC_DTYPE_F32 || dt == FC_DTYPE_F16 || dt == FC_DTYPE_BF16; }
+
+fc_status validate_codec(const fc_codec* c);
+
+// kernels (fc_codec.cu)
+fc_status launch_quantize(const void* x, int in_dtype, int64_t n, const fc_codec& c, void* dst,
+                          uint32_t* err, cudaStream_t st, bool allow_fast);
+fc_status launch_dequantize(const void* src, int64_t n, const fc_codec& c, void* out, int out_dtype,
+                            cudaStream_t st, bool allow_fast);
+
+int num_sms(int device);
+
+}  // namespace fc

@@ -1,0 +1,218 @@
+"""GPU parity of the flash all-reduce (libflashcomm sm_100a kernels) against
+the reference's golden outputs, its own wire messages (through the oracle's
+per-slot restatement) and its reported error numbers.
+
+Several logical ranks share cuda:0 (the reference's list-of-tensors call);
+the same kernels serve one rank per GPU. Float32 outputs must equal the
+reference bit for bit; bf16/fp16 outputs equal its RNE rounding.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import flash_oracle as orc
+from tests import golden_io as gio
+
+pytestmark = pytest.mark.gpu
+
+fc = pytest.importorskip("paper_2412_04964_b200")
+from paper_2412_04964_b200 import _lib  # noqa: E402
+from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for  # noqa: E402
+
+MODES = {"fused": dict(fused=1, fast=1), "split": dict(fused=0, fast=1), "generic": dict(fused=1, fast=0)}
+
+
+def _stage(spec):
+    if spec == "fp16":
+        return fc.PASSTHROUGH_FP16
+    bits, g, sym, rnd = spec
+    return fc.CodecConfig(bits=bits, group_size=g, symmetric=sym, rounding=rnd)
+
+
+def _comm(n, seg, cfg, mode, slot_bytes=None):
+    comm = FlashComm.local([0] * n, slot_bytes or slot_bytes_for(seg, cfg.stage1_codec, cfg.stage2_codec))
+    comm.set_option(_lib.OPT_FUSED, MODES[mode]["fused"])
+    comm.set_option(_lib.OPT_FAST, MODES[mode]["fast"])
+    return comm
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("i", range(len(gio.flash_meta())))
+def test_flash_golden(i, mode):
+    meta, xs, ref_out, ref_exact = gio.flash_case(i)
+    n, m = meta["n"], meta["m"]
+    cfg = fc.FlashConfig(_stage(meta["stage1"]), _stage(meta["stage2"]), chunk_size=meta["chunk"])
+    seg = -(-m // n)
+    comm = _comm(n, seg, cfg, mode)
+    ts = [torch.from_numpy(x).cuda() for x in xs]
+    run = fc.flash_all_reduce(ts, cfg, comm=comm)
+    for o in run.outputs:
+        assert np.array_equal(_bits(o.cpu().numpy()), _bits(ref_out))
+    assert run.wire_bytes_per_rank == meta["wire_bytes_per_rank"]
+    assert run.qdq_passes == meta["qdq"] and run.reduce_elems_per_rank == meta["reduce_elems"]
+    # stage buffers: the reference's per-piece wire messages restated per slot
+    s1, s2 = gio.oracle_stage(meta["stage1"]), gio.oracle_stage(meta["stage2"])
+    res = orc.flash_all_reduce(xs, s1, s2, meta["chunk"])
+    for j in range(n):
+        for s in range(n):
+            if s != j:
+                got = comm.slot(j, 1, s, cfg.stage1_codec).to_bytes()
+                assert got == res.stage1[j][s].wire_bytes(), f"stage-1 slot {j}<-{s}"
+        p = (j + 1) % n
+        assert comm.slot(p, 2, j, cfg.stage2_codec).to_bytes() == res.stage2[j].wire_bytes(), f"stage-2 {j}"
+    comm.close()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_half_in_half_out(n, dtype):
+    m = 4 * 8192 * n + 136
+    xs = orc.gen_rank_activations(8192, -(-m // 8192), 11, n)
+    xs = [x.ravel()[:m] for x in xs]
+    ts = [torch.from_numpy(x).cuda().to(dtype) for x in xs]
+    xr = [t.float().cpu().numpy() for t in ts]
+    cfg = fc.FlashConfig.from_bits(4)
+    run = fc.flash_all_reduce(ts, cfg)
+    ref = orc.flash_all_reduce(xr, orc.Codec(bits=4), orc.Codec(bits=4)).outputs[0]
+    want = torch.from_numpy(ref).to(dtype)
+    for o in run.outputs:
+        assert o.dtype == dtype
+        assert torch.equal(o.cpu().view(torch.int16), want.view(torch.int16))
+
+
+@pytest.mark.parametrize("mode", ["fused", "split", "generic"])
+def test_many_rounds_transparent(mode):
+    # slots far smaller than a segment: the call runs in rounds; results unchanged
+    n, m = 4, 4 * 8192 * 9 + 4 * 1000
+    rng = np.random.default_rng(3)
+    xs = [orc.round_to_bf16((rng.standard_normal(m) * 2).astype(np.float32)) for _ in range(n)]
+    cfg = fc.FlashConfig.int6()
+    comm = _comm(n, 0, cfg, mode, slot_bytes=3 * 8192 + 4096)
+    ts = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in xs]
+    run = fc.flash_all_reduce(ts, cfg, comm=comm, out_dtype=torch.float32)
+    ref = orc.flash_all_reduce(xs, orc.Codec(bits=4), orc.Codec(bits=8)).outputs[0]
+    for o in run.outputs:
+        assert np.array_equal(_bits(o.cpu().numpy()), _bits(ref))
+    comm.close()
+
+
+def test_in_place_and_back_to_back():
+    n, m = 8, 8 * 8192 * 3
+    cfg = fc.FlashConfig.from_bits(4)
+    comm = _comm(n, m // n, cfg, "fused")
+    for it in range(5):
+        g = torch.Generator(device="cuda").manual_seed(it)
+        ts = [torch.randn(m, device="cuda", generator=g).to(torch.bfloat16) for _ in range(n)]
+        xr = [t.float().cpu().numpy() for t in ts]
+        ref = orc.flash_all_reduce(xr, orc.Codec(bits=4), orc.Codec(bits=4)).outputs[0]
+        outs = comm.all_reduce_local(ts, cfg, outs=ts)  # in place
+        want = torch.from_numpy(ref).to(torch.bfloat16)
+        for o in outs:
+            assert torch.equal(o.cpu().view(torch.int16), want.view(torch.int16))
+    comm.close()
+
+
+def test_decode_sizes_tp8():
+    # C4: bs x 8192 bf16 at TP=8 (1 to 8 tiles per segment)
+    cfg = fc.FlashConfig.from_bits(4)
+    for bs in (8, 16, 32, 64):
+        m = bs * 8192
+        g = torch.Generator(device="cuda").manual_seed(bs)
+        ts = [torch.randn(m, device="cuda", generator=g).to(torch.bfloat16) for _ in range(8)]
+        xr = [t.float().cpu().numpy() for t in ts]
+        ref = orc.flash_all_reduce(xr, orc.Codec(bits=4), orc.Codec(bits=4)).outputs[0]
+        run = fc.flash_all_reduce(ts, cfg, out_dtype=torch.float32)
+        assert np.array_equal(_bits(run.outputs[3].cpu().numpy()), _bits(ref))
+
+
+def test_nonfinite_raises_and_comm_recovers():
+    n, m = 4, 4 * 8192
+    cfg = fc.FlashConfig.from_bits(4)
+    comm = _comm(n, m // n, cfg, "fused")
+    ts = [torch.randn(m, device="cuda") for _ in range(n)]
+    ts[2][777] = float("inf")
+    with pytest.raises(fc.DomainError):
+        fc.flash_all_reduce(ts, cfg, comm=comm)
+    ts[2][777] = 0.0
+    xr = [t.cpu().numpy() for t in ts]
+    run = fc.flash_all_reduce(ts, cfg, comm=comm)
+    ref = orc.flash_all_reduce(xr, orc.Codec(bits=4), orc.Codec(bits=4)).outputs[0]
+    assert np.array_equal(_bits(run.outputs[0].cpu().numpy()), _bits(ref))
+    comm.close()
+
+
+def test_api_errors():
+    cfg = fc.FlashConfig.from_bits(4, group_size=128, chunk_size=128)
+    with pytest.raises(fc.ConfigError):  # test_collectives.py:176-179
+        fc.flash_all_reduce([torch.zeros(1024, device="cuda")] * 4, cfg)
+    with pytest.raises(fc.ProtocolError):
+        fc.flash_all_reduce([torch.zeros(4, device="cuda"), torch.zeros(5, device="cuda")], fc.FlashConfig.from_bits(4))
+    with pytest.raises(fc.DomainError):
+        fc.flash_all_reduce([torch.zeros(0, device="cuda")] * 2, fc.FlashConfig.from_bits(4))
+    with pytest.raises(fc.ConfigError):
+        fc.run_collective("flash", [torch.zeros(8, device="cuda")] * 2)
+    with pytest.raises(fc.ConfigError):
+        fc.flash_all_reduce([torch.zeros(8, device="cuda")] * 2, fc.FlashConfig.from_bits(4),
+                            topology=fc.FabricTopology(world_size=3))
+    x = torch.arange(10, dtype=torch.float32, device="cuda")
+    run = fc.flash_all_reduce([x], fc.FlashConfig.from_bits(4, group_size=2))
+    assert torch.equal(run.outputs[0], x) and run.qdq_passes == 0
+
+
+def test_exact_and_order():
+    xs = [torch.tensor([1e8], device="cuda"), torch.tensor([-1e8], device="cuda"), torch.tensor([1.0], device="cuda")]
+    assert float(fc.all_reduce_exact(xs).outputs[0][0]) == 1.0
+
+
+def test_baseline_mse_table():
+    # 1024x8192 outlier activations (bf16), flash vs exact fp32
+    rep = gio.reports()["baseline_mse"]
+    for n in (2, 4, 8):
+        xs = orc.gen_rank_activations(8192, 1024, 0, n)
+        ts = [torch.from_numpy(orc.round_to_bf16(x)).cuda().to(torch.bfloat16) for x in xs]
+        exact = fc.all_reduce_exact(ts).outputs[0]
+        for bits in (8, 6, 4):
+            out = fc.flash_all_reduce(ts, fc.FlashConfig.from_bits(bits), out_dtype=torch.float32).outputs[0]
+            got = fc.mse(out, exact)
+            assert got == pytest.approx(rep[f"n{n}_b{bits}"], rel=1e-6), (n, bits)
+
+
+def test_rs_vs_ag_reproduced():
+    # workload.py:176-200 on the default profile (4096 x 16)
+    rep = gio.reports()["rs_vs_ag"]
+    for key, (half_ref, full_ref) in rep.items():
+        n, bits = int(key.split("_")[0][1:]), int(key.split("_")[1][1:])
+        xs = [torch.from_numpy(x).cuda() for x in orc.gen_rank_activations(4096, 16, 0, n)]
+        exact = fc.all_reduce_exact(xs).outputs[0]
+        half = fc.flash_all_reduce(xs, fc.FlashConfig(fc.CodecConfig(bits=bits), fc.PASSTHROUGH_FP16)).outputs[0]
+        full_cfg = fc.FlashConfig.int6() if bits == 6 else fc.FlashConfig.from_bits(bits)
+        full = fc.flash_all_reduce(xs, full_cfg).outputs[0]
+        assert fc.mse(half, exact) == pytest.approx(half_ref, rel=1e-9)
+        assert fc.mse(full, exact) == pytest.approx(full_ref, rel=1e-9)
+
+
+@pytest.mark.slow
+def test_c2_full_size_segment_spot_check():
+    # C2: TP=8, INT4 g128, bf16 [8,1024,8192] per rank, all 8 ranks on one GPU.
+    n, m = 8, 8 * 1024 * 8192
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    ts = [torch.randn(m, device="cuda", generator=g).to(torch.bfloat16) for _ in range(n)]
+    cfg = fc.FlashConfig.from_bits(4)
+    run = fc.flash_all_reduce(ts, cfg)
+    seg = m // n
+    for r in range(1, n):  # every rank decodes the same stage-2 payloads
+        assert torch.equal(run.outputs[r], run.outputs[0])
+    j = 5  # segment j depends only on segment j of every rank
+    xr = [t[j * seg:(j + 1) * seg].float().cpu().numpy() for t in ts]
+    c = orc.Codec(bits=4)
+    red = orc.sequential_sum([orc.dequantize(orc.quantize(x, c)) for x in xr])
+    ref = orc.dequantize(orc.quantize(red, c))
+    want = torch.from_numpy(ref).to(torch.bfloat16)
+    assert torch.equal(run.outputs[0][j * seg:(j + 1) * seg].cpu().view(torch.int16), want.view(torch.int16))

@@ -1,0 +1,106 @@
+"""One process per rank over CUDA IPC (the torchrun path), exercised on a
+single GPU: 2-4 processes share cuda:0, map each other's blocks with
+cudaIpcOpenMemHandle and run the fused flag-synchronised kernel. Parity vs the
+oracle, plus the fault path: a rank that never arrives -> ProtocolError
+naming the stuck peer (fabric.py:158-178)."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q, mode):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    try:
+        import torch
+        import torch.distributed as dist
+
+        import paper_2412_04964_b200 as fc
+        from oracle import flash_oracle as orc
+        from paper_2412_04964_b200 import _lib
+        from paper_2412_04964_b200.comm import FlashComm
+
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        comm = FlashComm.from_process_group(device=0, slot_bytes=1 << 20)
+        comm.set_timeout(20.0)
+        if mode == "split":
+            comm.set_option(_lib.OPT_FUSED, 0)
+        if mode == "generic":
+            comm.set_option(_lib.OPT_FAST, 0)
+        m = 8192 * world * 3 + (0 if mode != "generic" else 100)
+        xs = orc.gen_rank_activations(8192, -(-m // 8192), 21, world)
+        xs = [orc.round_to_bf16(x.ravel()[:m]) for x in xs]
+        cfg = fc.FlashConfig.from_bits(4)
+        want = orc.flash_all_reduce(xs, orc.Codec(bits=4), orc.Codec(bits=4)).outputs[0]
+        for it in range(3):
+            x = torch.from_numpy(xs[rank]).cuda().to(torch.bfloat16)
+            out = comm.all_reduce(x, cfg, out_dtype=torch.float32, check=True)
+            got = out.cpu().numpy()
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), f"iteration {it}"
+        if mode == "timeout":
+            dist.barrier()
+            if rank == 0:
+                comm.set_timeout(2.0)
+                x = torch.from_numpy(xs[0]).cuda().to(torch.bfloat16)
+                comm.all_reduce(x, cfg)
+                try:
+                    comm.check()
+                    raise AssertionError("expected ProtocolError")
+                except fc.ProtocolError as e:
+                    assert "timed out waiting on rank" in str(e), str(e)
+            dist.barrier()
+        comm.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover
+        import traceback
+
+        q.put((rank, repr(e) + traceback.format_exc()[-800:]))
+
+
+def _run(world, mode):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in range(world):
+            r, v = q.get(timeout=240)
+            res[r] = v
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert res == {r: "ok" for r in range(world)}, res
+
+
+@pytest.mark.parametrize("world,mode", [(2, "fused"), (4, "fused"), (2, "split"), (3, "generic")])
+def test_ipc_parity(world, mode):
+    _run(world, mode)
+
+
+def test_ipc_timeout_names_peer():
+    _run(2, "timeout")
