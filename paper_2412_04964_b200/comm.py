@@ -101,11 +101,20 @@ def flash_ledger(n_ranks: int, seg: int, piece: int, stage1: CodecConfig, stage2
     return led
 
 
+TILE_ELEMS = 8192  # elements per CTA tile (csrc/fc_common.cuh kTileElems)
+
+
 def slot_bytes_for(seg: int, *codecs: CodecConfig) -> int:
-    """Smallest slot capacity holding one round of a whole segment."""
+    """Smallest slot capacity holding one round of a whole segment (rounds
+    are cut at multiples of the tile and of every group size)."""
+    unit = TILE_ELEMS
+    for c in codecs:
+        if not c.is_passthrough:
+            unit = math.lcm(unit, c.group_size)
+    n = -(-seg // unit) * unit
     need = 4096
     for c in codecs:
-        need = max(need, int(c.device_layout(seg).total_bytes))
+        need = max(need, int(c.device_layout(n).total_bytes))
     return int(math.ceil(need / 4096.0) * 4096)
 
 
