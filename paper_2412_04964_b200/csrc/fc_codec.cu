@@ -39,8 +39,7 @@ __global__ void __launch_bounds__(kThreads) k_dequant_fast(const uint8_t* __rest
     LaneCodes L;
     load_lane(c, src, p0, L);
     float v[kLaneElems];
-#pragma unroll
-    for (int k = 0; k < kLaneElems; ++k) v[k] = lane_value(c, L, k);
+    lane_decode<false>(c, L, v);
     store_chunk(out, p0, n, nvalid, v);
   }
 }

@@ -196,38 +196,177 @@ __device__ __forceinline__ __half snap_scale(double raw, double floor) {
 // lane quantizer: one 32-element chunk, group of `lpg` consecutive lanes.
 //
 // All 32 lanes of the warp must call this together (shuffles). Elements
-// k >= nvalid are excluded from the statistics and produce code 0.
-// Outputs: packed codes in w[] (INT4: w[0..3], INT8: w[0..7], fp16: w[0..15]),
-// the group's fp16 scale, fp32 scale and zero; returns true if a valid
-// element was non-finite.
+// k >= nvalid are excluded from the statistics and produce stored code 0.
+//
+// Per element the code is round(x / s) + z, clamped (codec.py:324), computed
+// without a divide: t = x * RN(1/s) is within a few ulps of x/s, so the
+// magic-number rounding k' = rint(t) is either right or one off; the exact
+// residual rho = x - k' * s (one FMA) decides: |rho| > s/2 means the other
+// neighbour, |rho| == s/2 is an exact tie and resolves to the even code
+// (np.round is half-to-even). Ceil mode: k' = ceil(t) corrected so that
+// -s < rho <= 0. Symmetric codes are computed in offset binary (z = 2^(b-1))
+// and XOR-ed back to two's complement, so both schemes share one decoder.
 
 struct LaneQuant {
-  uint32_t w[16];
+  uint32_t w[16];  // packed codes: INT4 w[0..3], INT8 w[0..7], fp16 bits w[0..15]
   __half s16;
-  float s;
-  float zf;   // zero point as float (0 for symmetric)
+  float s;         // scale (exact fp16 value as fp32)
+  float mz;        // decode bias 2^23 + zero (asym) or 2^23 + 2^(b-1) (sym)
+  uint32_t xr;     // per-word XOR taking stored codes to offset binary
   uint8_t z8;
 };
 
+struct LaneCodes {
+  uint32_t w[16];  // offset-binary codes (xr already applied) or fp16 bits
+  float s;
+  float mz;
+};
+
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t rep_xor(const DevCodec& c) {
+  if (!c.sym) return 0u;
+  const uint32_t h = 1u << (c.bits - 1);
+  return c.sb == 4 ? h * 0x11111111u : h * 0x01010101u;
+}
+
+// Statistics of the lane's valid elements: asym (min, max), sym (-, absmax).
+// NaN propagates; +-inf shows up as a non-finite bound.
+template <bool SYM>
+__device__ __forceinline__ void lane_stats(const float v[kLaneElems], int nvalid, float& lo, float& hi) {
+  if (nvalid == kLaneElems) {
+    float a[16], b[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float x = SYM ? fabsf(v[2 * k]) : v[2 * k];
+      const float y = SYM ? fabsf(v[2 * k + 1]) : v[2 * k + 1];
+      a[k] = fminf(x, y);
+      b[k] = fmaxf(x, y);
+    }
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+      for (int k = 0; k < w; ++k) {
+        a[k] = fminf(a[k], a[k + w]);
+        b[k] = fmaxf(b[k], b[k + w]);
+      }
+    lo = a[0];
+    hi = b[0];
+  } else {
+    lo = INFINITY;
+    hi = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < kLaneElems; ++k)
+      if (k < nvalid) {
+        const float x = SYM ? fabsf(v[k]) : v[k];
+        lo = fmin_nan(lo, x);
+        hi = fmax_nan(hi, x);
+      }
+  }
+}
+
+// Exact codes of one lane chunk (any input): k' = rint/ceil(t) from the
+// magic add, corrected by the exact residual; |t| clamped to 2^21 (codes clamp
+// far earlier); NaN input -> *nan = true. This is the slow, always-correct path.
+template <int SB, bool CEIL>
+__device__ __forceinline__ void lane_codes_exact(const float v[kLaneElems], float s, int z, int qmax, uint32_t* w,
+                                              bool* nan) {
+  const float r = __frcp_rn(s);
+  const float C0 = 12582912.0f;  // 1.5 * 2^23: y = t + C0 holds rint(t) in its low mantissa bits
+  const int hb = __float_as_int(0.5f * s);
+  const int zb = z - 0x4B400000;
+  bool anynan = false;
+#pragma unroll
+  for (int k = 0; k < kLaneElems; ++k) {
+    anynan |= v[k] != v[k];
+    const float t = fminf(fmaxf(v[k] * r, -2097152.0f), 2097152.0f);
+    const float y = CEIL ? __fadd_ru(t, C0) : __fadd_rn(t, C0);
+    const float kf = y - C0;
+    const float rho = fmaf(-kf, s, v[k]);
+    const int yi = __float_as_int(y);
+    int d;
+    if (CEIL) {
+      d = rho > 0.0f ? 1 : (rho <= -s ? -1 : 0);
+    } else {
+      const float thr = __int_as_float(hb - (yi & 1));  // s/2, or prev(s/2) when k' is odd
+      d = fabsf(rho) > thr ? (rho > 0.0f ? 1 : -1) : 0;
+    }
+    const int code = min(max(yi + zb + d, 0), qmax);
+    if (SB == 4) {
+      if ((k & 7) == 0) w[k >> 3] = 0;
+      w[k >> 3] |= (uint32_t)code << (4 * (k & 7));
+    } else {
+      if ((k & 3) == 0) w[k >> 2] = 0;
+      w[k >> 2] |= (uint32_t)code << (8 * (k & 3));
+    }
+  }
+  *nan = anynan;
+}
+
+// Fast path (nearest-even, |x/s| < 2^20): takes k' = rint(x * RN(1/s)) and
+// only checks that every residual is strictly inside (-s/2, s/2) up to one
+// ulp; any element that is not (near-tie, exact tie, NaN) sends the whole
+// lane to lane_codes_exact. Returns false in that case.
+template <int SB>
+__device__ __forceinline__ bool lane_codes_fast(const float v[kLaneElems], float s, int z, int qmax, uint32_t* w) {
+  const float r = __frcp_rn(s);
+  const float C0 = 12582912.0f;
+  const float hp = __int_as_float(__float_as_int(0.5f * s) - 1);  // prev(s/2)
+  const int zb = z - 0x4B400000;
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < kLaneElems; ++k) {
+    const float y = __fadd_rn(v[k] * r, C0);
+    const float rho = fmaf(-(y - C0), s, v[k]);
+    ok &= fabsf(rho) < hp;  // false for NaN too
+    const int code = min(max(__float_as_int(y) + zb, 0), qmax);
+    if (SB == 4) {
+      if ((k & 7) == 0) w[k >> 3] = 0;
+      w[k >> 3] |= (uint32_t)code << (4 * (k & 7));
+    } else {
+      if ((k & 3) == 0) w[k >> 2] = 0;
+      w[k >> 2] |= (uint32_t)code << (8 * (k & 3));
+    }
+  }
+  return ok;
+}
+
+template <int SB>
+__device__ __forceinline__ bool lane_codes_any(const float v[kLaneElems], float s, int z, int qmax, bool ceil_mode,
+                                               bool wide, uint32_t* w) {
+  bool nan = false;
+  if (ceil_mode) {
+    lane_codes_exact<SB, true>(v, s, z, qmax, w, &nan);
+  } else if (wide || !lane_codes_fast<SB>(v, s, z, qmax, w)) {
+    lane_codes_exact<SB, false>(v, s, z, qmax, w, &nan);
+  }
+  return nan;
+}
+
 __device__ __forceinline__ float group_allreduce_min(float v, int lpg) {
-  for (int o = 1; o < lpg; o <<= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 1; o < lpg; o <<= 1) v = fmin_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 __device__ __forceinline__ float group_allreduce_max(float v, int lpg) {
-  for (int o = 1; o < lpg; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 1; o < lpg; o <<= 1) v = fmax_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
+// returns true if a valid element of the lane's group is NaN/inf (codec.py:230-231)
 __device__ __forceinline__ bool lane_quantize(const DevCodec& c, const float v[kLaneElems], int nvalid,
                                               LaneQuant& q) {
-  // non-finite detection: x*0 is NaN iff x is inf/NaN
-  float probe = 0.0f;
-#pragma unroll
-  for (int k = 0; k < kLaneElems; ++k)
-    if (k < nvalid) probe = fmaf(v[k], 0.0f, probe);
-  const bool bad = probe != probe;
-
   if (c.kind == FC_KIND_FP16) {
+    float lo, hi;
+    lane_stats<true>(v, nvalid, lo, hi);
 #pragma unroll
     for (int k = 0; k < kLaneElems; k += 2) {
       __half2 h = __floats2half2_rn(k < nvalid ? v[k] : 0.0f, k + 1 < nvalid ? v[k + 1] : 0.0f);
@@ -235,50 +374,59 @@ __device__ __forceinline__ bool lane_quantize(const DevCodec& c, const float v[k
     }
     q.s16 = __ushort_as_half(0);
     q.s = 1.0f;
-    q.zf = 0.0f;
+    q.mz = 0.0f;
+    q.xr = 0u;
     q.z8 = 0;
-    return bad;
+    return nvalid > 0 && !(hi <= 3.402823466e38f);
   }
-
-  float lo = INFINITY, hi = -INFINITY;
+  float lo, hi;
   if (c.sym) {
-#pragma unroll
-    for (int k = 0; k < kLaneElems; ++k)
-      if (k < nvalid) hi = fmaxf(hi, fabsf(v[k]));
+    lane_stats<true>(v, nvalid, lo, hi);
     hi = group_allreduce_max(hi, c.lpg);
-    q.s16 = snap_scale((double)hi / c.qdiv, c.floor);
-    q.zf = 0.0f;
-    q.z8 = 0;
+    lo = -hi;
   } else {
-#pragma unroll
-    for (int k = 0; k < kLaneElems; ++k)
-      if (k < nvalid) {
-        lo = fminf(lo, v[k]);
-        hi = fmaxf(hi, v[k]);
-      }
+    lane_stats<false>(v, nvalid, lo, hi);
     lo = group_allreduce_min(lo, c.lpg);
     hi = group_allreduce_max(hi, c.lpg);
+  }
+  bool bad = nvalid > 0 && !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
+  int z;
+  if (c.sym) {
+    q.s16 = snap_scale((double)hi / c.qdiv, c.floor);
+    z = 1 << (c.bits - 1);
+    q.z8 = 0;
+  } else {
     q.s16 = snap_scale(((double)hi - (double)lo) / c.qdiv, c.floor);
-    double z = ceil(-(double)lo / (double)__half2float(q.s16));
-    z = fmin(fmax(z, 0.0), (double)c.qmax_f);
-    q.zf = (float)z;
-    q.z8 = (uint8_t)(int)z;
+    double zd = ceil(-(double)lo / (double)__half2float(q.s16));
+    zd = fmin(fmax(zd, 0.0), (double)c.qmax_f);
+    z = (int)zd;
+    q.z8 = (uint8_t)z;
   }
   q.s = __half2float(q.s16);
-
-  const uint32_t mask = (1u << c.bits) - 1u;
+  q.mz = 8388608.0f + (float)z;
+  q.xr = rep_xor(c);
+  const int qmax = (1 << c.bits) - 1;
+  const bool wide = !(fmaxf(fabsf(lo), fabsf(hi)) * __frcp_rn(q.s) < 1048576.0f);
+  bool nan;
+  if (c.sb == 4)
+    nan = lane_codes_any<4>(v, q.s, z, qmax, c.ceil_mode, wide, q.w);
+  else
+    nan = lane_codes_any<8>(v, q.s, z, qmax, c.ceil_mode, wide, q.w);
+  bad |= nan && nvalid > 0;
+  const int nw = c.sb == 4 ? 4 : 8;
 #pragma unroll
-  for (int k = 0; k < kLaneElems; ++k) {
-    float t = __fdiv_rn(v[k], q.s);
-    t = c.ceil_mode ? ceilf(t) : rintf(t);
-    t = fminf(fmaxf(t + q.zf, c.qmin_f), c.qmax_f);
-    uint32_t code = (k < nvalid) ? ((uint32_t)(int)t & mask) : 0u;
-    if (c.sb == 4) {
-      if ((k & 7) == 0) q.w[k >> 3] = 0;
-      q.w[k >> 3] |= code << (4 * (k & 7));
-    } else {
-      if ((k & 3) == 0) q.w[k >> 2] = 0;
-      q.w[k >> 2] |= code << (8 * (k & 3));
+  for (int i = 0; i < 8; ++i)
+    if (i < nw) q.w[i] ^= q.xr;  // offset binary -> stored (two's complement for sym)
+  if (nvalid < kLaneElems) {     // stored code 0 past the end of the range
+    const int per = 32 / c.sb;   // codes per word
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int first = i * per;
+      if (i < nw && first + per > nvalid) {
+        const int keep = max(0, nvalid - first);
+        const uint32_t m = keep >= per ? 0xFFFFFFFFu : ((1u << (keep * c.sb)) - 1u);
+        q.w[i] &= m;
+      }
     }
   }
   return bad;
@@ -297,7 +445,7 @@ __device__ __forceinline__ void store_lane(const DevCodec& c, uint8_t* buf, int6
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     if (i < nq) st_v4(cp + 16 * i, make_uint4(q.w[4 * i], q.w[4 * i + 1], q.w[4 * i + 2], q.w[4 * i + 3]));
-  if (c.kind == FC_KIND_INT && nvalid > 0 && (lane % c.lpg) == 0) {
+  if (c.kind == FC_KIND_INT && (lane % c.lpg) == 0) {
     int64_t grp = p0 / c.g;
     reinterpret_cast<__half*>(buf + c.scales_off)[grp] = q.s16;
     if (!c.sym) buf[c.zeros_off + grp] = q.z8;
@@ -306,14 +454,13 @@ __device__ __forceinline__ void store_lane(const DevCodec& c, uint8_t* buf, int6
 
 // Decode helpers ------------------------------------------------------------
 
-// float(code) via the 2^23 magic: exact for 0 <= c < 2^23 (LOP3 + FADD)
-__device__ __forceinline__ float u2f_magic(uint32_t c) { return __uint_as_float(0x4B000000u | c) - 8388608.0f; }
-
-struct LaneCodes {
-  uint32_t w[16];
-  float s;
-  float zf;
-};
+// in-register codes of a freshly quantized lane, in offset binary
+__device__ __forceinline__ void lane_codes_from(const DevCodec& c, const LaneQuant& q, LaneCodes& L) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) L.w[i] = (c.kind == FC_KIND_INT && i < 8) ? (q.w[i] ^ q.xr) : q.w[i];
+  L.s = q.s;
+  L.mz = q.mz;
+}
 
 __device__ __forceinline__ void load_lane(const DevCodec& c, const uint8_t* buf, int64_t p0, LaneCodes& L) {
   const uint8_t* cp = buf + p0 * c.sb / 8;
@@ -328,30 +475,69 @@ __device__ __forceinline__ void load_lane(const DevCodec& c, const uint8_t* buf,
     L.w[4 * i + 3] = u.w;
   }
   if (c.kind == FC_KIND_INT) {
-    int64_t grp = p0 / c.g;
+    const int64_t grp = p0 / c.g;
     L.s = __half2float(__ldcg(reinterpret_cast<const __half*>(buf + c.scales_off) + grp));
-    L.zf = c.sym ? 0.0f : (float)__ldcg(buf + c.zeros_off + grp);
+    const uint32_t xr = rep_xor(c);
+    L.mz = 8388608.0f + (c.sym ? (float)(1 << (c.bits - 1)) : (float)__ldcg(buf + c.zeros_off + grp));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) L.w[i] ^= xr;
   } else {
     L.s = 1.0f;
-    L.zf = 0.0f;
+    L.mz = 0.0f;
   }
 }
 
-// element k of a loaded lane: (c - z) * s (asym), signext(c) * s (sym), fp16 value
-__device__ __forceinline__ float lane_value(const DevCodec& c, const LaneCodes& L, int k) {
+// magic(c) = 2^23 + c as fp32 bits, from byte `b` of word `w`
+__device__ __forceinline__ float magic_byte(uint32_t w, int b) {
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | (uint32_t)b));
+}
+
+// out[k] = (c_k - z) * s, exact in fp32 (codec.py:383-384); fp16 kind: value
+// ACC: out[k] += that value with one rounding (fp32 sum, collectives.py:186)
+template <bool ACC>
+__device__ __forceinline__ void lane_decode(const DevCodec& c, const LaneCodes& L, float out[kLaneElems]) {
   if (c.kind == FC_KIND_FP16) {
-    uint32_t h = (L.w[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
-    return __half2float(__ushort_as_half((unsigned short)h));
+#pragma unroll
+    for (int k = 0; k < kLaneElems; k += 2) {
+      __half2 h = *reinterpret_cast<const __half2*>(&L.w[k / 2]);
+      const float2 f = __half22float2(h);
+      if (ACC) {
+        out[k] += f.x;
+        out[k + 1] += f.y;
+      } else {
+        out[k] = f.x;
+        out[k + 1] = f.y;
+      }
+    }
+    return;
   }
-  uint32_t code = (c.sb == 4) ? (L.w[k >> 3] >> (4 * (k & 7))) & 0xFu : (L.w[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-  float cf;
-  if (c.sym) {
-    int sh = 32 - c.bits;
-    cf = (float)(((int)(code << sh)) >> sh);
+  if (c.sb == 4) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t lo = L.w[i] & 0x0F0F0F0Fu, hi = (L.w[i] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float d0 = magic_byte(lo, b) - L.mz, d1 = magic_byte(hi, b) - L.mz;
+        const int k = 8 * i + 2 * b;
+        if (ACC) {
+          out[k] = fmaf(d0, L.s, out[k]);
+          out[k + 1] = fmaf(d1, L.s, out[k + 1]);
+        } else {
+          out[k] = d0 * L.s;
+          out[k + 1] = d1 * L.s;
+        }
+      }
+    }
   } else {
-    cf = u2f_magic(code);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float d = magic_byte(L.w[i], b) - L.mz;
+        const int k = 4 * i + b;
+        out[k] = ACC ? fmaf(d, L.s, out[k]) : d * L.s;
+      }
   }
-  return (cf - L.zf) * L.s;
 }
 
 // --------------------------------------------------------------------------

@@ -68,13 +68,6 @@ __device__ __forceinline__ uint32_t* barflag(const FlashArgs& a, int owner, int 
 
 enum Phase : uint32_t { kPhScatter = 1, kPhReduce = 2, kPhGather = 3, kPhBarrier = 4 };
 
-__device__ __forceinline__ void lane_codes_from(const LaneQuant& q, LaneCodes& L) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) L.w[i] = q.w[i];
-  L.s = q.s;
-  L.zf = q.zf;
-}
-
 // ---------------------------------------------------------------- work items
 
 template <typename Tin>
@@ -105,22 +98,19 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
       load_chunk(reinterpret_cast<const Tin*>(a.in[j]), idx0, a.M, nvalid, v);
       LaneQuant q;
       bad |= lane_quantize(a.c1, v, nvalid, q);  // own piece: QDQ in registers (collectives.py:364-365)
-      lane_codes_from(q, L);
+      lane_codes_from(a.c1, q, L);
     } else if (nvalid > 0) {
       load_lane(a.c1, recv_slot(a, j, s), p0, L);
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i) L.w[i] = 0;
       L.s = 0.0f;
-      L.zf = 0.0f;
+      L.mz = 0.0f;
     }
-    if (s == 0) {
-#pragma unroll
-      for (int k = 0; k < kLaneElems; ++k) acc[k] = lane_value(a.c1, L, k);
-    } else {
-#pragma unroll
-      for (int k = 0; k < kLaneElems; ++k) acc[k] += lane_value(a.c1, L, k);
-    }
+    if (s == 0)
+      lane_decode<false>(a.c1, L, acc);  // ascending source rank (collectives.py:182-187)
+    else
+      lane_decode<true>(a.c1, L, acc);
   }
   LaneQuant q2;
   bad |= lane_quantize(a.c2, acc, nvalid, q2);
@@ -129,10 +119,9 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
     store_lane(a.c2, gath_slot(a, p, j), p0, nvalid, q2, lane);
   }
   LaneCodes L2;
-  lane_codes_from(q2, L2);
+  lane_codes_from(a.c2, q2, L2);
   float o[kLaneElems];
-#pragma unroll
-  for (int k = 0; k < kLaneElems; ++k) o[k] = lane_value(a.c2, L2, k);  // owner decodes too (collectives.py:378)
+  lane_decode<false>(a.c2, L2, o);  // owner decodes its own payload too (collectives.py:378)
   if (nvalid > 0) store_chunk(reinterpret_cast<Tout*>(a.out[j]), idx0, a.M, nvalid, o);
   if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
 }
@@ -145,8 +134,7 @@ __device__ __forceinline__ void do_gather(const FlashArgs& a, int r, int j, int 
   LaneCodes L;
   load_lane(a.c2, gath_slot(a, r, j), p0, L);
   float o[kLaneElems];
-#pragma unroll
-  for (int k = 0; k < kLaneElems; ++k) o[k] = lane_value(a.c2, L, k);
+  lane_decode<false>(a.c2, L, o);
   store_chunk(reinterpret_cast<Tout*>(a.out[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, o);
 }
 
