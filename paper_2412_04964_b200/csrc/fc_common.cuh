@@ -275,14 +275,18 @@ __device__ __forceinline__ void lane_stats(const float v[kLaneElems], int nvalid
 }
 
 // Exact codes of one lane chunk (any input): k' = rint/ceil(t) from the
-// magic add, corrected by the exact residual; |t| clamped to 2^21 (codes clamp
-// far earlier); NaN input -> *nan = true. This is the slow, always-correct path.
+// magic add, then corrected with sign tests of exact residuals — an FMA
+// rounds x - m*s once, so its sign (and whether it is zero) is exact for any
+// m of at most 24 bits:
+//   nearest: up   iff x - (k'+1/2)s > 0, or == 0 with k' odd (ties to even)
+//            down iff x - (k'-1/2)s < 0, or == 0 with k' odd
+//   ceil:    up   iff x - k's > 0;  down iff x - (k'-1)s <= 0
+// |t| is clamped to 2^21 first (codes clamp far earlier). NaN -> *nan.
 template <int SB, bool CEIL>
 __device__ __forceinline__ void lane_codes_exact(const float v[kLaneElems], float s, int z, int qmax, uint32_t* w,
-                                              bool* nan) {
+                                                 bool* nan) {
   const float r = __frcp_rn(s);
   const float C0 = 12582912.0f;  // 1.5 * 2^23: y = t + C0 holds rint(t) in its low mantissa bits
-  const int hb = __float_as_int(0.5f * s);
   const int zb = z - 0x4B400000;
   bool anynan = false;
 #pragma unroll
@@ -291,14 +295,17 @@ __device__ __forceinline__ void lane_codes_exact(const float v[kLaneElems], floa
     const float t = fminf(fmaxf(v[k] * r, -2097152.0f), 2097152.0f);
     const float y = CEIL ? __fadd_ru(t, C0) : __fadd_rn(t, C0);
     const float kf = y - C0;
-    const float rho = fmaf(-kf, s, v[k]);
     const int yi = __float_as_int(y);
     int d;
     if (CEIL) {
-      d = rho > 0.0f ? 1 : (rho <= -s ? -1 : 0);
+      const float up = fmaf(-kf, s, v[k]);
+      const float dn = fmaf(-(kf - 1.0f), s, v[k]);
+      d = up > 0.0f ? 1 : (dn <= 0.0f ? -1 : 0);
     } else {
-      const float thr = __int_as_float(hb - (yi & 1));  // s/2, or prev(s/2) when k' is odd
-      d = fabsf(rho) > thr ? (rho > 0.0f ? 1 : -1) : 0;
+      const bool odd = (yi & 1) != 0;
+      const float up = fmaf(-(kf + 0.5f), s, v[k]);
+      const float dn = fmaf(-(kf - 0.5f), s, v[k]);
+      d = (up > 0.0f || (up == 0.0f && odd)) ? 1 : ((dn < 0.0f || (dn == 0.0f && odd)) ? -1 : 0);
     }
     const int code = min(max(yi + zb + d, 0), qmax);
     if (SB == 4) {
