@@ -319,22 +319,31 @@ __device__ __forceinline__ void lane_codes_exact(const float v[kLaneElems], floa
   *nan = anynan;
 }
 
-// Fast path (nearest-even, |x/s| < 2^20): takes k' = rint(x * RN(1/s)) and
-// only checks that every residual is strictly inside (-s/2, s/2) up to one
-// ulp; any element that is not (near-tie, exact tie, NaN) sends the whole
-// lane to lane_codes_exact. Returns false in that case.
-template <int SB>
+// Fast path (|x/s| < 2^20). One Newton step on the quotient,
+// q1 = t + RN(1/s) * (x - t*s) with t = x * RN(1/s), is x/s exactly whenever
+// x/s is representable — in particular at exact ties (k + 1/2) and exact
+// integers, which bf16 inputs hit often — so the magic-add rounding
+// (ties-to-even / ceil) is right there. The exact residual rho = x - k*s then
+// certifies every element: nearest needs |rho| <= s/2, ceil needs
+// -s < rho <= 0. A lane with any uncertified element (a near-tie a few ulps
+// off, NaN) returns false and is redone by lane_codes_exact.
+template <int SB, bool CEIL>
 __device__ __forceinline__ bool lane_codes_fast(const float v[kLaneElems], float s, int z, int qmax, uint32_t* w) {
   const float r = __frcp_rn(s);
   const float C0 = 12582912.0f;
-  const float hp = __int_as_float(__float_as_int(0.5f * s) - 1);  // prev(s/2)
+  const float h = 0.5f * s;
   const int zb = z - 0x4B400000;
   bool ok = true;
 #pragma unroll
   for (int k = 0; k < kLaneElems; ++k) {
-    const float y = __fadd_rn(v[k] * r, C0);
+    const float t = v[k] * r;
+    const float q1 = fmaf(fmaf(-t, s, v[k]), r, t);
+    const float y = CEIL ? __fadd_ru(q1, C0) : __fadd_rn(q1, C0);
     const float rho = fmaf(-(y - C0), s, v[k]);
-    ok &= fabsf(rho) < hp;  // false for NaN too
+    if (CEIL)
+      ok &= (rho <= 0.0f) & (rho > -s);
+    else
+      ok &= fabsf(rho) <= h;  // false for NaN
     const int code = min(max(__float_as_int(y) + zb, 0), qmax);
     if (SB == 4) {
       if ((k & 7) == 0) w[k >> 3] = 0;
@@ -352,9 +361,9 @@ __device__ __forceinline__ bool lane_codes_any(const float v[kLaneElems], float 
                                                bool wide, uint32_t* w) {
   bool nan = false;
   if (ceil_mode) {
-    lane_codes_exact<SB, true>(v, s, z, qmax, w, &nan);
-  } else if (wide || !lane_codes_fast<SB>(v, s, z, qmax, w)) {
-    lane_codes_exact<SB, false>(v, s, z, qmax, w, &nan);
+    if (wide || !lane_codes_fast<SB, true>(v, s, z, qmax, w)) lane_codes_exact<SB, true>(v, s, z, qmax, w, &nan);
+  } else {
+    if (wide || !lane_codes_fast<SB, false>(v, s, z, qmax, w)) lane_codes_exact<SB, false>(v, s, z, qmax, w, &nan);
   }
   return nan;
 }
