@@ -203,6 +203,8 @@ def bench_local(args, cfg, peaks):
         comm.set_option(_lib.OPT_LAG, args.lag)
     if args.split:
         comm.set_option(_lib.OPT_FUSED, 0)
+    if args.fused:
+        comm.set_option(_lib.OPT_FUSED, 1)
     g = torch.Generator(device=dev).manual_seed(1234)
     ins = [torch.randn(m, device=dev, generator=g).to(dt) for _ in range(tp)]
     outs = [torch.empty(m, device=dev, dtype=dt) for _ in range(tp)]
@@ -282,7 +284,7 @@ def bench_local(args, cfg, peaks):
                    "tp": tp, "bits": cfg["bits"], "group_size": cfg["group"], "elems_per_rank": m,
                    "value_def": "sum over TP ranks of bf16 input bytes all-reduced per second",
                    "l2": "inputs (%.0f MiB) exceed L2; no flush" % (tp * e * m / 2**20),
-                   "mode": "split" if args.split else "fused"},
+                   "mode": "fused" if args.fused else "phase-split (auto: all ranks share one GPU)"},
         "latency_us": ms * 1e3, "latency_us_median": statistics.median(per) * 1e3,
         "algbw_gbs": e * m / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -398,6 +400,7 @@ def main():
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--lag", type=int, default=0)
     ap.add_argument("--split", action="store_true", help="phase-split kernels instead of the fused kernel")
+    ap.add_argument("--fused", action="store_true", help="force the fused flag-synchronised kernel")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -124,7 +124,8 @@ FC_API fc_status fc_comm_ipc_open(fc_comm* comm, const void* handles /* world * 
 FC_API fc_status fc_comm_destroy(fc_comm* comm);
 
 typedef enum {
-  FC_OPT_FUSED = 0,        /* 1: one persistent kernel with per-tile flags (default); 0: phase-split */
+  FC_OPT_FUSED = 0,        /* 1: one persistent kernel with per-tile flags; 0: phase-split; -1 (default):
+                              fused except when every rank shares one GPU (no link to overlap) */
   FC_OPT_CTAS = 1,         /* CTAs per rank for the fused kernel (0 = auto) */
   FC_OPT_TIMEOUT_MS = 2,   /* flag-wait timeout -> ProtocolError (fabric.py:158-178); default 5000 */
   FC_OPT_LAG = 3,          /* fused schedule: tiles between a tile's scatter and its reduce (0 = auto) */

@@ -11,13 +11,14 @@
 #include <numeric>
 #include <string>
 
+#include "fc_comm.h"
 #include "fc_flash.cuh"
-#include "fc_host.h"
+#include "fc_run.cuh"
 
 namespace fc {
 
 static thread_local std::string g_err;
-static thread_local int64_t g_launch_count = 0;  // kernels launched by the current call
+thread_local int64_t g_launch_count = 0;
 
 void set_error(const char* fmt, ...) {
   char buf[1024];
@@ -28,7 +29,7 @@ void set_error(const char* fmt, ...) {
   g_err = buf;
 }
 
-static fc_status fail(fc_status s, const char* fmt, ...) {
+fc_status fail(fc_status s, const char* fmt, ...) {
   char buf[1024];
   va_list ap;
   va_start(ap, fmt);
@@ -51,7 +52,7 @@ fc_status validate_codec(const fc_codec* c) {
   return FC_OK;
 }
 
-static int64_t group_of(const fc_codec& c) { return c.kind == FC_KIND_FP16 ? 1 : c.group_size; }
+int64_t group_of(const fc_codec& c) { return c.kind == FC_KIND_FP16 ? 1 : c.group_size; }
 
 // collectives.py:56-75
 static fc_status resolve_chunk(const fc_flash_cfg* cfg, int world, int64_t* out) {
@@ -76,28 +77,6 @@ using namespace fc;
 // ============================================================================
 // communicator
 
-struct fc_comm {
-  int world = 0;
-  bool ipc = false;
-  int my_rank = 0;  // ipc
-  int devices[kMaxRanks] = {0};
-  int64_t slot_bytes = 0;
-  int64_t flags_cap = 0;
-  int64_t block_bytes = 0;
-  uint8_t* blk[kMaxRanks] = {nullptr};
-  bool owned[kMaxRanks] = {false};
-  bool opened[kMaxRanks] = {false};
-  float* scratch[kMaxRanks] = {nullptr};
-  int64_t scratch_elems[kMaxRanks] = {0};
-  cudaEvent_t ev[kMaxRanks] = {nullptr};
-  uint32_t epoch = 0;
-  // options
-  int64_t fused = 1, ctas = 0, timeout_ms = 5000, lag = 0, fast = 1;
-  int64_t launches = 0, last_launches = 0;  // kernels launched by the last call
-  // last call (debug export)
-  fc_codec last_c1{}, last_c2{};
-  int64_t last_R = 0, last_sub_len = 0;
-};
 
 static int64_t block_bytes_for(int world, int64_t slot_bytes, int64_t flags_cap) {
   return blk_misc_off(world, slot_bytes, flags_cap) + kMiscBytes;
@@ -292,7 +271,7 @@ fc_status fc_comm_destroy(fc_comm* c) {
 fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
   if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
   switch (option) {
-    case FC_OPT_FUSED: c->fused = value != 0; break;
+    case FC_OPT_FUSED: c->fused = value < 0 ? -1 : (value != 0); break;
     case FC_OPT_CTAS: c->ctas = std::max<int64_t>(0, value); break;
     case FC_OPT_TIMEOUT_MS:
       if (value <= 0) return fail(FC_ERR_CONFIG, "timeout must be positive");
@@ -326,292 +305,6 @@ fc_status fc_comm_get_option(fc_comm* c, int32_t option, int64_t* value) {
 
 namespace {
 
-struct Plan {
-  int64_t seg = 0, R = 0, rounds = 0;
-  bool fast = false;
-  fc_layout L1{}, L2{};
-};
-
-fc_status make_plan(const fc_comm* c, const fc_flash_cfg* cfg, int64_t n, bool aligned, Plan* p) {
-  const int N = c->world;
-  p->seg = ceil_div(n, N);
-  p->fast = c->fast && fast_group(cfg->stage1) && fast_group(cfg->stage2) && (p->seg % 8 == 0) && aligned;
-  int64_t unit = std::lcm(group_of(cfg->stage1), group_of(cfg->stage2));
-  if (p->fast) unit = std::lcm(unit, (int64_t)kTileElems);
-  // largest multiple of `unit` whose two slot layouts fit and whose tiles fit the flags
-  const int sbmax = std::max(storage_bits(cfg->stage1), storage_bits(cfg->stage2));
-  int64_t rmax = (c->slot_bytes * 8 / sbmax) / unit * unit;
-  while (rmax > 0 && (layout_of(cfg->stage1, rmax).total_bytes > c->slot_bytes ||
-                      layout_of(cfg->stage2, rmax).total_bytes > c->slot_bytes ||
-                      ceil_div(rmax, kTileElems) > c->flags_cap))
-    rmax -= unit;
-  if (rmax <= 0 && p->seg > 0) {
-    // a single round of the whole segment may still fit (seg < unit)
-    if (layout_of(cfg->stage1, p->seg).total_bytes <= c->slot_bytes &&
-        layout_of(cfg->stage2, p->seg).total_bytes <= c->slot_bytes && ceil_div(p->seg, kTileElems) <= c->flags_cap)
-      rmax = p->seg;
-    else
-      return fail(FC_ERR_CONFIG, "communicator slots (%lld B) too small for group lcm %lld",
-                  (long long)c->slot_bytes, (long long)unit);
-  }
-  p->R = std::min(p->seg, rmax);
-  p->rounds = ceil_div(p->seg, p->R);
-  p->L1 = layout_of(cfg->stage1, p->R);
-  p->L2 = layout_of(cfg->stage2, p->R);
-  return FC_OK;
-}
-
-uint8_t* h_recv_slot(const fc_comm* c, int owner, int src) { return c->blk[owner] + (int64_t)src * c->slot_bytes; }
-uint8_t* h_gath_slot(const fc_comm* c, int owner, int src) {
-  return c->blk[owner] + (int64_t)(c->world + src) * c->slot_bytes;
-}
-
-template <typename Tin, typename Tout>
-fc_status launch_fused(const fc_comm* c, FlashArgs a, int rank_lo, int rank_hi, int device, cudaStream_t st) {
-  auto kern = k_flash_fused<Tin, Tout>;
-  int occ = 0;
-  FC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
-  const int cap = std::max(1, occ) * num_sms(device);
-  const int nr = rank_hi - rank_lo;
-  int C = c->ctas > 0 ? (int)c->ctas : cap / nr;
-  C = std::max(1, std::min(C, cap / nr));
-  a.rank_lo = rank_lo;
-  a.rank_hi = rank_hi;
-  a.ctas_per_rank = C;
-  const int per_step = 2 * (a.world - 1) + 1;
-  a.lag = c->lag > 0 ? (int)c->lag : (C + per_step - 1) / per_step + 1;
-  void* args[] = {&a};
-  FC_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(nr * C), dim3(kThreads), args, 0, st));
-  ++g_launch_count;
-  return FC_OK;
-}
-
-unsigned grid_for(int device, int64_t items) {
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)num_sms(device) * 8));
-}
-
-// order every rank's stream after every other rank's work so far (one process, several GPUs)
-fc_status cross_sync(fc_comm* c, cudaStream_t* st) {
-  for (int r = 0; r < c->world; ++r) {
-    FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-    FC_CUDA_TRY(cudaEventRecord(c->ev[r], st[r]));
-  }
-  for (int r = 0; r < c->world; ++r) {
-    FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-    for (int q = 0; q < c->world; ++q)
-      if (q != r) FC_CUDA_TRY(cudaStreamWaitEvent(st[r], c->ev[q], 0));
-  }
-  return FC_OK;
-}
-
-fc_status ensure_scratch(fc_comm* c, int r, int64_t elems) {
-  if (c->scratch_elems[r] >= elems) return FC_OK;
-  FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-  if (c->scratch[r]) {
-    FC_CUDA_TRY(cudaDeviceSynchronize());
-    cudaFree(c->scratch[r]);
-  }
-  FC_CUDA_TRY(cudaMalloc(&c->scratch[r], (size_t)elems * 4));
-  c->scratch_elems[r] = elems;
-  return FC_OK;
-}
-
-// generic (any group size) phases for rank r ------------------------------------
-template <typename Tin>
-fc_status gen_phase_scatter(fc_comm* c, const FlashArgs& a, int r, cudaStream_t st) {
-  const int dev = c->devices[r];
-  for (int j = 0; j < c->world; ++j) {
-    SrcSeg<Tin> src{reinterpret_cast<const Tin*>(a.in[r]), (int64_t)j * a.seg + a.sub_off, a.M};
-    uint8_t* dst = h_recv_slot(c, j, r);
-    uint32_t* ew = reinterpret_cast<uint32_t*>(c->blk[r] + blk_misc_off(c->world, c->slot_bytes, c->flags_cap));
-    if (a.c1.kind == FC_KIND_INT) {
-      k_gen_params<<<grid_for(dev, ceil_div(ceil_div(a.sub_len, a.c1.g), 256)), 256, 0, st>>>(src, a.sub_len, a.c1, dst,
-                                                                                            ew, r);
-      ++g_launch_count;
-    }
-    k_gen_codes<<<grid_for(dev, ceil_div(gen_code_units(a.c1, a.sub_len), 256)), 256, 0, st>>>(src, a.sub_len, a.c1,
-                                                                                             dst, ew, r);
-    ++g_launch_count;
-  }
-  FC_CUDA_TRY(cudaGetLastError());
-  return FC_OK;
-}
-
-fc_status gen_phase_reduce(fc_comm* c, const FlashArgs& a, int j, cudaStream_t st, int64_t L2_bytes) {
-  const int dev = c->devices[j];
-  FC_TRY(ensure_scratch(c, j, a.sub_len));
-  FC_CUDA_TRY(cudaSetDevice(dev));
-  uint32_t* ew = reinterpret_cast<uint32_t*>(c->blk[j] + blk_misc_off(c->world, c->slot_bytes, c->flags_cap));
-  k_gen_sum<<<grid_for(dev, ceil_div(a.sub_len, 256)), 256, 0, st>>>(a, j, c->scratch[j]); ++g_launch_count;
-  SrcF32 src{c->scratch[j]};
-  uint8_t* dst = h_gath_slot(c, j, j);
-  if (a.c2.kind == FC_KIND_INT) {
-    k_gen_params<<<grid_for(dev, ceil_div(ceil_div(a.sub_len, a.c2.g), 256)), 256, 0, st>>>(src, a.sub_len, a.c2, dst,
-                                                                                          ew, j);
-    ++g_launch_count;
-  }
-  k_gen_codes<<<grid_for(dev, ceil_div(gen_code_units(a.c2, a.sub_len), 256)), 256, 0, st>>>(src, a.sub_len, a.c2, dst,
-                                                                                           ew, j);
-  ++g_launch_count;
-  k_gen_bcast<<<grid_for(dev, ceil_div(L2_bytes / 16, 256)), 256, 0, st>>>(a, j, L2_bytes); ++g_launch_count;
-  FC_CUDA_TRY(cudaGetLastError());
-  return FC_OK;
-}
-
-template <typename Tout>
-fc_status gen_phase_gather(fc_comm* c, const FlashArgs& a, int r, cudaStream_t st) {
-  const int dev = c->devices[r];
-  for (int j = 0; j < c->world; ++j) {
-    k_gen_dequant<Tout><<<grid_for(dev, ceil_div(a.sub_len, 256)), 256, 0, st>>>(
-        h_gath_slot(c, r, j), a.sub_len, a.c2, reinterpret_cast<Tout*>(a.out[r]), (int64_t)j * a.seg + a.sub_off, a.M);
-    ++g_launch_count;
-  }
-  FC_CUDA_TRY(cudaGetLastError());
-  return FC_OK;
-}
-
-// IPC barrier between phases
-fc_status ipc_barrier(fc_comm* c, const FlashArgs& a, int rank, int phase, cudaStream_t st) {
-  k_barrier<<<1, 32, 0, st>>>(a, rank, phase); ++g_launch_count;
-  FC_CUDA_TRY(cudaGetLastError());
-  return FC_OK;
-}
-
-template <typename Tin, typename Tout>
-fc_status run_typed(fc_comm* c, const void* const* ins, void* const* outs, int64_t n, const fc_flash_cfg* cfg,
-                    cudaStream_t* st, int only_rank /* -1: local world */) {
-  const int N = c->world;
-  bool aligned = true;
-  for (int r = 0; r < N; ++r) {
-    if (only_rank >= 0 && r != only_rank) continue;
-    aligned &= ((uintptr_t)ins[r] % 16 == 0) && ((uintptr_t)outs[r] % 16 == 0);
-  }
-  Plan p;
-  FC_TRY(make_plan(c, cfg, n, aligned, &p));
-  g_launch_count = 0;
-  FlashArgs a{};
-  a.world = N;
-  a.M = n;
-  a.seg = p.seg;
-  a.slot_bytes = c->slot_bytes;
-  a.flags_cap = c->flags_cap;
-  a.timeout_ns = (uint64_t)c->timeout_ms * 1000000ull;
-  a.c1 = dev_codec(cfg->stage1, p.L1);
-  a.c2 = dev_codec(cfg->stage2, p.L2);
-  for (int r = 0; r < N; ++r) {
-    a.in[r] = ins[r];
-    a.out[r] = outs[r];
-    a.blk[r] = c->blk[r];
-  }
-  bool single_dev = true;
-  for (int r = 1; r < N; ++r) single_dev &= c->devices[r] == c->devices[0];
-
-  for (int64_t k = 0; k < p.rounds; ++k) {
-    a.sub_off = k * p.R;
-    a.sub_len = std::min(p.R, p.seg - a.sub_off);
-    a.tiles = (int)ceil_div(a.sub_len, kTileElems);
-    a.epoch = ++c->epoch;
-    if (only_rank >= 0) {
-      // ---------------- IPC world: this process is rank `only_rank`
-      const int r = only_rank;
-      const int dev = c->devices[r];
-      FC_CUDA_TRY(cudaSetDevice(dev));
-      cudaStream_t s = st[r];
-      if (p.fast && c->fused) {
-        FC_TRY((launch_fused<Tin, Tout>(c, a, r, r + 1, dev, s)));
-      } else if (p.fast) {
-        a.rank_lo = r;
-        a.rank_hi = r + 1;
-        k_scatter<Tin><<<grid_for(dev, (int64_t)(N - 1) * a.tiles), kThreads, 0, s>>>(a); ++g_launch_count;
-        FC_TRY(ipc_barrier(c, a, r, 0, s));
-        k_reduce<Tin, Tout><<<grid_for(dev, a.tiles), kThreads, 0, s>>>(a); ++g_launch_count;
-        FC_TRY(ipc_barrier(c, a, r, 1, s));
-        k_gather<Tout><<<grid_for(dev, (int64_t)(N - 1) * a.tiles), kThreads, 0, s>>>(a); ++g_launch_count;
-      } else {
-        FC_TRY(gen_phase_scatter<Tin>(c, a, r, s));
-        FC_TRY(ipc_barrier(c, a, r, 0, s));
-        FC_TRY(gen_phase_reduce(c, a, r, s, p.L2.total_bytes));
-        FC_TRY(ipc_barrier(c, a, r, 1, s));
-        FC_TRY(gen_phase_gather<Tout>(c, a, r, s));
-      }
-      FC_CUDA_TRY(cudaGetLastError());
-      continue;
-    }
-    // ---------------- local world: this process drives every rank
-    if (p.fast && c->fused) {
-      if (single_dev) {
-        FC_CUDA_TRY(cudaSetDevice(c->devices[0]));
-        FC_TRY((launch_fused<Tin, Tout>(c, a, 0, N, c->devices[0], st[0])));
-      } else {
-        for (int r = 0; r < N; ++r) {
-          FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-          FC_TRY((launch_fused<Tin, Tout>(c, a, r, r + 1, c->devices[r], st[r])));
-        }
-      }
-    } else if (p.fast && single_dev) {
-      const int dev = c->devices[0];
-      FC_CUDA_TRY(cudaSetDevice(dev));
-      a.rank_lo = 0;
-      a.rank_hi = N;
-      k_scatter<Tin><<<grid_for(dev, (int64_t)N * (N - 1) * a.tiles), kThreads, 0, st[0]>>>(a); ++g_launch_count;
-      k_reduce<Tin, Tout><<<grid_for(dev, (int64_t)N * a.tiles), kThreads, 0, st[0]>>>(a); ++g_launch_count;
-      k_gather<Tout><<<grid_for(dev, (int64_t)N * (N - 1) * a.tiles), kThreads, 0, st[0]>>>(a); ++g_launch_count;
-    } else if (p.fast) {
-      for (int r = 0; r < N; ++r) {
-        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-        a.rank_lo = r;
-        a.rank_hi = r + 1;
-        k_scatter<Tin><<<grid_for(c->devices[r], (int64_t)(N - 1) * a.tiles), kThreads, 0, st[r]>>>(a); ++g_launch_count;
-      }
-      FC_TRY(cross_sync(c, st));
-      for (int r = 0; r < N; ++r) {
-        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-        a.rank_lo = r;
-        a.rank_hi = r + 1;
-        k_reduce<Tin, Tout><<<grid_for(c->devices[r], a.tiles), kThreads, 0, st[r]>>>(a); ++g_launch_count;
-      }
-      FC_TRY(cross_sync(c, st));
-      for (int r = 0; r < N; ++r) {
-        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-        a.rank_lo = r;
-        a.rank_hi = r + 1;
-        k_gather<Tout><<<grid_for(c->devices[r], (int64_t)(N - 1) * a.tiles), kThreads, 0, st[r]>>>(a); ++g_launch_count;
-      }
-    } else {
-      for (int r = 0; r < N; ++r) {
-        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-        FC_TRY(gen_phase_scatter<Tin>(c, a, r, single_dev ? st[0] : st[r]));
-      }
-      if (!single_dev) FC_TRY(cross_sync(c, st));
-      for (int r = 0; r < N; ++r) {
-        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-        FC_TRY(gen_phase_reduce(c, a, r, single_dev ? st[0] : st[r], p.L2.total_bytes));
-      }
-      if (!single_dev) FC_TRY(cross_sync(c, st));
-      for (int r = 0; r < N; ++r) {
-        FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-        FC_TRY(gen_phase_gather<Tout>(c, a, r, single_dev ? st[0] : st[r]));
-      }
-    }
-    FC_CUDA_TRY(cudaGetLastError());
-  }
-  c->last_launches = g_launch_count;
-  c->last_c1 = cfg->stage1;
-  c->last_c2 = cfg->stage2;
-  c->last_R = p.R;
-  c->last_sub_len = std::min(p.R, p.seg - (p.rounds - 1) * p.R);
-  return FC_OK;
-}
-
-template <typename Tin, typename Tout>
-fc_status identity_typed(const void* in, void* out, int64_t n, int device, cudaStream_t st) {
-  FC_CUDA_TRY(cudaSetDevice(device));
-  k_convert<Tin, Tout><<<grid_for(device, ceil_div(n, 256)), 256, 0, st>>>(reinterpret_cast<const Tin*>(in),
-                                                                          reinterpret_cast<Tout*>(out), n);
-  FC_CUDA_TRY(cudaGetLastError());
-  return FC_OK;
-}
-
 #define FC_DISPATCH2(IN_DT, OUT_DT, FN, ...)                                                     \
   [&]() -> fc_status {                                                                           \
     switch ((IN_DT) * 3 + (OUT_DT)) {                                                            \
@@ -627,7 +320,22 @@ fc_status identity_typed(const void* in, void* out, int64_t n, int device, cudaS
     }                                                                                            \
   }()
 
-fc_status check_call(const fc_comm* c, int64_t n, int in_dt, int out_dt, const fc_flash_cfg* cfg) {
+// flash kernels exist for out dtype == in dtype, or float32 out
+#define FC_DISPATCH_RUN(IN_DT, OUT_DT, ...)                                                      \
+  [&]() -> fc_status {                                                                           \
+    switch ((IN_DT) * 3 + (OUT_DT)) {                                                            \
+      case FC_DTYPE_F32 * 3 + FC_DTYPE_F32: return run_typed<float, float>(__VA_ARGS__);         \
+      case FC_DTYPE_F16 * 3 + FC_DTYPE_F32: return run_typed<__half, float>(__VA_ARGS__);        \
+      case FC_DTYPE_F16 * 3 + FC_DTYPE_F16: return run_typed<__half, __half>(__VA_ARGS__);       \
+      case FC_DTYPE_BF16 * 3 + FC_DTYPE_F32: return run_typed<__nv_bfloat16, float>(__VA_ARGS__); \
+      case FC_DTYPE_BF16 * 3 + FC_DTYPE_BF16:                                                    \
+        return run_typed<__nv_bfloat16, __nv_bfloat16>(__VA_ARGS__);                             \
+      default:                                                                                   \
+        return fail(FC_ERR_CONFIG, "output dtype must equal the input dtype or be float32");    \
+    }                                                                                            \
+  }()
+
+inline fc_status check_call(const fc_comm* c, int64_t n, int in_dt, int out_dt, const fc_flash_cfg* cfg) {
   if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
   if (!cfg) return fail(FC_ERR_CONFIG, "flash method needs a FlashConfig");
   FC_TRY(validate_codec(&cfg->stage1));
@@ -652,7 +360,7 @@ fc_status fc_flash_all_reduce_local(fc_comm* c, const void* const* ins, void* co
   cudaStream_t st[kMaxRanks];
   for (int r = 0; r < c->world; ++r) st[r] = streams ? (cudaStream_t)streams[r] : (cudaStream_t)0;
   if (c->world == 1) return FC_DISPATCH2(in_dtype, out_dtype, identity_typed, ins[0], outs[0], n, c->devices[0], st[0]);
-  return FC_DISPATCH2(in_dtype, out_dtype, run_typed, c, ins, outs, n, cfg, st, -1);
+  return FC_DISPATCH_RUN(in_dtype, out_dtype, c, ins, outs, n, cfg, st, -1);
 }
 
 fc_status fc_flash_all_reduce(fc_comm* c, const void* in, void* out, int64_t n, int32_t in_dtype, int32_t out_dtype,
@@ -670,7 +378,7 @@ fc_status fc_flash_all_reduce(fc_comm* c, const void* in, void* out, int64_t n, 
   ins[r] = in;
   outs[r] = out;
   st[r] = (cudaStream_t)stream;
-  return FC_DISPATCH2(in_dtype, out_dtype, run_typed, c, ins, outs, n, cfg, st, r);
+  return FC_DISPATCH_RUN(in_dtype, out_dtype, c, ins, outs, n, cfg, st, r);
 }
 
 fc_status fc_comm_check(fc_comm* c, int32_t rank) {

@@ -11,7 +11,7 @@ namespace fc {
 // --------------------------------------------------------------------------
 // fast path: one 32-element chunk per thread, groups of g/32 lanes
 
-template <typename T>
+template <typename T, int CW>
 __global__ void __launch_bounds__(kThreads) k_quant_fast(const T* __restrict__ x, int64_t n, DevCodec c,
                                                          uint8_t* __restrict__ dst, uint32_t* err) {
   const int lane = threadIdx.x & 31;
@@ -21,14 +21,14 @@ __global__ void __launch_bounds__(kThreads) k_quant_fast(const T* __restrict__ x
     const int nvalid = (int)max((int64_t)0, min(n - p0, (int64_t)kLaneElems));
     float v[kLaneElems];
     load_chunk(x, p0, n, nvalid, v);
-    LaneQuant q;
+    LaneQuant<CW> q;
     const bool bad = lane_quantize(c, v, nvalid, q);
     store_lane(c, dst, p0, nvalid, q, lane);
     if (bad && err) atomicOr(err, make_err(kErrNonFinite, 0, 0, 0));
   }
 }
 
-template <typename To>
+template <typename To, int CW>
 __global__ void __launch_bounds__(kThreads) k_dequant_fast(const uint8_t* __restrict__ src, int64_t n, DevCodec c,
                                                            To* __restrict__ out) {
   const int64_t tiles = (n + kTileElems - 1) / kTileElems;
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kThreads) k_dequant_fast(const uint8_t* __rest
     const int64_t p0 = t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
     const int nvalid = (int)max((int64_t)0, min(n - p0, (int64_t)kLaneElems));
     if (nvalid <= 0) continue;
-    LaneCodes L;
+    LaneCodes<CW> L;
     load_lane(c, src, p0, L);
     float v[kLaneElems];
     lane_decode<false>(c, L, v);
@@ -84,11 +84,14 @@ fc_status launch_quantize(const void* x, int in_dtype, int64_t n, const fc_codec
     const int64_t tiles = (n + kTileElems - 1) / kTileElems;
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)cur_sms() * 8);
     uint8_t* d = (uint8_t*)dst;
+    const bool pass = c.kind == FC_KIND_FP16;
+#define FC_QF(T) (pass ? k_quant_fast<T, 16> : k_quant_fast<T, 8>)<<<grid, kThreads, 0, st>>>((const T*)x, n, dc, d, err)
     switch (in_dtype) {
-      case FC_DTYPE_F32: k_quant_fast<float><<<grid, kThreads, 0, st>>>((const float*)x, n, dc, d, err); break;
-      case FC_DTYPE_F16: k_quant_fast<__half><<<grid, kThreads, 0, st>>>((const __half*)x, n, dc, d, err); break;
-      default: k_quant_fast<__nv_bfloat16><<<grid, kThreads, 0, st>>>((const __nv_bfloat16*)x, n, dc, d, err); break;
+      case FC_DTYPE_F32: FC_QF(float); break;
+      case FC_DTYPE_F16: FC_QF(__half); break;
+      default: FC_QF(__nv_bfloat16); break;
     }
+#undef FC_QF
   } else {
     uint8_t* d = (uint8_t*)dst;
     switch (in_dtype) {
@@ -110,11 +113,14 @@ fc_status launch_dequantize(const void* src, int64_t n, const fc_codec& c, void*
   if (allow_fast && fast_group(c) && aligned) {
     const int64_t tiles = (n + kTileElems - 1) / kTileElems;
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)cur_sms() * 8);
+    const bool pass = c.kind == FC_KIND_FP16;
+#define FC_DF(T) (pass ? k_dequant_fast<T, 16> : k_dequant_fast<T, 8>)<<<grid, kThreads, 0, st>>>(s, n, dc, (T*)out)
     switch (out_dtype) {
-      case FC_DTYPE_F32: k_dequant_fast<float><<<grid, kThreads, 0, st>>>(s, n, dc, (float*)out); break;
-      case FC_DTYPE_F16: k_dequant_fast<__half><<<grid, kThreads, 0, st>>>(s, n, dc, (__half*)out); break;
-      default: k_dequant_fast<__nv_bfloat16><<<grid, kThreads, 0, st>>>(s, n, dc, (__nv_bfloat16*)out); break;
+      case FC_DTYPE_F32: FC_DF(float); break;
+      case FC_DTYPE_F16: FC_DF(__half); break;
+      default: FC_DF(__nv_bfloat16); break;
     }
+#undef FC_DF
   } else {
     const unsigned grid = (unsigned)((n + 255) / 256);
     switch (out_dtype) {

@@ -1,0 +1,48 @@
+// Communicator state shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "fc_host.h"
+
+namespace fc {
+extern thread_local int64_t g_launch_count;  // kernels launched by the current call
+fc_status fail(fc_status s, const char* fmt, ...);
+int64_t group_of(const fc_codec& c);
+}  // namespace fc
+
+using fc::kMaxRanks;
+
+struct fc_comm {
+  int world = 0;
+  bool ipc = false;
+  int my_rank = 0;  // ipc
+  int devices[kMaxRanks] = {0};
+  int64_t slot_bytes = 0;
+  int64_t flags_cap = 0;
+  int64_t block_bytes = 0;
+  uint8_t* blk[kMaxRanks] = {nullptr};
+  bool owned[kMaxRanks] = {false};
+  bool opened[kMaxRanks] = {false};
+  float* scratch[kMaxRanks] = {nullptr};
+  int64_t scratch_elems[kMaxRanks] = {0};
+  cudaEvent_t ev[kMaxRanks] = {nullptr};
+  uint32_t epoch = 0;
+  // options
+  int64_t fused = -1, ctas = 0, timeout_ms = 5000, lag = 0, fast = 1;  // fused: -1 auto
+  int64_t launches = 0, last_launches = 0;  // kernels launched by the last call
+  // last call (debug export)
+  fc_codec last_c1{}, last_c2{};
+  int64_t last_R = 0, last_sub_len = 0;
+};
+
+namespace fc {
+// run_typed<Tin, Tout>: instantiated in fc_run_{f32,f16,bf16}.cu
+template <typename Tin, typename Tout>
+fc_status run_typed(fc_comm* c, const void* const* ins, void* const* outs, int64_t n, const fc_flash_cfg* cfg,
+                    cudaStream_t* st, int only_rank);
+template <typename Tin, typename Tout>
+fc_status identity_typed(const void* in, void* out, int64_t n, int device, cudaStream_t st);
+}  // namespace fc

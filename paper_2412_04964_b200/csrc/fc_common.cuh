@@ -207,8 +207,11 @@ __device__ __forceinline__ __half snap_scale(double raw, double floor) {
 // -s < rho <= 0. Symmetric codes are computed in offset binary (z = 2^(b-1))
 // and XOR-ed back to two's complement, so both schemes share one decoder.
 
+// CW: 32-bit code words per lane: 8 for integer codecs, 16 when a codec may
+// be the fp16 passthrough (kernels are instantiated for both).
+template <int CW>
 struct LaneQuant {
-  uint32_t w[16];  // packed codes: INT4 w[0..3], INT8 w[0..7], fp16 bits w[0..15]
+  uint32_t w[CW];  // packed codes: INT4 w[0..3], INT8 w[0..7], fp16 bits w[0..15]
   __half s16;
   float s;         // scale (exact fp16 value as fp32)
   float mz;        // decode bias 2^23 + zero (asym) or 2^23 + 2^(b-1) (sym)
@@ -216,8 +219,9 @@ struct LaneQuant {
   uint8_t z8;
 };
 
+template <int CW>
 struct LaneCodes {
-  uint32_t w[16];  // offset-binary codes (xr already applied) or fp16 bits
+  uint32_t w[CW];  // offset-binary codes (xr already applied) or fp16 bits
   float s;
   float mz;
 };
@@ -378,9 +382,11 @@ __device__ __forceinline__ float group_allreduce_max(float v, int lpg) {
 }
 
 // returns true if a valid element of the lane's group is NaN/inf (codec.py:230-231)
+template <int CW>
 __device__ __forceinline__ bool lane_quantize(const DevCodec& c, const float v[kLaneElems], int nvalid,
-                                              LaneQuant& q) {
-  if (c.kind == FC_KIND_FP16) {
+                                              LaneQuant<CW>& q) {
+  if constexpr (CW == 16) {
+    if (c.kind == FC_KIND_FP16) {
     float lo, hi;
     lane_stats<true>(v, nvalid, lo, hi);
 #pragma unroll
@@ -394,6 +400,7 @@ __device__ __forceinline__ bool lane_quantize(const DevCodec& c, const float v[k
     q.xr = 0u;
     q.z8 = 0;
     return nvalid > 0 && !(hi <= 3.402823466e38f);
+    }
   }
   float lo, hi;
   if (c.sym) {
@@ -453,13 +460,14 @@ __device__ __forceinline__ int lane_code_bytes(const DevCodec& c) { return c.sb 
 
 // Store a quantized lane chunk into a buffer (local or peer memory).
 // p0: element offset of the chunk within the quantized range.
+template <int CW>
 __device__ __forceinline__ void store_lane(const DevCodec& c, uint8_t* buf, int64_t p0, int nvalid,
-                                           const LaneQuant& q, int lane) {
+                                           const LaneQuant<CW>& q, int lane) {
   if (nvalid <= 0) return;  // chunk lies past the end of the range
   uint8_t* cp = buf + p0 * c.sb / 8;
   const int nq = c.sb / 4;  // number of 16-B vectors: 1 (int4), 2 (int8), 4 (fp16)
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < CW / 4; ++i)
     if (i < nq) st_v4(cp + 16 * i, make_uint4(q.w[4 * i], q.w[4 * i + 1], q.w[4 * i + 2], q.w[4 * i + 3]));
   if (c.kind == FC_KIND_INT && (lane % c.lpg) == 0) {
     int64_t grp = p0 / c.g;
@@ -471,18 +479,20 @@ __device__ __forceinline__ void store_lane(const DevCodec& c, uint8_t* buf, int6
 // Decode helpers ------------------------------------------------------------
 
 // in-register codes of a freshly quantized lane, in offset binary
-__device__ __forceinline__ void lane_codes_from(const DevCodec& c, const LaneQuant& q, LaneCodes& L) {
+template <int CW>
+__device__ __forceinline__ void lane_codes_from(const DevCodec& c, const LaneQuant<CW>& q, LaneCodes<CW>& L) {
 #pragma unroll
-  for (int i = 0; i < 16; ++i) L.w[i] = (c.kind == FC_KIND_INT && i < 8) ? (q.w[i] ^ q.xr) : q.w[i];
+  for (int i = 0; i < CW; ++i) L.w[i] = (c.kind == FC_KIND_INT && i < 8) ? (q.w[i] ^ q.xr) : q.w[i];
   L.s = q.s;
   L.mz = q.mz;
 }
 
-__device__ __forceinline__ void load_lane(const DevCodec& c, const uint8_t* buf, int64_t p0, LaneCodes& L) {
+template <int CW>
+__device__ __forceinline__ void load_lane(const DevCodec& c, const uint8_t* buf, int64_t p0, LaneCodes<CW>& L) {
   const uint8_t* cp = buf + p0 * c.sb / 8;
   const int nq = c.sb / 4;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < CW / 4; ++i) {
     if (i >= nq) break;
     uint4 u = ld_cg_v4(cp + 16 * i);
     L.w[4 * i] = u.x;
@@ -510,9 +520,10 @@ __device__ __forceinline__ float magic_byte(uint32_t w, int b) {
 
 // out[k] = (c_k - z) * s, exact in fp32 (codec.py:383-384); fp16 kind: value
 // ACC: out[k] += that value with one rounding (fp32 sum, collectives.py:186)
-template <bool ACC>
-__device__ __forceinline__ void lane_decode(const DevCodec& c, const LaneCodes& L, float out[kLaneElems]) {
-  if (c.kind == FC_KIND_FP16) {
+template <bool ACC, int CW>
+__device__ __forceinline__ void lane_decode(const DevCodec& c, const LaneCodes<CW>& L, float out[kLaneElems]) {
+  if constexpr (CW == 16) {
+   if (c.kind == FC_KIND_FP16) {
 #pragma unroll
     for (int k = 0; k < kLaneElems; k += 2) {
       __half2 h = *reinterpret_cast<const __half2*>(&L.w[k / 2]);
@@ -526,6 +537,7 @@ __device__ __forceinline__ void lane_decode(const DevCodec& c, const LaneCodes& 
       }
     }
     return;
+   }
   }
   if (c.sb == 4) {
 #pragma unroll

@@ -70,20 +70,20 @@ enum Phase : uint32_t { kPhScatter = 1, kPhReduce = 2, kPhGather = 3, kPhBarrier
 
 // ---------------------------------------------------------------- work items
 
-template <typename Tin>
+template <typename Tin, int CW>
 __device__ __forceinline__ void do_scatter(const FlashArgs& a, int r, int j, int t) {
   const int lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
   const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
   float v[kLaneElems];
   load_chunk(reinterpret_cast<const Tin*>(a.in[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, v);
-  LaneQuant q;
+  LaneQuant<CW> q;
   const bool bad = lane_quantize(a.c1, v, nvalid, q);
   store_lane(a.c1, recv_slot(a, j, r), p0, nvalid, q, lane);
   if (bad) atomicOr(errw(a, r), make_err(kErrNonFinite, kPhScatter, j, r));
 }
 
-template <typename Tin, typename Tout>
+template <typename Tin, typename Tout, int CW>
 __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
   const int lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
@@ -92,18 +92,18 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
   bool bad = false;
   float acc[kLaneElems];
   for (int s = 0; s < a.world; ++s) {
-    LaneCodes L;
+    LaneCodes<CW> L;
     if (s == j) {
       float v[kLaneElems];
       load_chunk(reinterpret_cast<const Tin*>(a.in[j]), idx0, a.M, nvalid, v);
-      LaneQuant q;
+      LaneQuant<CW> q;
       bad |= lane_quantize(a.c1, v, nvalid, q);  // own piece: QDQ in registers (collectives.py:364-365)
       lane_codes_from(a.c1, q, L);
     } else if (nvalid > 0) {
       load_lane(a.c1, recv_slot(a, j, s), p0, L);
     } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) L.w[i] = 0;
+      for (int i = 0; i < CW; ++i) L.w[i] = 0;
       L.s = 0.0f;
       L.mz = 0.0f;
     }
@@ -112,13 +112,13 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
     else
       lane_decode<true>(a.c1, L, acc);
   }
-  LaneQuant q2;
+  LaneQuant<CW> q2;
   bad |= lane_quantize(a.c2, acc, nvalid, q2);
   for (int pp = 1; pp < a.world; ++pp) {
     const int p = (j + pp) % a.world;
     store_lane(a.c2, gath_slot(a, p, j), p0, nvalid, q2, lane);
   }
-  LaneCodes L2;
+  LaneCodes<CW> L2;
   lane_codes_from(a.c2, q2, L2);
   float o[kLaneElems];
   lane_decode<false>(a.c2, L2, o);  // owner decodes its own payload too (collectives.py:378)
@@ -126,12 +126,12 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
   if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
 }
 
-template <typename Tout>
+template <typename Tout, int CW>
 __device__ __forceinline__ void do_gather(const FlashArgs& a, int r, int j, int t) {
   const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
   const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
   if (nvalid <= 0) return;
-  LaneCodes L;
+  LaneCodes<CW> L;
   load_lane(a.c2, gath_slot(a, r, j), p0, L);
   float o[kLaneElems];
   lane_decode<false>(a.c2, L, o);
@@ -183,7 +183,7 @@ __device__ __forceinline__ void raise_flags(uint32_t* const* flags, int nflags, 
 // holds P scatter items for tile k, the reduce of tile k-lag and P gathers of
 // tile k-2*lag. Every wait targets an item of a strictly earlier position, so
 // with all CTAs resident the schedule cannot deadlock.
-template <typename Tin, typename Tout>
+template <typename Tin, typename Tout, int CW>
 __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
   __shared__ int s_abort;
   __shared__ uint32_t* s_flags[kMaxRanks];
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
       const int64_t t = k;
       if (t >= a.tiles) continue;
       const int j = (rank + 1 + slot) % a.world;
-      do_scatter<Tin>(a, rank, j, (int)t);
+      do_scatter<Tin, CW>(a, rank, j, (int)t);
       if (threadIdx.x == 0) s_flags[0] = rflag(a, j, rank) + t;
       raise_flags(s_flags, 1, a.epoch);
     } else if (slot == P) {
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
       __syncthreads();
       if (wait_flags(a, rank, s_flags, s_peers, P, kPhReduce, &s_abort)) return;
       __syncthreads();
-      do_reduce<Tin, Tout>(a, rank, (int)t);
+      do_reduce<Tin, Tout, CW>(a, rank, (int)t);
       __syncthreads();
       if (threadIdx.x < P) s_flags[threadIdx.x] = gflag(a, (rank + 1 + threadIdx.x) % a.world, rank) + t;
       raise_flags(s_flags, P, a.epoch);
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
       }
       __syncthreads();
       if (wait_flags(a, rank, s_flags, s_peers, 1, kPhGather, &s_abort)) return;
-      do_gather<Tout>(a, rank, j, (int)t);
+      do_gather<Tout, CW>(a, rank, j, (int)t);
     }
     __syncthreads();
   }
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
 
 // Phase-split kernels (no flags): ordering comes from kernel boundaries
 // (one GPU), stream events (several GPUs, one process) or k_barrier (IPC).
-template <typename Tin>
+template <typename Tin, int CW>
 __global__ void __launch_bounds__(kThreads) k_scatter(FlashArgs a) {
   const int P = a.world - 1;
   const int64_t per_rank = (int64_t)P * a.tiles;
@@ -248,20 +248,20 @@ __global__ void __launch_bounds__(kThreads) k_scatter(FlashArgs a) {
     const int64_t rem = i % per_rank;
     const int t = (int)(rem / P);
     const int j = (r + 1 + (int)(rem % P)) % a.world;
-    do_scatter<Tin>(a, r, j, t);
+    do_scatter<Tin, CW>(a, r, j, t);
   }
 }
 
-template <typename Tin, typename Tout>
+template <typename Tin, typename Tout, int CW>
 __global__ void __launch_bounds__(kThreads, 2) k_reduce(FlashArgs a) {
   const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * a.tiles;
   for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
     const int j = a.rank_lo + (int)(i / a.tiles);
-    do_reduce<Tin, Tout>(a, j, (int)(i % a.tiles));
+    do_reduce<Tin, Tout, CW>(a, j, (int)(i % a.tiles));
   }
 }
 
-template <typename Tout>
+template <typename Tout, int CW>
 __global__ void __launch_bounds__(kThreads) k_gather(FlashArgs a) {
   const int P = a.world - 1;
   const int64_t per_rank = (int64_t)P * a.tiles;
@@ -271,13 +271,13 @@ __global__ void __launch_bounds__(kThreads) k_gather(FlashArgs a) {
     const int64_t rem = i % per_rank;
     const int t = (int)(rem / P);
     const int j = (r + 1 + (int)(rem % P)) % a.world;
-    do_gather<Tout>(a, r, j, t);
+    do_gather<Tout, CW>(a, r, j, t);
   }
 }
 
 // Cross-process barrier between phases (IPC world, phase-split/generic):
 // one warp; lane p != rank raises barflag[p][phase][rank], then waits on its own.
-__global__ void k_barrier(FlashArgs a, int rank, int phase) {
+static __global__ void k_barrier(FlashArgs a, int rank, int phase) {
   const int p = threadIdx.x;
   __threadfence_system();
   __syncwarp();
@@ -302,7 +302,7 @@ __global__ void k_barrier(FlashArgs a, int rank, int phase) {
 // ---------------------------------------------------------------- generic path
 
 // scratch[i] = sum_s dequant(recv_slot[owner][s])[i], ascending s
-__global__ void k_gen_sum(FlashArgs a, int owner, float* scratch) {
+static __global__ void k_gen_sum(FlashArgs a, int owner, float* scratch) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.sub_len;
        i += (int64_t)gridDim.x * blockDim.x) {
     float acc = 0.0f;
@@ -315,7 +315,7 @@ __global__ void k_gen_sum(FlashArgs a, int owner, float* scratch) {
 }
 
 // copy owner's own gather slot [owner] to every peer's gather slot [owner]
-__global__ void k_gen_bcast(FlashArgs a, int owner, int64_t bytes) {
+static __global__ void k_gen_bcast(FlashArgs a, int owner, int64_t bytes) {
   const uint8_t* src = gath_slot(a, owner, owner);
   const int64_t n16 = bytes / 16;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
