@@ -2,8 +2,11 @@
 // (codec.py:354-384), plus the generic (any group size) kernels that the
 // flash path reuses for group sizes outside {32, 64, 128, 256}.
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "fc_codec_dev.cuh"
+#include "fc_stage.cuh"
 #include "fc_host.h"
 
 namespace fc {
@@ -13,35 +16,87 @@ namespace fc {
 
 template <typename T, int CW>
 __global__ void __launch_bounds__(kThreads) k_quant_fast(const T* __restrict__ x, int64_t n, DevCodec c,
-                                                         uint8_t* __restrict__ dst, uint32_t* err) {
+                                                         uint8_t* __restrict__ dst, uint32_t* err, int S) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int CB = Chunk<T>::kBytes;
   const int lane = threadIdx.x & 31;
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem) + threadIdx.x * CB;
   const int64_t tiles = (n + kTileElems - 1) / kTileElems;
+  auto issue = [&](int64_t t, int st) {
+    if (t < tiles) {
+      const int64_t p0 = t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+      const int nvalid = (int)max((int64_t)0, min(n - p0, (int64_t)kLaneElems));
+      chunk_issue<T>(s0 + st * kThreads * CB, x, p0, n, nvalid, lane);
+    }
+    cp_async_commit();
+  };
+  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+  int st = 0;
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    issue(t + (int64_t)(S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
+    cp_async_wait_dyn(S - 1);
     const int64_t p0 = t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
     const int nvalid = (int)max((int64_t)0, min(n - p0, (int64_t)kLaneElems));
     float v[kLaneElems];
-    load_chunk(x, p0, n, nvalid, v);
+    chunk_read<T>(s0 + st * kThreads * CB, lane, v);
     LaneQuant<CW> q;
     const bool bad = lane_quantize(c, v, nvalid, q);
     store_lane(c, dst, p0, nvalid, q, lane);
     if (bad && err) atomicOr(err, make_err(kErrNonFinite, 0, 0, 0));
+    st = (st + 1 == S) ? 0 : st + 1;
   }
 }
 
 template <typename To, int CW>
 __global__ void __launch_bounds__(kThreads) k_dequant_fast(const uint8_t* __restrict__ src, int64_t n, DevCodec c,
-                                                           To* __restrict__ out) {
+                                                           To* __restrict__ out, int S) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int CB = code_chunk_bytes(c);
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem) + threadIdx.x * CB;
   const int64_t tiles = (n + kTileElems - 1) / kTileElems;
+  auto issue = [&](int64_t t, int st) {
+    if (t < tiles) {
+      const int64_t p0 = t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+      if (p0 < n) code_issue(c, s0 + st * kThreads * CB, src, p0);
+    }
+    cp_async_commit();
+  };
+  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+  int st = 0;
   for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    issue(t + (int64_t)(S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
+    cp_async_wait_dyn(S - 1);
     const int64_t p0 = t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
     const int nvalid = (int)max((int64_t)0, min(n - p0, (int64_t)kLaneElems));
-    if (nvalid <= 0) continue;
-    LaneCodes<CW> L;
-    load_lane(c, src, p0, L);
-    float v[kLaneElems];
-    lane_decode<false>(c, L, v);
-    store_chunk(out, p0, n, nvalid, v);
+    if (nvalid > 0) {
+      LaneCodes<CW> L;
+      code_read(c, s0 + st * kThreads * CB, p0, L);
+      float v[kLaneElems];
+      lane_decode<false>(c, L, v);
+      store_chunk(out, p0, n, nvalid, v);
+    }
+    st = (st + 1 == S) ? 0 : st + 1;
   }
+}
+
+static fc_status ensure_smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{kern, dev}];
+  if (bytes > have) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
+  }
+  return FC_OK;
+}
+
+static unsigned resident_grid(const void* kern, int smem, int64_t items, int sms) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)occ * sms));
 }
 
 // --------------------------------------------------------------------------
@@ -82,10 +137,20 @@ fc_status launch_quantize(const void* x, int in_dtype, int64_t n, const fc_codec
   const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)dst % 16 == 0);
   if (allow_fast && fast_group(c) && aligned) {
     const int64_t tiles = (n + kTileElems - 1) / kTileElems;
-    const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)cur_sms() * 8);
     uint8_t* d = (uint8_t*)dst;
     const bool pass = c.kind == FC_KIND_FP16;
-#define FC_QF(T) (pass ? k_quant_fast<T, 16> : k_quant_fast<T, 8>)<<<grid, kThreads, 0, st>>>((const T*)x, n, dc, d, err)
+#define FC_QF(T)                                                                                  \
+  do {                                                                                            \
+    const void* k = pass ? (const void*)k_quant_fast<T, 16> : (const void*)k_quant_fast<T, 8>;    \
+    const int S = sizeof(T) == 4 ? 3 : 4;                                                         \
+    const int smem = S * kThreads * Chunk<T>::kBytes;                                             \
+    FC_TRY(ensure_smem_attr(k, smem));                                                            \
+    const unsigned g = resident_grid(k, smem, tiles, cur_sms());                                  \
+    if (pass)                                                                                     \
+      k_quant_fast<T, 16><<<g, kThreads, smem, st>>>((const T*)x, n, dc, d, err, S);             \
+    else                                                                                          \
+      k_quant_fast<T, 8><<<g, kThreads, smem, st>>>((const T*)x, n, dc, d, err, S);              \
+  } while (0)
     switch (in_dtype) {
       case FC_DTYPE_F32: FC_QF(float); break;
       case FC_DTYPE_F16: FC_QF(__half); break;
@@ -112,9 +177,19 @@ fc_status launch_dequantize(const void* src, int64_t n, const fc_codec& c, void*
   const bool aligned = ((uintptr_t)src % 16 == 0) && ((uintptr_t)out % 16 == 0);
   if (allow_fast && fast_group(c) && aligned) {
     const int64_t tiles = (n + kTileElems - 1) / kTileElems;
-    const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)cur_sms() * 8);
     const bool pass = c.kind == FC_KIND_FP16;
-#define FC_DF(T) (pass ? k_dequant_fast<T, 16> : k_dequant_fast<T, 8>)<<<grid, kThreads, 0, st>>>(s, n, dc, (T*)out)
+    const int S = 4;
+    const int smem = S * kThreads * code_chunk_bytes(dc);
+#define FC_DF(T)                                                                                      \
+  do {                                                                                                \
+    const void* k = pass ? (const void*)k_dequant_fast<T, 16> : (const void*)k_dequant_fast<T, 8>;    \
+    FC_TRY(ensure_smem_attr(k, smem));                                                                \
+    const unsigned g = resident_grid(k, smem, tiles, cur_sms());                                      \
+    if (pass)                                                                                         \
+      k_dequant_fast<T, 16><<<g, kThreads, smem, st>>>(s, n, dc, (T*)out, S);                        \
+    else                                                                                              \
+      k_dequant_fast<T, 8><<<g, kThreads, smem, st>>>(s, n, dc, (T*)out, S);                         \
+  } while (0)
     switch (out_dtype) {
       case FC_DTYPE_F32: FC_DF(float); break;
       case FC_DTYPE_F16: FC_DF(__half); break;

@@ -44,7 +44,7 @@ struct DevCodec {
   int ceil_mode;   // rounding == ceil
   int sb;          // storage bits: 4, 8 or 16 (fp16 passthrough)
   int lpg;         // lanes per group in the fast path (g / 32), 0 if not fast
-  int pad_;
+  int gshift;      // log2(g) when g is a power of two (fast path), else -1
   float qmax_f;    // asym: 2^b-1 ; sym: 2^(b-1)-1
   float qmin_f;    // asym: 0     ; sym: -2^(b-1)
   double qdiv;     // divisor of the raw scale: 2^b-1 (asym) or 2^(b-1)-1 (sym)
@@ -469,8 +469,8 @@ __device__ __forceinline__ void store_lane(const DevCodec& c, uint8_t* buf, int6
 #pragma unroll
   for (int i = 0; i < CW / 4; ++i)
     if (i < nq) st_v4(cp + 16 * i, make_uint4(q.w[4 * i], q.w[4 * i + 1], q.w[4 * i + 2], q.w[4 * i + 3]));
-  if (c.kind == FC_KIND_INT && (lane % c.lpg) == 0) {
-    int64_t grp = p0 / c.g;
+  if (c.kind == FC_KIND_INT && (lane & (c.lpg - 1)) == 0) {
+    const int64_t grp = p0 >> c.gshift;
     reinterpret_cast<__half*>(buf + c.scales_off)[grp] = q.s16;
     if (!c.sym) buf[c.zeros_off + grp] = q.z8;
   }
@@ -501,7 +501,7 @@ __device__ __forceinline__ void load_lane(const DevCodec& c, const uint8_t* buf,
     L.w[4 * i + 3] = u.w;
   }
   if (c.kind == FC_KIND_INT) {
-    const int64_t grp = p0 / c.g;
+    const int64_t grp = p0 >> c.gshift;
     L.s = __half2float(__ldcg(reinterpret_cast<const __half*>(buf + c.scales_off) + grp));
     const uint32_t xr = rep_xor(c);
     L.mz = 8388608.0f + (c.sym ? (float)(1 << (c.bits - 1)) : (float)__ldcg(buf + c.zeros_off + grp));

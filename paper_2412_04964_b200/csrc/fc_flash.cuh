@@ -17,6 +17,7 @@
 #pragma once
 
 #include "fc_codec_dev.cuh"
+#include "fc_stage.cuh"
 
 namespace fc {
 
@@ -33,6 +34,7 @@ struct FlashArgs {
   int64_t slot_bytes;
   int64_t flags_cap;
   uint64_t timeout_ns;
+  int stages;               // cp.async ring depth of the phase-split kernels
   DevCodec c1, c2;
   const void* in[kMaxRanks];
   void* out[kMaxRanks];
@@ -238,40 +240,178 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
 
 // Phase-split kernels (no flags): ordering comes from kernel boundaries
 // (one GPU), stream events (several GPUs, one process) or k_barrier (IPC).
+// Each thread streams its operands through a cp.async ring of a.stages items
+// (fc_stage.cuh), so S items of HBM traffic are in flight per thread.
+
+__device__ __forceinline__ void split_item(const FlashArgs& a, int64_t i, int P, int64_t per_rank, int& r, int& j,
+                                           int& t) {
+  r = a.rank_lo + (int)(i / per_rank);
+  const int64_t rem = i % per_rank;
+  t = (int)(rem / P);
+  j = (r + 1 + (int)(rem % P)) % a.world;
+}
+
 template <typename Tin, int CW>
 __global__ void __launch_bounds__(kThreads) k_scatter(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int CB = Chunk<Tin>::kBytes;
+  const int lane = threadIdx.x & 31;
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem) + threadIdx.x * CB;
+  const int S = a.stages;
   const int P = a.world - 1;
   const int64_t per_rank = (int64_t)P * a.tiles;
   const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * per_rank;
+  auto issue = [&](int64_t i, int st) {
+    if (i < total) {
+      int r, j, t;
+      split_item(a, i, P, per_rank, r, j, t);
+      const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+      const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+      chunk_issue<Tin>(s0 + st * kThreads * CB, reinterpret_cast<const Tin*>(a.in[r]),
+                       (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, lane);
+    }
+    cp_async_commit();
+  };
+  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+  int st = 0;
   for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
-    const int r = a.rank_lo + (int)(i / per_rank);
-    const int64_t rem = i % per_rank;
-    const int t = (int)(rem / P);
-    const int j = (r + 1 + (int)(rem % P)) % a.world;
-    do_scatter<Tin, CW>(a, r, j, t);
+    issue(i + (int64_t)(S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
+    cp_async_wait_dyn(S - 1);
+    int r, j, t;
+    split_item(a, i, P, per_rank, r, j, t);
+    const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+    const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+    float v[kLaneElems];
+    chunk_read<Tin>(s0 + st * kThreads * CB, lane, v);
+    LaneQuant<CW> q;
+    const bool bad = lane_quantize(a.c1, v, nvalid, q);
+    store_lane(a.c1, recv_slot(a, j, r), p0, nvalid, q, lane);
+    if (bad) atomicOr(errw(a, r), make_err(kErrNonFinite, kPhScatter, j, r));
+    st = (st + 1 == S) ? 0 : st + 1;
   }
 }
 
+// bytes of one thread's reduce stage: own input chunk + (world-1) code chunks
+template <typename Tin>
+__host__ __device__ inline int reduce_thread_bytes(const DevCodec& c1, int world) {
+  return Chunk<Tin>::kBytes + (world - 1) * code_chunk_bytes(c1);
+}
+
 template <typename Tin, typename Tout, int CW>
-__global__ void __launch_bounds__(kThreads, 2) k_reduce(FlashArgs a) {
+__global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int TB = reduce_thread_bytes<Tin>(a.c1, a.world);
+  const int CCB = code_chunk_bytes(a.c1);
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem) + threadIdx.x * TB;
+  const int S = a.stages;
   const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * a.tiles;
+  auto issue = [&](int64_t i, int st) {
+    if (i < total) {
+      const int j = a.rank_lo + (int)(i / a.tiles);
+      const int t = (int)(i % a.tiles);
+      const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+      const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+      const uint32_t base = s0 + st * kThreads * TB;
+      chunk_issue<Tin>(base, reinterpret_cast<const Tin*>(a.in[j]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid,
+                       lane);
+      if (nvalid > 0) {
+        uint32_t off = base + Chunk<Tin>::kBytes;
+        for (int s = 0; s < a.world; ++s) {
+          if (s == j) continue;
+          code_issue(a.c1, off, recv_slot(a, j, s), p0);
+          off += CCB;
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+  int st = 0;
   for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
+    issue(i + (int64_t)(S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
+    cp_async_wait_dyn(S - 1);
     const int j = a.rank_lo + (int)(i / a.tiles);
-    do_reduce<Tin, Tout, CW>(a, j, (int)(i % a.tiles));
+    const int t = (int)(i % a.tiles);
+    const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+    const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+    const int64_t idx0 = (int64_t)j * a.seg + a.sub_off + p0;
+    const uint32_t base = s0 + st * kThreads * TB;
+    bool bad = false;
+    float acc[kLaneElems];
+    uint32_t off = base + Chunk<Tin>::kBytes;
+    for (int s = 0; s < a.world; ++s) {  // ascending source rank (collectives.py:182-187)
+      LaneCodes<CW> L;
+      if (s == j) {
+        float v[kLaneElems];
+        chunk_read<Tin>(base, lane, v);
+        LaneQuant<CW> q;
+        bad |= lane_quantize(a.c1, v, nvalid, q);  // own piece: QDQ in registers (collectives.py:364-365)
+        lane_codes_from(a.c1, q, L);
+      } else {
+        if (nvalid > 0) {
+          code_read(a.c1, off, p0, L);
+        } else {
+#pragma unroll
+          for (int w = 0; w < CW; ++w) L.w[w] = 0;
+          L.s = 0.0f;
+          L.mz = 0.0f;
+        }
+        off += CCB;
+      }
+      if (s == 0)
+        lane_decode<false>(a.c1, L, acc);
+      else
+        lane_decode<true>(a.c1, L, acc);
+    }
+    LaneQuant<CW> q2;
+    bad |= lane_quantize(a.c2, acc, nvalid, q2);
+    for (int pp = 1; pp < a.world; ++pp) store_lane(a.c2, gath_slot(a, (j + pp) % a.world, j), p0, nvalid, q2, lane);
+    LaneCodes<CW> L2;
+    lane_codes_from(a.c2, q2, L2);
+    float o[kLaneElems];
+    lane_decode<false>(a.c2, L2, o);  // owner decodes its own payload too (collectives.py:378)
+    if (nvalid > 0) store_chunk(reinterpret_cast<Tout*>(a.out[j]), idx0, a.M, nvalid, o);
+    if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
+    st = (st + 1 == S) ? 0 : st + 1;
   }
 }
 
 template <typename Tout, int CW>
 __global__ void __launch_bounds__(kThreads) k_gather(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int CB = code_chunk_bytes(a.c2);
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem) + threadIdx.x * CB;
+  const int S = a.stages;
   const int P = a.world - 1;
   const int64_t per_rank = (int64_t)P * a.tiles;
   const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * per_rank;
+  auto issue = [&](int64_t i, int st) {
+    if (i < total) {
+      int r, j, t;
+      split_item(a, i, P, per_rank, r, j, t);
+      const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+      if (p0 < a.sub_len) code_issue(a.c2, s0 + st * kThreads * CB, gath_slot(a, r, j), p0);
+    }
+    cp_async_commit();
+  };
+  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+  int st = 0;
   for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
-    const int r = a.rank_lo + (int)(i / per_rank);
-    const int64_t rem = i % per_rank;
-    const int t = (int)(rem / P);
-    const int j = (r + 1 + (int)(rem % P)) % a.world;
-    do_gather<Tout, CW>(a, r, j, t);
+    issue(i + (int64_t)(S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
+    cp_async_wait_dyn(S - 1);
+    int r, j, t;
+    split_item(a, i, P, per_rank, r, j, t);
+    const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
+    const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+    if (nvalid > 0) {
+      LaneCodes<CW> L;
+      code_read(a.c2, s0 + st * kThreads * CB, p0, L);
+      float o[kLaneElems];
+      lane_decode<false>(a.c2, L, o);
+      store_chunk(reinterpret_cast<Tout*>(a.out[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, o);
+    }
+    st = (st + 1 == S) ? 0 : st + 1;
   }
 }
 

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <numeric>
 
 #include "fc_comm.h"
@@ -166,6 +168,63 @@ inline fc_status ipc_barrier(fc_comm* c, const FlashArgs& a, int rank, int phase
   return FC_OK;
 }
 
+
+// ---------------------------------------------------------------- staged launches
+
+inline fc_status ensure_smem(const void* kern, int dev, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{kern, dev}];
+  if (bytes > have) {
+    FC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
+  }
+  return FC_OK;
+}
+
+inline unsigned persistent_grid(const void* kern, int dev, int smem, int64_t items) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)occ * num_sms(dev)));
+}
+
+constexpr int kStageBudget = 200 * 1024;  // dynamic smem per CTA for the cp.async rings
+
+template <typename Tin, int CW>
+fc_status launch_scatter(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
+  const void* kern = (const void*)k_scatter<Tin, CW>;
+  a.stages = Chunk<Tin>::kBytes <= 64 ? 4 : 3;
+  const int smem = a.stages * kThreads * Chunk<Tin>::kBytes;
+  FC_TRY(ensure_smem(kern, dev, smem));
+  k_scatter<Tin, CW><<<persistent_grid(kern, dev, smem, items), kThreads, smem, st>>>(a);
+  ++g_launch_count;
+  return FC_OK;
+}
+
+template <typename Tin, typename Tout, int CW>
+fc_status launch_reduce(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
+  const void* kern = (const void*)k_reduce<Tin, Tout, CW>;
+  const int tb = reduce_thread_bytes<Tin>(a.c1, a.world) * kThreads;
+  a.stages = std::max(1, std::min(3, kStageBudget / tb));
+  const int smem = a.stages * tb;
+  FC_TRY(ensure_smem(kern, dev, smem));
+  k_reduce<Tin, Tout, CW><<<persistent_grid(kern, dev, smem, items), kThreads, smem, st>>>(a);
+  ++g_launch_count;
+  return FC_OK;
+}
+
+template <typename Tout, int CW>
+fc_status launch_gather(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
+  const void* kern = (const void*)k_gather<Tout, CW>;
+  a.stages = 4;
+  const int smem = a.stages * kThreads * code_chunk_bytes(a.c2);
+  FC_TRY(ensure_smem(kern, dev, smem));
+  k_gather<Tout, CW><<<persistent_grid(kern, dev, smem, items), kThreads, smem, st>>>(a);
+  ++g_launch_count;
+  return FC_OK;
+}
+
 template <typename Tin, typename Tout, int CW>
 fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, int64_t n, const fc_flash_cfg* cfg,
                        cudaStream_t* st, int only_rank /* -1: local world */) {
@@ -211,11 +270,11 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
       } else if (p.fast) {
         a.rank_lo = r;
         a.rank_hi = r + 1;
-        k_scatter<Tin, CW><<<grid_for(dev, (int64_t)(N - 1) * a.tiles), kThreads, 0, s>>>(a); ++g_launch_count;
+        FC_TRY((launch_scatter<Tin, CW>(a, dev, s, (int64_t)(N - 1) * a.tiles)));
         FC_TRY(ipc_barrier(c, a, r, 0, s));
-        k_reduce<Tin, Tout, CW><<<grid_for(dev, a.tiles), kThreads, 0, s>>>(a); ++g_launch_count;
+        FC_TRY((launch_reduce<Tin, Tout, CW>(a, dev, s, a.tiles)));
         FC_TRY(ipc_barrier(c, a, r, 1, s));
-        k_gather<Tout, CW><<<grid_for(dev, (int64_t)(N - 1) * a.tiles), kThreads, 0, s>>>(a); ++g_launch_count;
+        FC_TRY((launch_gather<Tout, CW>(a, dev, s, (int64_t)(N - 1) * a.tiles)));
       } else {
         FC_TRY(gen_phase_scatter<Tin>(c, a, r, s));
         FC_TRY(ipc_barrier(c, a, r, 0, s));
@@ -242,29 +301,29 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
       FC_CUDA_TRY(cudaSetDevice(dev));
       a.rank_lo = 0;
       a.rank_hi = N;
-      k_scatter<Tin, CW><<<grid_for(dev, (int64_t)N * (N - 1) * a.tiles), kThreads, 0, st[0]>>>(a); ++g_launch_count;
-      k_reduce<Tin, Tout, CW><<<grid_for(dev, (int64_t)N * a.tiles), kThreads, 0, st[0]>>>(a); ++g_launch_count;
-      k_gather<Tout, CW><<<grid_for(dev, (int64_t)N * (N - 1) * a.tiles), kThreads, 0, st[0]>>>(a); ++g_launch_count;
+      FC_TRY((launch_scatter<Tin, CW>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+      FC_TRY((launch_reduce<Tin, Tout, CW>(a, dev, st[0], (int64_t)N * a.tiles)));
+      FC_TRY((launch_gather<Tout, CW>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
     } else if (p.fast) {
       for (int r = 0; r < N; ++r) {
         FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
         a.rank_lo = r;
         a.rank_hi = r + 1;
-        k_scatter<Tin, CW><<<grid_for(c->devices[r], (int64_t)(N - 1) * a.tiles), kThreads, 0, st[r]>>>(a); ++g_launch_count;
+        FC_TRY((launch_scatter<Tin, CW>(a, c->devices[r], st[r], (int64_t)(N - 1) * a.tiles)));
       }
       FC_TRY(cross_sync(c, st));
       for (int r = 0; r < N; ++r) {
         FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
         a.rank_lo = r;
         a.rank_hi = r + 1;
-        k_reduce<Tin, Tout, CW><<<grid_for(c->devices[r], a.tiles), kThreads, 0, st[r]>>>(a); ++g_launch_count;
+        FC_TRY((launch_reduce<Tin, Tout, CW>(a, c->devices[r], st[r], a.tiles)));
       }
       FC_TRY(cross_sync(c, st));
       for (int r = 0; r < N; ++r) {
         FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
         a.rank_lo = r;
         a.rank_hi = r + 1;
-        k_gather<Tout, CW><<<grid_for(c->devices[r], (int64_t)(N - 1) * a.tiles), kThreads, 0, st[r]>>>(a); ++g_launch_count;
+        FC_TRY((launch_gather<Tout, CW>(a, c->devices[r], st[r], (int64_t)(N - 1) * a.tiles)));
       }
     } else {
       for (int r = 0; r < N; ++r) {
