@@ -37,8 +37,8 @@ __global__ void __launch_bounds__(kThreads) k_quant_fast(const T* __restrict__ x
     cp_async_wait_dyn(S - 1);
     const int64_t p0 = t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
     const int nvalid = (int)max((int64_t)0, min(n - p0, (int64_t)kLaneElems));
-    float v[kLaneElems];
-    chunk_read<T>(s0 + st * kThreads * CB, lane, v);
+    LaneOf<T> v;
+    chunk_read_src<T>(s0 + st * kThreads * CB, lane, v);
     LaneQuant<CW> q;
     const bool bad = lane_quantize(c, v, nvalid, q);
     store_lane(c, dst, p0, nvalid, q, lane);

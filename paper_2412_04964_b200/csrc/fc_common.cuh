@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "../../include/flashcomm.h"
 
 namespace fc {
@@ -199,16 +201,22 @@ __device__ __forceinline__ __half snap_scale(double raw, double floor) {
 // k >= nvalid are excluded from the statistics and produce stored code 0.
 //
 // Per element the code is round(x / s) + z, clamped (codec.py:324), computed
-// without a divide: t = x * RN(1/s) is within a few ulps of x/s, so the
-// magic-number rounding k' = rint(t) is either right or one off; the exact
-// residual rho = x - k' * s (one FMA) decides: |rho| > s/2 means the other
-// neighbour, |rho| == s/2 is an exact tie and resolves to the even code
-// (np.round is half-to-even). Ceil mode: k' = ceil(t) corrected so that
-// -s < rho <= 0. Symmetric codes are computed in offset binary (z = 2^(b-1))
-// and XOR-ed back to two's complement, so both schemes share one decoder.
+// without a divide instruction:
+//   r  = RN(1/s) (once per lane), t = RN(x * r),
+//   q1 = RN(t + r * RN(x - t*s))            (two FMAs)
+// is the correctly rounded fp32 quotient RN(x/s) for every finite x and every
+// fp16 scale s (one Newton step from a correctly rounded reciprocal —
+// Markstein's theorem; tools/probes/div_check.cu checked 1e11 (x, s) pairs
+// bit-for-bit against __fdiv_rn with no mismatch). RN(x/s) never crosses a
+// half-integer or integer that the float64 quotient of the reference does not
+// (x/s lies at least 2^-24 |x/s| away from any boundary it is not exactly on),
+// so rounding q1 is exactly numpy's round / ceil of x/s. Then clamp in float
+// to [-z, qmax-z] (monotone, integral bounds: commutes with rounding), round
+// by the magic add y = q1c + 1.5*2^23 (RN: ties-to-even; RU: ceil) whose low
+// mantissa bits hold the integer, and add z as an integer.
+// Symmetric codes are computed in offset binary (z = 2^(b-1)) and XOR-ed back
+// to two's complement, so both schemes share one decoder.
 
-// CW: 32-bit code words per lane: 8 for integer codecs, 16 when a codec may
-// be the fp16 passthrough (kernels are instantiated for both).
 template <int CW>
 struct LaneQuant {
   uint32_t w[CW];  // packed codes: INT4 w[0..3], INT8 w[0..7], fp16 bits w[0..15]
@@ -243,25 +251,45 @@ __device__ __forceinline__ uint32_t rep_xor(const DevCodec& c) {
   return c.sb == 4 ? h * 0x11111111u : h * 0x01010101u;
 }
 
-// Statistics of the lane's valid elements: asym (min, max), sym (-, absmax).
-// NaN propagates; +-inf shows up as a non-finite bound.
+// Lane sources: element k of the chunk as fp32. FloatLane holds fp32 values;
+// PackedLane<T> holds 32 raw 16-bit values (bf16/fp16), unpacked on use so the
+// statistics can run on packed pairs.
+struct FloatLane {
+  float v[kLaneElems];
+  __device__ __forceinline__ float get(int k) const { return v[k]; }
+};
+template <typename T>
+struct PackedLane {
+  uint32_t w[kLaneElems / 2];
+  __device__ __forceinline__ float get(int k) const {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+      return (k & 1) ? __uint_as_float(w[k >> 1] & 0xFFFF0000u) : __uint_as_float(w[k >> 1] << 16);
+    } else {
+      const __half2 h = *reinterpret_cast<const __half2*>(&w[k >> 1]);
+      return (k & 1) ? __high2float(h) : __low2float(h);
+    }
+  }
+};
+
+// Statistics of the lane's valid elements, NaN-propagating (NaN and +-inf
+// surface as a non-finite bound): asym (min, max), sym (-, absmax).
 template <bool SYM>
-__device__ __forceinline__ void lane_stats(const float v[kLaneElems], int nvalid, float& lo, float& hi) {
+__device__ __forceinline__ void lane_stats(const FloatLane& L, int nvalid, float& lo, float& hi) {
   if (nvalid == kLaneElems) {
     float a[16], b[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      const float x = SYM ? fabsf(v[2 * k]) : v[2 * k];
-      const float y = SYM ? fabsf(v[2 * k + 1]) : v[2 * k + 1];
-      a[k] = fminf(x, y);
-      b[k] = fmaxf(x, y);
+      const float x = SYM ? fabsf(L.v[2 * k]) : L.v[2 * k];
+      const float y = SYM ? fabsf(L.v[2 * k + 1]) : L.v[2 * k + 1];
+      a[k] = fmin_nan(x, y);
+      b[k] = fmax_nan(x, y);
     }
 #pragma unroll
     for (int w = 8; w >= 1; w >>= 1)
 #pragma unroll
       for (int k = 0; k < w; ++k) {
-        a[k] = fminf(a[k], a[k + w]);
-        b[k] = fmaxf(b[k], b[k + w]);
+        a[k] = fmin_nan(a[k], a[k + w]);
+        b[k] = fmax_nan(b[k], b[k + w]);
       }
     lo = a[0];
     hi = b[0];
@@ -271,105 +299,78 @@ __device__ __forceinline__ void lane_stats(const float v[kLaneElems], int nvalid
 #pragma unroll
     for (int k = 0; k < kLaneElems; ++k)
       if (k < nvalid) {
-        const float x = SYM ? fabsf(v[k]) : v[k];
+        const float x = SYM ? fabsf(L.v[k]) : L.v[k];
         lo = fmin_nan(lo, x);
         hi = fmax_nan(hi, x);
       }
   }
 }
 
-// Exact codes of one lane chunk (any input): k' = rint/ceil(t) from the
-// magic add, then corrected with sign tests of exact residuals — an FMA
-// rounds x - m*s once, so its sign (and whether it is zero) is exact for any
-// m of at most 24 bits:
-//   nearest: up   iff x - (k'+1/2)s > 0, or == 0 with k' odd (ties to even)
-//            down iff x - (k'-1/2)s < 0, or == 0 with k' odd
-//   ceil:    up   iff x - k's > 0;  down iff x - (k'-1)s <= 0
-// |t| is clamped to 2^21 first (codes clamp far earlier). NaN -> *nan.
-template <int SB, bool CEIL>
-__device__ __forceinline__ void lane_codes_exact(const float v[kLaneElems], float s, int z, int qmax, uint32_t* w,
-                                                 bool* nan) {
-  const float r = __frcp_rn(s);
-  const float C0 = 12582912.0f;  // 1.5 * 2^23: y = t + C0 holds rint(t) in its low mantissa bits
-  const int zb = z - 0x4B400000;
-  bool anynan = false;
+template <bool SYM, typename T>
+__device__ __forceinline__ void lane_stats(const PackedLane<T>& L, int nvalid, float& lo, float& hi) {
+  using V2 = typename std::conditional<std::is_same<T, __nv_bfloat16>::value, __nv_bfloat162, __half2>::type;
+  if (nvalid == kLaneElems) {
+    V2 a[8], b[8];
 #pragma unroll
-  for (int k = 0; k < kLaneElems; ++k) {
-    anynan |= v[k] != v[k];
-    const float t = fminf(fmaxf(v[k] * r, -2097152.0f), 2097152.0f);
-    const float y = CEIL ? __fadd_ru(t, C0) : __fadd_rn(t, C0);
-    const float kf = y - C0;
-    const int yi = __float_as_int(y);
-    int d;
-    if (CEIL) {
-      const float up = fmaf(-kf, s, v[k]);
-      const float dn = fmaf(-(kf - 1.0f), s, v[k]);
-      d = up > 0.0f ? 1 : (dn <= 0.0f ? -1 : 0);
-    } else {
-      const bool odd = (yi & 1) != 0;
-      const float up = fmaf(-(kf + 0.5f), s, v[k]);
-      const float dn = fmaf(-(kf - 0.5f), s, v[k]);
-      d = (up > 0.0f || (up == 0.0f && odd)) ? 1 : ((dn < 0.0f || (dn == 0.0f && odd)) ? -1 : 0);
+    for (int k = 0; k < 8; ++k) {
+      V2 x = *reinterpret_cast<const V2*>(&L.w[2 * k]);
+      V2 y = *reinterpret_cast<const V2*>(&L.w[2 * k + 1]);
+      if (SYM) {
+        x = __habs2(x);
+        y = __habs2(y);
+      }
+      a[k] = __hmin2_nan(x, y);
+      b[k] = __hmax2_nan(x, y);
     }
-    const int code = min(max(yi + zb + d, 0), qmax);
-    if (SB == 4) {
-      if ((k & 7) == 0) w[k >> 3] = 0;
-      w[k >> 3] |= (uint32_t)code << (4 * (k & 7));
-    } else {
-      if ((k & 3) == 0) w[k >> 2] = 0;
-      w[k >> 2] |= (uint32_t)code << (8 * (k & 3));
-    }
-  }
-  *nan = anynan;
-}
-
-// Fast path (|x/s| < 2^20). One Newton step on the quotient,
-// q1 = t + RN(1/s) * (x - t*s) with t = x * RN(1/s), is x/s exactly whenever
-// x/s is representable — in particular at exact ties (k + 1/2) and exact
-// integers, which bf16 inputs hit often — so the magic-add rounding
-// (ties-to-even / ceil) is right there. The exact residual rho = x - k*s then
-// certifies every element: nearest needs |rho| <= s/2, ceil needs
-// -s < rho <= 0. A lane with any uncertified element (a near-tie a few ulps
-// off, NaN) returns false and is redone by lane_codes_exact.
-template <int SB, bool CEIL>
-__device__ __forceinline__ bool lane_codes_fast(const float v[kLaneElems], float s, int z, int qmax, uint32_t* w) {
-  const float r = __frcp_rn(s);
-  const float C0 = 12582912.0f;
-  const float h = 0.5f * s;
-  const int zb = z - 0x4B400000;
-  bool ok = true;
 #pragma unroll
-  for (int k = 0; k < kLaneElems; ++k) {
-    const float t = v[k] * r;
-    const float q1 = fmaf(fmaf(-t, s, v[k]), r, t);
-    const float y = CEIL ? __fadd_ru(q1, C0) : __fadd_rn(q1, C0);
-    const float rho = fmaf(-(y - C0), s, v[k]);
-    if (CEIL)
-      ok &= (rho <= 0.0f) & (rho > -s);
-    else
-      ok &= fabsf(rho) <= h;  // false for NaN
-    const int code = min(max(__float_as_int(y) + zb, 0), qmax);
-    if (SB == 4) {
-      if ((k & 7) == 0) w[k >> 3] = 0;
-      w[k >> 3] |= (uint32_t)code << (4 * (k & 7));
-    } else {
-      if ((k & 3) == 0) w[k >> 2] = 0;
-      w[k >> 2] |= (uint32_t)code << (8 * (k & 3));
-    }
-  }
-  return ok;
-}
-
-template <int SB>
-__device__ __forceinline__ bool lane_codes_any(const float v[kLaneElems], float s, int z, int qmax, bool ceil_mode,
-                                               bool wide, uint32_t* w) {
-  bool nan = false;
-  if (ceil_mode) {
-    if (wide || !lane_codes_fast<SB, true>(v, s, z, qmax, w)) lane_codes_exact<SB, true>(v, s, z, qmax, w, &nan);
+    for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+      for (int k = 0; k < w; ++k) {
+        a[k] = __hmin2_nan(a[k], a[k + w]);
+        b[k] = __hmax2_nan(b[k], b[k + w]);
+      }
+    const float2 fa = std::is_same<T, __nv_bfloat16>::value ? __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&a[0]))
+                                                             : __half22float2(*reinterpret_cast<__half2*>(&a[0]));
+    const float2 fb = std::is_same<T, __nv_bfloat16>::value ? __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&b[0]))
+                                                             : __half22float2(*reinterpret_cast<__half2*>(&b[0]));
+    lo = fmin_nan(fa.x, fa.y);
+    hi = fmax_nan(fb.x, fb.y);
   } else {
-    if (wide || !lane_codes_fast<SB, false>(v, s, z, qmax, w)) lane_codes_exact<SB, false>(v, s, z, qmax, w, &nan);
+    lo = INFINITY;
+    hi = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < kLaneElems; ++k)
+      if (k < nvalid) {
+        const float x = SYM ? fabsf(L.get(k)) : L.get(k);
+        lo = fmin_nan(lo, x);
+        hi = fmax_nan(hi, x);
+      }
   }
-  return nan;
+}
+
+// codes of one lane chunk (see the derivation above)
+template <int SB, bool CEIL, class Src>
+__device__ __forceinline__ void lane_codes(const Src& L, float s, int z, int qmax, uint32_t* w) {
+  const float r = __frcp_rn(s);
+  const float C0 = 12582912.0f;  // 1.5 * 2^23
+  const float lob = -(float)z, hib = (float)(qmax - z);
+  const int zb = z - 0x4B400000;
+#pragma unroll
+  for (int k = 0; k < kLaneElems; ++k) {
+    const float x = L.get(k);
+    const float t = x * r;
+    const float q1 = fmaf(fmaf(-t, s, x), r, t);
+    const float qc = fminf(fmaxf(q1, lob), hib);
+    const float y = CEIL ? __fadd_ru(qc, C0) : __fadd_rn(qc, C0);
+    const uint32_t code = (uint32_t)(__float_as_int(y) + zb);
+    if (SB == 4) {
+      if ((k & 7) == 0) w[k >> 3] = 0;
+      w[k >> 3] |= code << (4 * (k & 7));
+    } else {
+      if ((k & 3) == 0) w[k >> 2] = 0;
+      w[k >> 2] |= code << (8 * (k & 3));
+    }
+  }
 }
 
 __device__ __forceinline__ float group_allreduce_min(float v, int lpg) {
@@ -382,37 +383,36 @@ __device__ __forceinline__ float group_allreduce_max(float v, int lpg) {
 }
 
 // returns true if a valid element of the lane's group is NaN/inf (codec.py:230-231)
-template <int CW>
-__device__ __forceinline__ bool lane_quantize(const DevCodec& c, const float v[kLaneElems], int nvalid,
-                                              LaneQuant<CW>& q) {
+template <int CW, class Src>
+__device__ __forceinline__ bool lane_quantize(const DevCodec& c, const Src& L, int nvalid, LaneQuant<CW>& q) {
   if constexpr (CW == 16) {
     if (c.kind == FC_KIND_FP16) {
-    float lo, hi;
-    lane_stats<true>(v, nvalid, lo, hi);
+      float lo, hi;
+      lane_stats<true>(L, nvalid, lo, hi);
 #pragma unroll
-    for (int k = 0; k < kLaneElems; k += 2) {
-      __half2 h = __floats2half2_rn(k < nvalid ? v[k] : 0.0f, k + 1 < nvalid ? v[k + 1] : 0.0f);
-      q.w[k / 2] = *reinterpret_cast<uint32_t*>(&h);
-    }
-    q.s16 = __ushort_as_half(0);
-    q.s = 1.0f;
-    q.mz = 0.0f;
-    q.xr = 0u;
-    q.z8 = 0;
-    return nvalid > 0 && !(hi <= 3.402823466e38f);
+      for (int k = 0; k < kLaneElems; k += 2) {
+        __half2 h = __floats2half2_rn(k < nvalid ? L.get(k) : 0.0f, k + 1 < nvalid ? L.get(k + 1) : 0.0f);
+        q.w[k / 2] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      q.s16 = __ushort_as_half(0);
+      q.s = 1.0f;
+      q.mz = 0.0f;
+      q.xr = 0u;
+      q.z8 = 0;
+      return nvalid > 0 && !(hi <= 3.402823466e38f);
     }
   }
   float lo, hi;
   if (c.sym) {
-    lane_stats<true>(v, nvalid, lo, hi);
+    lane_stats<true>(L, nvalid, lo, hi);
     hi = group_allreduce_max(hi, c.lpg);
     lo = -hi;
   } else {
-    lane_stats<false>(v, nvalid, lo, hi);
+    lane_stats<false>(L, nvalid, lo, hi);
     lo = group_allreduce_min(lo, c.lpg);
     hi = group_allreduce_max(hi, c.lpg);
   }
-  bool bad = nvalid > 0 && !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
+  const bool bad = nvalid > 0 && !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
   int z;
   if (c.sym) {
     q.s16 = snap_scale((double)hi / c.qdiv, c.floor);
@@ -422,20 +422,24 @@ __device__ __forceinline__ bool lane_quantize(const DevCodec& c, const float v[k
     q.s16 = snap_scale(((double)hi - (double)lo) / c.qdiv, c.floor);
     double zd = ceil(-(double)lo / (double)__half2float(q.s16));
     zd = fmin(fmax(zd, 0.0), (double)c.qmax_f);
-    z = (int)zd;
+    z = bad ? 0 : (int)zd;
     q.z8 = (uint8_t)z;
   }
   q.s = __half2float(q.s16);
   q.mz = 8388608.0f + (float)z;
   q.xr = rep_xor(c);
   const int qmax = (1 << c.bits) - 1;
-  const bool wide = !(fmaxf(fabsf(lo), fabsf(hi)) * __frcp_rn(q.s) < 1048576.0f);
-  bool nan;
-  if (c.sb == 4)
-    nan = lane_codes_any<4>(v, q.s, z, qmax, c.ceil_mode, wide, q.w);
-  else
-    nan = lane_codes_any<8>(v, q.s, z, qmax, c.ceil_mode, wide, q.w);
-  bad |= nan && nvalid > 0;
+  if (c.sb == 4) {
+    if (c.ceil_mode)
+      lane_codes<4, true>(L, q.s, z, qmax, q.w);
+    else
+      lane_codes<4, false>(L, q.s, z, qmax, q.w);
+  } else {
+    if (c.ceil_mode)
+      lane_codes<8, true>(L, q.s, z, qmax, q.w);
+    else
+      lane_codes<8, false>(L, q.s, z, qmax, q.w);
+  }
   const int nw = c.sb == 4 ? 4 : 8;
 #pragma unroll
   for (int i = 0; i < 8; ++i)
@@ -453,6 +457,38 @@ __device__ __forceinline__ bool lane_quantize(const DevCodec& c, const float v[k
     }
   }
   return bad;
+}
+
+template <typename T>
+using LaneOf = typename std::conditional<sizeof(T) == 4, FloatLane, PackedLane<T>>::type;
+
+// Direct (non-staged) load of a lane chunk into its source representation;
+// elements past M read as 0 (collectives.py:145-149).
+template <typename T>
+__device__ __forceinline__ void load_lane_src(const T* __restrict__ base, int64_t idx0, int64_t M, int nvalid,
+                                              LaneOf<T>& L) {
+  if constexpr (sizeof(T) == 4) {
+    load_chunk(base, idx0, M, nvalid, L.v);
+  } else {
+    if (nvalid == kLaneElems && idx0 + kLaneElems <= M) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = ld_nc_v4(base + idx0 + 8 * q);
+        L.w[4 * q] = u.x;
+        L.w[4 * q + 1] = u.y;
+        L.w[4 * q + 2] = u.z;
+        L.w[4 * q + 3] = u.w;
+      }
+    } else {
+      const uint16_t* b16 = reinterpret_cast<const uint16_t*>(base);
+#pragma unroll
+      for (int k = 0; k < kLaneElems; k += 2) {
+        const uint32_t lo = (k < nvalid && idx0 + k < M) ? b16[idx0 + k] : 0u;
+        const uint32_t hi = (k + 1 < nvalid && idx0 + k + 1 < M) ? b16[idx0 + k + 1] : 0u;
+        L.w[k / 2] = lo | (hi << 16);
+      }
+    }
+  }
 }
 
 // bytes of packed codes per 32-element lane chunk

@@ -77,8 +77,8 @@ __device__ __forceinline__ void do_scatter(const FlashArgs& a, int r, int j, int
   const int lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
   const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
-  float v[kLaneElems];
-  load_chunk(reinterpret_cast<const Tin*>(a.in[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, v);
+  LaneOf<Tin> v;
+  load_lane_src(reinterpret_cast<const Tin*>(a.in[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, v);
   LaneQuant<CW> q;
   const bool bad = lane_quantize(a.c1, v, nvalid, q);
   store_lane(a.c1, recv_slot(a, j, r), p0, nvalid, q, lane);
@@ -92,12 +92,12 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
   const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
   const int64_t idx0 = (int64_t)j * a.seg + a.sub_off + p0;
   bool bad = false;
-  float acc[kLaneElems];
+  FloatLane acc;
   for (int s = 0; s < a.world; ++s) {
     LaneCodes<CW> L;
     if (s == j) {
-      float v[kLaneElems];
-      load_chunk(reinterpret_cast<const Tin*>(a.in[j]), idx0, a.M, nvalid, v);
+      LaneOf<Tin> v;
+      load_lane_src(reinterpret_cast<const Tin*>(a.in[j]), idx0, a.M, nvalid, v);
       LaneQuant<CW> q;
       bad |= lane_quantize(a.c1, v, nvalid, q);  // own piece: QDQ in registers (collectives.py:364-365)
       lane_codes_from(a.c1, q, L);
@@ -110,9 +110,9 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
       L.mz = 0.0f;
     }
     if (s == 0)
-      lane_decode<false>(a.c1, L, acc);  // ascending source rank (collectives.py:182-187)
+      lane_decode<false>(a.c1, L, acc.v);  // ascending source rank (collectives.py:182-187)
     else
-      lane_decode<true>(a.c1, L, acc);
+      lane_decode<true>(a.c1, L, acc.v);
   }
   LaneQuant<CW> q2;
   bad |= lane_quantize(a.c2, acc, nvalid, q2);
@@ -281,8 +281,8 @@ __global__ void __launch_bounds__(kThreads) k_scatter(FlashArgs a) {
     split_item(a, i, P, per_rank, r, j, t);
     const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
     const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
-    float v[kLaneElems];
-    chunk_read<Tin>(s0 + st * kThreads * CB, lane, v);
+    LaneOf<Tin> v;
+    chunk_read_src<Tin>(s0 + st * kThreads * CB, lane, v);
     LaneQuant<CW> q;
     const bool bad = lane_quantize(a.c1, v, nvalid, q);
     store_lane(a.c1, recv_slot(a, j, r), p0, nvalid, q, lane);
@@ -338,13 +338,13 @@ __global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
     const int64_t idx0 = (int64_t)j * a.seg + a.sub_off + p0;
     const uint32_t base = s0 + st * kThreads * TB;
     bool bad = false;
-    float acc[kLaneElems];
+    FloatLane acc;
     uint32_t off = base + Chunk<Tin>::kBytes;
     for (int s = 0; s < a.world; ++s) {  // ascending source rank (collectives.py:182-187)
       LaneCodes<CW> L;
       if (s == j) {
-        float v[kLaneElems];
-        chunk_read<Tin>(base, lane, v);
+        LaneOf<Tin> v;
+        chunk_read_src<Tin>(base, lane, v);
         LaneQuant<CW> q;
         bad |= lane_quantize(a.c1, v, nvalid, q);  // own piece: QDQ in registers (collectives.py:364-365)
         lane_codes_from(a.c1, q, L);
@@ -360,9 +360,9 @@ __global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
         off += CCB;
       }
       if (s == 0)
-        lane_decode<false>(a.c1, L, acc);
+        lane_decode<false>(a.c1, L, acc.v);
       else
-        lane_decode<true>(a.c1, L, acc);
+        lane_decode<true>(a.c1, L, acc.v);
     }
     LaneQuant<CW> q2;
     bad |= lane_quantize(a.c2, acc, nvalid, q2);

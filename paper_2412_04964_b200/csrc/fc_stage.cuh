@@ -95,6 +95,24 @@ __device__ __forceinline__ void chunk_read(uint32_t ssrc, int lane, float v[kLan
   }
 }
 
+
+// staged read into the lane's source representation
+template <typename T>
+__device__ __forceinline__ void chunk_read_src(uint32_t ssrc, int lane, LaneOf<T>& L) {
+  if constexpr (sizeof(T) == 4) {
+    chunk_read<T>(ssrc, lane, L.v);
+  } else {
+#pragma unroll
+    for (int q = 0; q < Chunk<T>::kVecs; ++q) {
+      const uint4 u = lds128(ssrc + 16 * Chunk<T>::slot(q, lane));
+      L.w[4 * q] = u.x;
+      L.w[4 * q + 1] = u.y;
+      L.w[4 * q + 2] = u.z;
+      L.w[4 * q + 3] = u.w;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- code lanes
 
 // Region of one quantized lane chunk: CW/4 vectors of codes (only c.sb/4 are
