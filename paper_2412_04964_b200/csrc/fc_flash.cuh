@@ -240,15 +240,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
 
 // Phase-split kernels (no flags): ordering comes from kernel boundaries
 // (one GPU), stream events (several GPUs, one process) or k_barrier (IPC).
-// Each thread streams its operands through a cp.async ring of a.stages items
-// (fc_stage.cuh), so S items of HBM traffic are in flight per thread.
+// Grids are 2-D: blockIdx.y names the (rank, peer) pair or the owning rank,
+// blockIdx.x strides over tiles, so no item index is ever divided. Each
+// thread streams its operands through a cp.async ring of a.stages tiles
+// (fc_stage.cuh), keeping that many tiles of HBM traffic in flight.
 
-__device__ __forceinline__ void split_item(const FlashArgs& a, int64_t i, int P, int64_t per_rank, int& r, int& j,
-                                           int& t) {
-  r = a.rank_lo + (int)(i / per_rank);
-  const int64_t rem = i % per_rank;
-  t = (int)(rem / P);
-  j = (r + 1 + (int)(rem % P)) % a.world;
+// blockIdx.y -> (r, j) with j = r+1+jj (mod world), for ranks [rank_lo, rank_hi)
+__device__ __forceinline__ void pair_of(const FlashArgs& a, int y, int& r, int& j) {
+  const int P = a.world - 1;
+  r = a.rank_lo + y / P;
+  j = r + 1 + y % P;
+  if (j >= a.world) j -= a.world;
+}
+
+__device__ __forceinline__ int lane_valid(int64_t len, int64_t p0) {
+  const int64_t d = len - p0;
+  return d <= 0 ? 0 : (d >= kLaneElems ? kLaneElems : (int)d);
 }
 
 template <typename Tin, int CW>
@@ -258,37 +265,35 @@ __global__ void __launch_bounds__(kThreads) k_scatter(FlashArgs a) {
   const int lane = threadIdx.x & 31;
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem) + threadIdx.x * CB;
   const int S = a.stages;
-  const int P = a.world - 1;
-  const int64_t per_rank = (int64_t)P * a.tiles;
-  const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * per_rank;
-  auto issue = [&](int64_t i, int st) {
-    if (i < total) {
-      int r, j, t;
-      split_item(a, i, P, per_rank, r, j, t);
-      const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
-      const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
-      chunk_issue<Tin>(s0 + st * kThreads * CB, reinterpret_cast<const Tin*>(a.in[r]),
-                       (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, lane);
+  int r, j;
+  pair_of(a, blockIdx.y, r, j);
+  const Tin* src = reinterpret_cast<const Tin*>(a.in[r]) + (int64_t)j * a.seg + a.sub_off;
+  const int64_t Mrel = a.M - ((int64_t)j * a.seg + a.sub_off);  // elements of `src` before the padding
+  uint8_t* dst = recv_slot(a, j, r);
+  const int tx = threadIdx.x * kLaneElems;
+  auto issue = [&](int t, int st) {
+    if (t < a.tiles) {
+      const int64_t p0 = (int64_t)t * kTileElems + tx;
+      chunk_issue<Tin>(s0 + st * kThreads * CB, src, p0, Mrel, lane_valid(a.sub_len, p0), lane);
     }
     cp_async_commit();
   };
-  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + k * gridDim.x, k);
   int st = 0;
-  for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
-    issue(i + (int64_t)(S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
+  bool bad = false;
+  for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+    issue(t + (S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
     cp_async_wait_dyn(S - 1);
-    int r, j, t;
-    split_item(a, i, P, per_rank, r, j, t);
-    const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
-    const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+    const int64_t p0 = (int64_t)t * kTileElems + tx;
+    const int nvalid = lane_valid(a.sub_len, p0);
     LaneOf<Tin> v;
     chunk_read_src<Tin>(s0 + st * kThreads * CB, lane, v);
     LaneQuant<CW> q;
-    const bool bad = lane_quantize(a.c1, v, nvalid, q);
-    store_lane(a.c1, recv_slot(a, j, r), p0, nvalid, q, lane);
-    if (bad) atomicOr(errw(a, r), make_err(kErrNonFinite, kPhScatter, j, r));
+    bad |= lane_quantize(a.c1, v, nvalid, q);
+    store_lane(a.c1, dst, p0, nvalid, q, lane);
     st = (st + 1 == S) ? 0 : st + 1;
   }
+  if (bad) atomicOr(errw(a, r), make_err(kErrNonFinite, kPhScatter, j, r));
 }
 
 // bytes of one thread's reduce stage: own input chunk + (world-1) code chunks
@@ -305,16 +310,17 @@ __global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
   const int CCB = code_chunk_bytes(a.c1);
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem) + threadIdx.x * TB;
   const int S = a.stages;
-  const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * a.tiles;
-  auto issue = [&](int64_t i, int st) {
-    if (i < total) {
-      const int j = a.rank_lo + (int)(i / a.tiles);
-      const int t = (int)(i % a.tiles);
-      const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
-      const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+  const int j = a.rank_lo + blockIdx.y;  // owner of the segment
+  const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
+  const Tin* own = reinterpret_cast<const Tin*>(a.in[j]) + seg0;
+  const int64_t Mrel = a.M - seg0;
+  const int tx = threadIdx.x * kLaneElems;
+  auto issue = [&](int t, int st) {
+    if (t < a.tiles) {
+      const int64_t p0 = (int64_t)t * kTileElems + tx;
+      const int nvalid = lane_valid(a.sub_len, p0);
       const uint32_t base = s0 + st * kThreads * TB;
-      chunk_issue<Tin>(base, reinterpret_cast<const Tin*>(a.in[j]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid,
-                       lane);
+      chunk_issue<Tin>(base, own, p0, Mrel, nvalid, lane);
       if (nvalid > 0) {
         uint32_t off = base + Chunk<Tin>::kBytes;
         for (int s = 0; s < a.world; ++s) {
@@ -326,39 +332,51 @@ __global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
     }
     cp_async_commit();
   };
-  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + k * gridDim.x, k);
   int st = 0;
-  for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
-    issue(i + (int64_t)(S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
+  bool bad = false;
+  for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+    issue(t + (S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
     cp_async_wait_dyn(S - 1);
-    const int j = a.rank_lo + (int)(i / a.tiles);
-    const int t = (int)(i % a.tiles);
-    const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
-    const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
-    const int64_t idx0 = (int64_t)j * a.seg + a.sub_off + p0;
+    const int64_t p0 = (int64_t)t * kTileElems + tx;
+    const int nvalid = lane_valid(a.sub_len, p0);
     const uint32_t base = s0 + st * kThreads * TB;
-    bool bad = false;
-    FloatLane acc;
-    uint32_t off = base + Chunk<Tin>::kBytes;
-    for (int s = 0; s < a.world; ++s) {  // ascending source rank (collectives.py:182-187)
+    // own piece: stage-1 QDQ in registers (collectives.py:364-365)
+    FloatLane mine;
+    {
+      LaneOf<Tin> v;
+      chunk_read_src<Tin>(base, lane, v);
+      LaneQuant<CW> q;
+      bad |= lane_quantize(a.c1, v, nvalid, q);
       LaneCodes<CW> L;
-      if (s == j) {
-        LaneOf<Tin> v;
-        chunk_read_src<Tin>(base, lane, v);
-        LaneQuant<CW> q;
-        bad |= lane_quantize(a.c1, v, nvalid, q);  // own piece: QDQ in registers (collectives.py:364-365)
-        lane_codes_from(a.c1, q, L);
-      } else {
-        if (nvalid > 0) {
-          code_read(a.c1, off, p0, L);
-        } else {
+      lane_codes_from(a.c1, q, L);
+      lane_decode<false>(a.c1, L, mine.v);
+    }
+    // fp32 sum in ascending source rank (collectives.py:182-187)
+    FloatLane acc;
+    if (j == 0) {
 #pragma unroll
-          for (int w = 0; w < CW; ++w) L.w[w] = 0;
-          L.s = 0.0f;
-          L.mz = 0.0f;
+      for (int k = 0; k < kLaneElems; ++k) acc.v[k] = mine.v[k];
+    }
+    uint32_t off = base + Chunk<Tin>::kBytes;
+    for (int s = 0; s < a.world; ++s) {
+      if (s == j) {
+        if (s != 0) {
+#pragma unroll
+          for (int k = 0; k < kLaneElems; ++k) acc.v[k] += mine.v[k];
         }
-        off += CCB;
+        continue;
       }
+      LaneCodes<CW> L;
+      if (nvalid > 0) {
+        code_read(a.c1, off, p0, L);
+      } else {
+#pragma unroll
+        for (int w = 0; w < CW; ++w) L.w[w] = 0;
+        L.s = 0.0f;
+        L.mz = 0.0f;
+      }
+      off += CCB;
       if (s == 0)
         lane_decode<false>(a.c1, L, acc.v);
       else
@@ -366,15 +384,19 @@ __global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
     }
     LaneQuant<CW> q2;
     bad |= lane_quantize(a.c2, acc, nvalid, q2);
-    for (int pp = 1; pp < a.world; ++pp) store_lane(a.c2, gath_slot(a, (j + pp) % a.world, j), p0, nvalid, q2, lane);
+    for (int p = j + 1;; ++p) {  // every peer's gather slot [j]
+      if (p == a.world) p = 0;
+      if (p == j) break;
+      store_lane(a.c2, gath_slot(a, p, j), p0, nvalid, q2, lane);
+    }
     LaneCodes<CW> L2;
     lane_codes_from(a.c2, q2, L2);
     float o[kLaneElems];
     lane_decode<false>(a.c2, L2, o);  // owner decodes its own payload too (collectives.py:378)
-    if (nvalid > 0) store_chunk(reinterpret_cast<Tout*>(a.out[j]), idx0, a.M, nvalid, o);
-    if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
+    if (nvalid > 0) store_chunk(reinterpret_cast<Tout*>(a.out[j]), seg0 + p0, a.M, nvalid, o);
     st = (st + 1 == S) ? 0 : st + 1;
   }
+  if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
 }
 
 template <typename Tout, int CW>
@@ -383,33 +405,32 @@ __global__ void __launch_bounds__(kThreads) k_gather(FlashArgs a) {
   const int CB = code_chunk_bytes(a.c2);
   const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem) + threadIdx.x * CB;
   const int S = a.stages;
-  const int P = a.world - 1;
-  const int64_t per_rank = (int64_t)P * a.tiles;
-  const int64_t total = (int64_t)(a.rank_hi - a.rank_lo) * per_rank;
-  auto issue = [&](int64_t i, int st) {
-    if (i < total) {
-      int r, j, t;
-      split_item(a, i, P, per_rank, r, j, t);
-      const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
-      if (p0 < a.sub_len) code_issue(a.c2, s0 + st * kThreads * CB, gath_slot(a, r, j), p0);
+  int r, j;
+  pair_of(a, blockIdx.y, r, j);
+  const uint8_t* src = gath_slot(a, r, j);
+  const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
+  Tout* out = reinterpret_cast<Tout*>(a.out[r]);
+  const int tx = threadIdx.x * kLaneElems;
+  auto issue = [&](int t, int st) {
+    if (t < a.tiles) {
+      const int64_t p0 = (int64_t)t * kTileElems + tx;
+      if (p0 < a.sub_len) code_issue(a.c2, s0 + st * kThreads * CB, src, p0);
     }
     cp_async_commit();
   };
-  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + (int64_t)k * gridDim.x, k);
+  for (int k = 0; k < S - 1; ++k) issue(blockIdx.x + k * gridDim.x, k);
   int st = 0;
-  for (int64_t i = blockIdx.x; i < total; i += gridDim.x) {
-    issue(i + (int64_t)(S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
+  for (int t = blockIdx.x; t < a.tiles; t += gridDim.x) {
+    issue(t + (S - 1) * gridDim.x, st == 0 ? S - 1 : st - 1);
     cp_async_wait_dyn(S - 1);
-    int r, j, t;
-    split_item(a, i, P, per_rank, r, j, t);
-    const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
-    const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
+    const int64_t p0 = (int64_t)t * kTileElems + tx;
+    const int nvalid = lane_valid(a.sub_len, p0);
     if (nvalid > 0) {
       LaneCodes<CW> L;
       code_read(a.c2, s0 + st * kThreads * CB, p0, L);
       float o[kLaneElems];
       lane_decode<false>(a.c2, L, o);
-      store_chunk(reinterpret_cast<Tout*>(a.out[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, o);
+      store_chunk(out, seg0 + p0, a.M, nvalid, o);
     }
     st = (st + 1 == S) ? 0 : st + 1;
   }

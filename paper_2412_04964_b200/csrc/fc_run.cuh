@@ -189,6 +189,15 @@ inline unsigned persistent_grid(const void* kern, int dev, int smem, int64_t ite
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)occ * num_sms(dev)));
 }
 
+// 2-D grid: y = ydim (rank pairs / owners), x strides over tiles; all CTAs resident
+inline dim3 grid2d(const void* kern, int dev, int smem, int tiles, int ydim) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  const int64_t total = (int64_t)occ * num_sms(dev);
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(tiles, (total + ydim - 1) / ydim));
+  return dim3((unsigned)gx, (unsigned)ydim);
+}
+
 constexpr int kStageBudget = 200 * 1024;  // dynamic smem per CTA for the cp.async rings
 
 template <typename Tin, int CW>
@@ -197,7 +206,7 @@ fc_status launch_scatter(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
   a.stages = Chunk<Tin>::kBytes <= 64 ? 4 : 3;
   const int smem = a.stages * kThreads * Chunk<Tin>::kBytes;
   FC_TRY(ensure_smem(kern, dev, smem));
-  k_scatter<Tin, CW><<<persistent_grid(kern, dev, smem, items), kThreads, smem, st>>>(a);
+  k_scatter<Tin, CW><<<grid2d(kern, dev, smem, a.tiles, (a.rank_hi - a.rank_lo) * (a.world - 1)), kThreads, smem, st>>>(a);
   ++g_launch_count;
   return FC_OK;
 }
@@ -209,7 +218,7 @@ fc_status launch_reduce(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
   a.stages = std::max(1, std::min(3, kStageBudget / tb));
   const int smem = a.stages * tb;
   FC_TRY(ensure_smem(kern, dev, smem));
-  k_reduce<Tin, Tout, CW><<<persistent_grid(kern, dev, smem, items), kThreads, smem, st>>>(a);
+  k_reduce<Tin, Tout, CW><<<grid2d(kern, dev, smem, a.tiles, a.rank_hi - a.rank_lo), kThreads, smem, st>>>(a);
   ++g_launch_count;
   return FC_OK;
 }
@@ -220,7 +229,7 @@ fc_status launch_gather(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
   a.stages = 4;
   const int smem = a.stages * kThreads * code_chunk_bytes(a.c2);
   FC_TRY(ensure_smem(kern, dev, smem));
-  k_gather<Tout, CW><<<persistent_grid(kern, dev, smem, items), kThreads, smem, st>>>(a);
+  k_gather<Tout, CW><<<grid2d(kern, dev, smem, a.tiles, (a.rank_hi - a.rank_lo) * (a.world - 1)), kThreads, smem, st>>>(a);
   ++g_launch_count;
   return FC_OK;
 }

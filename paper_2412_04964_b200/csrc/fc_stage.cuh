@@ -66,6 +66,12 @@ struct Chunk {
 template <typename T>
 __device__ __forceinline__ void chunk_issue(uint32_t sdst, const T* base, int64_t idx0, int64_t M, int nvalid,
                                             int lane) {
+  if (nvalid == kLaneElems && idx0 + kLaneElems <= M) {  // common case: whole chunk in range
+#pragma unroll
+    for (int q = 0; q < Chunk<T>::kVecs; ++q)
+      cp_async16(sdst + 16 * Chunk<T>::slot(q, lane), base + idx0 + q * Chunk<T>::kPer, 16);
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < Chunk<T>::kVecs; ++q) {
     const int64_t i = idx0 + q * Chunk<T>::kPer;
