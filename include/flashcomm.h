@@ -130,7 +130,8 @@ typedef enum {
   FC_OPT_TIMEOUT_MS = 2,   /* flag-wait timeout -> ProtocolError (fabric.py:158-178); default 5000 */
   FC_OPT_LAG = 3,          /* fused schedule: tiles between a tile's scatter and its reduce (0 = auto) */
   FC_OPT_FAST = 4,         /* 0: force the generic (any group size) kernels; for testing */
-  FC_OPT_LAST_LAUNCHES = 5 /* read-only: kernels launched by the last all-reduce call */
+  FC_OPT_LAST_LAUNCHES = 5,/* read-only: kernels launched by the last all-reduce call */
+  FC_OPT_REDUCE_STAGES = 6 /* cp.async ring depth of the phase-split reduce kernel (0 = auto) */
 } fc_option;
 FC_API fc_status fc_comm_set_option(fc_comm* comm, int32_t option, int64_t value);
 FC_API fc_status fc_comm_get_option(fc_comm* comm, int32_t option, int64_t* value);

@@ -279,6 +279,7 @@ fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
       break;
     case FC_OPT_LAG: c->lag = std::max<int64_t>(0, value); break;
     case FC_OPT_FAST: c->fast = value != 0; break;
+    case FC_OPT_REDUCE_STAGES: c->reduce_stages = std::max<int64_t>(0, std::min<int64_t>(3, value)); break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
   return FC_OK;
@@ -293,6 +294,7 @@ fc_status fc_comm_get_option(fc_comm* c, int32_t option, int64_t* value) {
     case FC_OPT_LAG: *value = c->lag; break;
     case FC_OPT_FAST: *value = c->fast; break;
     case FC_OPT_LAST_LAUNCHES: *value = c->last_launches; break;
+    case FC_OPT_REDUCE_STAGES: *value = c->reduce_stages; break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
   return FC_OK;

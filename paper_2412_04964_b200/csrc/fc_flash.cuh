@@ -35,6 +35,7 @@ struct FlashArgs {
   int64_t flags_cap;
   uint64_t timeout_ns;
   int stages;               // cp.async ring depth of the phase-split kernels
+  int stage_hint;           // host-side override of the reduce ring depth (0 = auto)
   DevCodec c1, c2;
   const void* in[kMaxRanks];
   void* out[kMaxRanks];

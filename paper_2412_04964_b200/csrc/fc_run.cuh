@@ -194,7 +194,7 @@ inline dim3 grid2d(const void* kern, int dev, int smem, int tiles, int ydim) {
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
   const int64_t total = (int64_t)occ * num_sms(dev);
-  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(tiles, (total + ydim - 1) / ydim));
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(tiles, total / ydim));  // one wave, never a ragged second
   return dim3((unsigned)gx, (unsigned)ydim);
 }
 
@@ -215,7 +215,7 @@ template <typename Tin, typename Tout, int CW>
 fc_status launch_reduce(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
   const void* kern = (const void*)k_reduce<Tin, Tout, CW>;
   const int tb = reduce_thread_bytes<Tin>(a.c1, a.world) * kThreads;
-  a.stages = std::max(1, std::min(3, kStageBudget / tb));
+  a.stages = a.stage_hint > 0 ? a.stage_hint : std::max(1, std::min(3, kStageBudget / tb));
   const int smem = a.stages * tb;
   FC_TRY(ensure_smem(kern, dev, smem));
   k_reduce<Tin, Tout, CW><<<grid2d(kern, dev, smem, a.tiles, a.rank_hi - a.rank_lo), kThreads, smem, st>>>(a);
@@ -253,6 +253,7 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
   a.slot_bytes = c->slot_bytes;
   a.flags_cap = c->flags_cap;
   a.timeout_ns = (uint64_t)c->timeout_ms * 1000000ull;
+  a.stage_hint = (int)c->reduce_stages;
   a.c1 = dev_codec(cfg->stage1, p.L1);
   a.c2 = dev_codec(cfg->stage2, p.L2);
   for (int r = 0; r < N; ++r) {

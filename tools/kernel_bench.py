@@ -75,12 +75,15 @@ def flash_sweep(quick=False):
         w = cfg.stage1_codec.wire_byte_len(seg)
         alg = tp * (2 * e * M + 2 * (tp - 1) * 2 * w)
         for mode, opts in (("fused", {}), ("split", {_lib.OPT_FUSED: 0}),
-                           ("fused_c1", {_lib.OPT_CTAS: 1}), ("fused_lag16", {_lib.OPT_LAG: 16})):
-            if quick and mode not in ("fused", "split"):
+                           ("split_rs1", {_lib.OPT_FUSED: 0, _lib.OPT_REDUCE_STAGES: 1}),
+                           ("split_rs2", {_lib.OPT_FUSED: 0, _lib.OPT_REDUCE_STAGES: 2}),
+                           ("fused_lag16", {_lib.OPT_LAG: 16})):
+            if quick and mode not in ("fused", "split", "split_rs1"):
                 continue
             comm.set_option(_lib.OPT_FUSED, 1)
             comm.set_option(_lib.OPT_CTAS, 0)
             comm.set_option(_lib.OPT_LAG, 0)
+            comm.set_option(_lib.OPT_REDUCE_STAGES, 0)
             for k, v in opts.items():
                 comm.set_option(k, v)
             t = timeit(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), iters=10, warm=3)
