@@ -131,7 +131,11 @@ typedef enum {
   FC_OPT_LAG = 3,          /* fused schedule: tiles between a tile's scatter and its reduce (0 = auto) */
   FC_OPT_FAST = 4,         /* 0: force the generic (any group size) kernels; for testing */
   FC_OPT_LAST_LAUNCHES = 5,/* read-only: kernels launched by the last all-reduce call */
-  FC_OPT_REDUCE_STAGES = 6 /* cp.async ring depth of the phase-split reduce kernel (0 = auto) */
+  FC_OPT_REDUCE_STAGES = 6,/* ring depth of the phase-split reduce kernel (0 = auto) */
+  FC_OPT_SCATTER_STAGES = 7,/* ring depth of the streaming scatter / quantize kernel (0 = auto) */
+  FC_OPT_GATHER_STAGES = 8, /* ring depth of the streaming gather / dequantize kernel (0 = auto) */
+  FC_OPT_CTAS_PER_SM = 9,   /* cap on resident CTAs per SM of the streaming kernels (0 = occupancy) */
+  FC_OPT_STREAM_MASK = 10   /* testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels */
 } fc_option;
 FC_API fc_status fc_comm_set_option(fc_comm* comm, int32_t option, int64_t value);
 FC_API fc_status fc_comm_get_option(fc_comm* comm, int32_t option, int64_t* value);

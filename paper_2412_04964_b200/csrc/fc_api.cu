@@ -278,8 +278,12 @@ fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
       c->timeout_ms = value;
       break;
     case FC_OPT_LAG: c->lag = std::max<int64_t>(0, value); break;
-    case FC_OPT_FAST: c->fast = value != 0; break;
-    case FC_OPT_REDUCE_STAGES: c->reduce_stages = std::max<int64_t>(0, std::min<int64_t>(3, value)); break;
+    case FC_OPT_FAST: c->fast = value < 0 ? 0 : (value > 2 ? 2 : value); break;
+    case FC_OPT_REDUCE_STAGES: c->reduce_stages = std::max<int64_t>(0, std::min<int64_t>(4, value)); break;
+    case FC_OPT_SCATTER_STAGES: c->q_stages = std::max<int64_t>(0, std::min<int64_t>(8, value)); break;
+    case FC_OPT_GATHER_STAGES: c->d_stages = std::max<int64_t>(0, std::min<int64_t>(12, value)); break;
+    case FC_OPT_CTAS_PER_SM: c->ctas_per_sm = std::max<int64_t>(0, std::min<int64_t>(16, value)); break;
+    case FC_OPT_STREAM_MASK: c->stream_mask = value & 7; break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
   return FC_OK;
@@ -295,6 +299,10 @@ fc_status fc_comm_get_option(fc_comm* c, int32_t option, int64_t* value) {
     case FC_OPT_FAST: *value = c->fast; break;
     case FC_OPT_LAST_LAUNCHES: *value = c->last_launches; break;
     case FC_OPT_REDUCE_STAGES: *value = c->reduce_stages; break;
+    case FC_OPT_SCATTER_STAGES: *value = c->q_stages; break;
+    case FC_OPT_GATHER_STAGES: *value = c->d_stages; break;
+    case FC_OPT_CTAS_PER_SM: *value = c->ctas_per_sm; break;
+    case FC_OPT_STREAM_MASK: *value = c->stream_mask; break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
   return FC_OK;

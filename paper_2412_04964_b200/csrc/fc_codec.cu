@@ -6,6 +6,8 @@
 #include <mutex>
 
 #include "fc_codec_dev.cuh"
+#include "fc_lane.cuh"
+#include "fc_stream.cuh"
 #include "fc_stage.cuh"
 #include "fc_host.h"
 
@@ -14,7 +16,7 @@ namespace fc {
 // --------------------------------------------------------------------------
 // fast path: one 32-element chunk per thread, groups of g/32 lanes
 
-template <typename T, int CW>
+template <typename T, int CW, class Spec>
 __global__ void __launch_bounds__(kThreads) k_quant_fast(const T* __restrict__ x, int64_t n, DevCodec c,
                                                          uint8_t* __restrict__ dst, uint32_t* err, int S) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -40,14 +42,14 @@ __global__ void __launch_bounds__(kThreads) k_quant_fast(const T* __restrict__ x
     LaneOf<T> v;
     chunk_read_src<T>(s0 + st * kThreads * CB, lane, v);
     LaneQuant<CW> q;
-    const bool bad = lane_quantize(c, v, nvalid, q);
+    const bool bad = quantize_lane<Spec>(c, v, nvalid, q);
     store_lane(c, dst, p0, nvalid, q, lane);
     if (bad && err) atomicOr(err, make_err(kErrNonFinite, 0, 0, 0));
     st = (st + 1 == S) ? 0 : st + 1;
   }
 }
 
-template <typename To, int CW>
+template <typename To, int CW, class Spec>
 __global__ void __launch_bounds__(kThreads) k_dequant_fast(const uint8_t* __restrict__ src, int64_t n, DevCodec c,
                                                            To* __restrict__ out, int S) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(kThreads) k_dequant_fast(const uint8_t* __rest
       LaneCodes<CW> L;
       code_read(c, s0 + st * kThreads * CB, p0, L);
       float v[kLaneElems];
-      lane_decode<false>(c, L, v);
+      decode_lane<Spec, false>(c, L, v);
       store_chunk(out, p0, n, nvalid, v);
     }
     st = (st + 1 == S) ? 0 : st + 1;
@@ -102,6 +104,12 @@ static unsigned resident_grid(const void* kern, int smem, int64_t items, int sms
 // --------------------------------------------------------------------------
 // launchers
 
+// 1: INT4 asym nearest, 2: INT8 asym nearest (compile-time lane codecs), 0: generic
+static int codec_spec(const fc_codec& c) {
+  if (c.kind != FC_KIND_INT || c.symmetric || c.rounding != FC_ROUND_NEAREST_EVEN) return 0;
+  return storage_bits(c) == 4 ? 1 : 2;
+}
+
 int num_sms(int device) {
   static int cache[64] = {0};
   if (device < 0 || device >= 64) return 148;
@@ -117,6 +125,55 @@ static int cur_sms() {
   int d = 0;
   cudaGetDevice(&d);
   return num_sms(d);
+}
+
+
+// single-GPU codec through the streaming kernels (fc_stream.cuh, mode 1)
+static FlashArgs codec_args(const void* in, void* out, int64_t n, const DevCodec& dc, uint32_t* err) {
+  FlashArgs a{};
+  a.mode = 1;
+  a.world = 1;
+  a.rank_lo = 0;
+  a.rank_hi = 1;
+  a.M = n;
+  a.seg = n;
+  a.sub_off = 0;
+  a.sub_len = n;
+  a.tiles = (int)((n + kTileElems - 1) / kTileElems);
+  a.c1 = dc;
+  a.c2 = dc;
+  a.cerr = err;
+  a.in[0] = in;
+  a.out[0] = out;
+  return a;
+}
+
+static unsigned stream_grid_cur(const void* kern, int threads, int smem, int64_t items) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)occ * cur_sms()));
+}
+
+template <typename T, class Spec>
+static fc_status quant_stream(const T* x, int64_t n, const DevCodec& dc, uint8_t* dst, uint32_t* err, cudaStream_t st) {
+  FlashArgs a = codec_args(x, dst, n, dc, err);
+  a.stages = 4;
+  const int smem = a.stages * (kTileElems * 2 + 16);
+  const void* k = (const void*)k_qstream<T, Spec>;
+  FC_TRY(ensure_smem_attr(k, smem));
+  k_qstream<T, Spec><<<stream_grid_cur(k, kStreamThreads, smem, a.tiles), kStreamThreads, smem, st>>>(a);
+  return FC_OK;
+}
+
+template <typename T, class Spec>
+static fc_status dequant_stream(const uint8_t* src, int64_t n, const DevCodec& dc, T* out, cudaStream_t st) {
+  FlashArgs a = codec_args(src, out, n, dc, nullptr);
+  a.stages = 6;
+  const int smem = a.stages * ((int)dstage_bytes(dc) + 16);
+  const void* k = (const void*)k_dstream<T, Spec>;
+  FC_TRY(ensure_smem_attr(k, smem));
+  k_dstream<T, Spec><<<stream_grid_cur(k, kStreamThreads, smem, a.tiles), kStreamThreads, smem, st>>>(a);
+  return FC_OK;
 }
 
 template <typename T>
@@ -139,17 +196,36 @@ fc_status launch_quantize(const void* x, int in_dtype, int64_t n, const fc_codec
     const int64_t tiles = (n + kTileElems - 1) / kTileElems;
     uint8_t* d = (uint8_t*)dst;
     const bool pass = c.kind == FC_KIND_FP16;
+    const int spec = codec_spec(c);
+    if (spec && in_dtype != FC_DTYPE_F32 && allow_fast) {
+      if (in_dtype == FC_DTYPE_F16) {
+        FC_TRY((spec == 1 ? quant_stream<__half, SpecA4>((const __half*)x, n, dc, d, err, st)
+                         : quant_stream<__half, SpecA8>((const __half*)x, n, dc, d, err, st)));
+      } else {
+        FC_TRY((spec == 1 ? quant_stream<__nv_bfloat16, SpecA4>((const __nv_bfloat16*)x, n, dc, d, err, st)
+                         : quant_stream<__nv_bfloat16, SpecA8>((const __nv_bfloat16*)x, n, dc, d, err, st)));
+      }
+      FC_CUDA_TRY(cudaGetLastError());
+      return FC_OK;
+    }
 #define FC_QF(T)                                                                                  \
   do {                                                                                            \
-    const void* k = pass ? (const void*)k_quant_fast<T, 16> : (const void*)k_quant_fast<T, 8>;    \
+    const void* k = pass ? (const void*)k_quant_fast<T, 16, GenSpec>                              \
+                         : spec == 1 ? (const void*)k_quant_fast<T, 8, SpecA4>                    \
+                         : spec == 2 ? (const void*)k_quant_fast<T, 8, SpecA8>                    \
+                                     : (const void*)k_quant_fast<T, 8, GenSpec>;                  \
     const int S = sizeof(T) == 4 ? 3 : 4;                                                         \
     const int smem = S * kThreads * Chunk<T>::kBytes;                                             \
     FC_TRY(ensure_smem_attr(k, smem));                                                            \
     const unsigned g = resident_grid(k, smem, tiles, cur_sms());                                  \
     if (pass)                                                                                     \
-      k_quant_fast<T, 16><<<g, kThreads, smem, st>>>((const T*)x, n, dc, d, err, S);             \
+      k_quant_fast<T, 16, GenSpec><<<g, kThreads, smem, st>>>((const T*)x, n, dc, d, err, S);    \
+    else if (spec == 1)                                                                           \
+      k_quant_fast<T, 8, SpecA4><<<g, kThreads, smem, st>>>((const T*)x, n, dc, d, err, S);      \
+    else if (spec == 2)                                                                           \
+      k_quant_fast<T, 8, SpecA8><<<g, kThreads, smem, st>>>((const T*)x, n, dc, d, err, S);      \
     else                                                                                          \
-      k_quant_fast<T, 8><<<g, kThreads, smem, st>>>((const T*)x, n, dc, d, err, S);              \
+      k_quant_fast<T, 8, GenSpec><<<g, kThreads, smem, st>>>((const T*)x, n, dc, d, err, S);     \
   } while (0)
     switch (in_dtype) {
       case FC_DTYPE_F32: FC_QF(float); break;
@@ -178,17 +254,42 @@ fc_status launch_dequantize(const void* src, int64_t n, const fc_codec& c, void*
   if (allow_fast && fast_group(c) && aligned) {
     const int64_t tiles = (n + kTileElems - 1) / kTileElems;
     const bool pass = c.kind == FC_KIND_FP16;
+    const int spec = codec_spec(c);
+    if (spec) {
+      switch (out_dtype) {
+        case FC_DTYPE_F32:
+          FC_TRY((spec == 1 ? dequant_stream<float, SpecA4>(s, n, dc, (float*)out, st)
+                           : dequant_stream<float, SpecA8>(s, n, dc, (float*)out, st)));
+          break;
+        case FC_DTYPE_F16:
+          FC_TRY((spec == 1 ? dequant_stream<__half, SpecA4>(s, n, dc, (__half*)out, st)
+                           : dequant_stream<__half, SpecA8>(s, n, dc, (__half*)out, st)));
+          break;
+        default:
+          FC_TRY((spec == 1 ? dequant_stream<__nv_bfloat16, SpecA4>(s, n, dc, (__nv_bfloat16*)out, st)
+                           : dequant_stream<__nv_bfloat16, SpecA8>(s, n, dc, (__nv_bfloat16*)out, st)));
+      }
+      FC_CUDA_TRY(cudaGetLastError());
+      return FC_OK;
+    }
     const int S = 4;
     const int smem = S * kThreads * code_chunk_bytes(dc);
 #define FC_DF(T)                                                                                      \
   do {                                                                                                \
-    const void* k = pass ? (const void*)k_dequant_fast<T, 16> : (const void*)k_dequant_fast<T, 8>;    \
+    const void* k = pass ? (const void*)k_dequant_fast<T, 16, GenSpec>                                \
+                         : spec == 1 ? (const void*)k_dequant_fast<T, 8, SpecA4>                      \
+                         : spec == 2 ? (const void*)k_dequant_fast<T, 8, SpecA8>                      \
+                                     : (const void*)k_dequant_fast<T, 8, GenSpec>;                    \
     FC_TRY(ensure_smem_attr(k, smem));                                                                \
     const unsigned g = resident_grid(k, smem, tiles, cur_sms());                                      \
     if (pass)                                                                                         \
-      k_dequant_fast<T, 16><<<g, kThreads, smem, st>>>(s, n, dc, (T*)out, S);                        \
+      k_dequant_fast<T, 16, GenSpec><<<g, kThreads, smem, st>>>(s, n, dc, (T*)out, S);               \
+    else if (spec == 1)                                                                               \
+      k_dequant_fast<T, 8, SpecA4><<<g, kThreads, smem, st>>>(s, n, dc, (T*)out, S);                 \
+    else if (spec == 2)                                                                               \
+      k_dequant_fast<T, 8, SpecA8><<<g, kThreads, smem, st>>>(s, n, dc, (T*)out, S);                 \
     else                                                                                              \
-      k_dequant_fast<T, 8><<<g, kThreads, smem, st>>>(s, n, dc, (T*)out, S);                         \
+      k_dequant_fast<T, 8, GenSpec><<<g, kThreads, smem, st>>>(s, n, dc, (T*)out, S);                \
   } while (0)
     switch (out_dtype) {
       case FC_DTYPE_F32: FC_DF(float); break;

@@ -50,7 +50,9 @@ struct DevCodec {
   float qmax_f;    // asym: 2^b-1 ; sym: 2^(b-1)-1
   float qmin_f;    // asym: 0     ; sym: -2^(b-1)
   double qdiv;     // divisor of the raw scale: 2^b-1 (asym) or 2^(b-1)-1 (sym)
+  double qinv;     // RN64(1 / qdiv)
   double floor;    // scale_floor
+  uint32_t floor16;  // bit pattern of the smallest fp16 >= floor (0x7C00 if none)
   int64_t scales_off;
   int64_t zeros_off;
 };

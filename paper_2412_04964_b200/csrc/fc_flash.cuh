@@ -17,6 +17,7 @@
 #pragma once
 
 #include "fc_codec_dev.cuh"
+#include "fc_lane.cuh"
 #include "fc_stage.cuh"
 
 namespace fc {
@@ -36,7 +37,11 @@ struct FlashArgs {
   uint64_t timeout_ns;
   int stages;               // cp.async ring depth of the phase-split kernels
   int stage_hint;           // host-side override of the reduce ring depth (0 = auto)
+  int q_hint, d_hint;       // ring depths of the streaming scatter / gather kernels (0 = auto)
+  int cta_cap;              // resident CTAs per SM cap for the streaming kernels (0 = occupancy)
   DevCodec c1, c2;
+  int mode;                 // 0: flash all-reduce; 1: single-GPU codec job (in[0] -> out[0], c1)
+  uint32_t* cerr;           // mode 1: error word
   const void* in[kMaxRanks];
   void* out[kMaxRanks];
   uint8_t* blk[kMaxRanks];  // every rank's block, addressable from the launching device
@@ -73,7 +78,7 @@ enum Phase : uint32_t { kPhScatter = 1, kPhReduce = 2, kPhGather = 3, kPhBarrier
 
 // ---------------------------------------------------------------- work items
 
-template <typename Tin, int CW>
+template <typename Tin, int CW, class S1>
 __device__ __forceinline__ void do_scatter(const FlashArgs& a, int r, int j, int t) {
   const int lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
@@ -81,12 +86,12 @@ __device__ __forceinline__ void do_scatter(const FlashArgs& a, int r, int j, int
   LaneOf<Tin> v;
   load_lane_src(reinterpret_cast<const Tin*>(a.in[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, v);
   LaneQuant<CW> q;
-  const bool bad = lane_quantize(a.c1, v, nvalid, q);
+  const bool bad = quantize_lane<S1>(a.c1, v, nvalid, q);
   store_lane(a.c1, recv_slot(a, j, r), p0, nvalid, q, lane);
   if (bad) atomicOr(errw(a, r), make_err(kErrNonFinite, kPhScatter, j, r));
 }
 
-template <typename Tin, typename Tout, int CW>
+template <typename Tin, typename Tout, int CW, class S1, class S2>
 __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
   const int lane = threadIdx.x & 31;
   const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
@@ -100,7 +105,7 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
       LaneOf<Tin> v;
       load_lane_src(reinterpret_cast<const Tin*>(a.in[j]), idx0, a.M, nvalid, v);
       LaneQuant<CW> q;
-      bad |= lane_quantize(a.c1, v, nvalid, q);  // own piece: QDQ in registers (collectives.py:364-365)
+      bad |= quantize_lane<S1>(a.c1, v, nvalid, q);  // own piece: QDQ in registers (collectives.py:364-365)
       lane_codes_from(a.c1, q, L);
     } else if (nvalid > 0) {
       load_lane(a.c1, recv_slot(a, j, s), p0, L);
@@ -111,12 +116,12 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
       L.mz = 0.0f;
     }
     if (s == 0)
-      lane_decode<false>(a.c1, L, acc.v);  // ascending source rank (collectives.py:182-187)
+      decode_lane<S1, false>(a.c1, L, acc.v);  // ascending source rank (collectives.py:182-187)
     else
-      lane_decode<true>(a.c1, L, acc.v);
+      decode_lane<S1, true>(a.c1, L, acc.v);
   }
   LaneQuant<CW> q2;
-  bad |= lane_quantize(a.c2, acc, nvalid, q2);
+  bad |= quantize_lane<S2>(a.c2, acc, nvalid, q2);
   for (int pp = 1; pp < a.world; ++pp) {
     const int p = (j + pp) % a.world;
     store_lane(a.c2, gath_slot(a, p, j), p0, nvalid, q2, lane);
@@ -124,12 +129,12 @@ __device__ __forceinline__ void do_reduce(const FlashArgs& a, int j, int t) {
   LaneCodes<CW> L2;
   lane_codes_from(a.c2, q2, L2);
   float o[kLaneElems];
-  lane_decode<false>(a.c2, L2, o);  // owner decodes its own payload too (collectives.py:378)
+  decode_lane<S2, false>(a.c2, L2, o);  // owner decodes its own payload too (collectives.py:378)
   if (nvalid > 0) store_chunk(reinterpret_cast<Tout*>(a.out[j]), idx0, a.M, nvalid, o);
   if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
 }
 
-template <typename Tout, int CW>
+template <typename Tout, int CW, class S2>
 __device__ __forceinline__ void do_gather(const FlashArgs& a, int r, int j, int t) {
   const int64_t p0 = (int64_t)t * kTileElems + (int64_t)threadIdx.x * kLaneElems;
   const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
@@ -137,7 +142,7 @@ __device__ __forceinline__ void do_gather(const FlashArgs& a, int r, int j, int 
   LaneCodes<CW> L;
   load_lane(a.c2, gath_slot(a, r, j), p0, L);
   float o[kLaneElems];
-  lane_decode<false>(a.c2, L, o);
+  decode_lane<S2, false>(a.c2, L, o);
   store_chunk(reinterpret_cast<Tout*>(a.out[r]), (int64_t)j * a.seg + a.sub_off + p0, a.M, nvalid, o);
 }
 
@@ -186,7 +191,7 @@ __device__ __forceinline__ void raise_flags(uint32_t* const* flags, int nflags, 
 // holds P scatter items for tile k, the reduce of tile k-lag and P gathers of
 // tile k-2*lag. Every wait targets an item of a strictly earlier position, so
 // with all CTAs resident the schedule cannot deadlock.
-template <typename Tin, typename Tout, int CW>
+template <typename Tin, typename Tout, int CW, class S1, class S2>
 __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
   __shared__ int s_abort;
   __shared__ uint32_t* s_flags[kMaxRanks];
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
       const int64_t t = k;
       if (t >= a.tiles) continue;
       const int j = (rank + 1 + slot) % a.world;
-      do_scatter<Tin, CW>(a, rank, j, (int)t);
+      do_scatter<Tin, CW, S1>(a, rank, j, (int)t);
       if (threadIdx.x == 0) s_flags[0] = rflag(a, j, rank) + t;
       raise_flags(s_flags, 1, a.epoch);
     } else if (slot == P) {
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
       __syncthreads();
       if (wait_flags(a, rank, s_flags, s_peers, P, kPhReduce, &s_abort)) return;
       __syncthreads();
-      do_reduce<Tin, Tout, CW>(a, rank, (int)t);
+      do_reduce<Tin, Tout, CW, S1, S2>(a, rank, (int)t);
       __syncthreads();
       if (threadIdx.x < P) s_flags[threadIdx.x] = gflag(a, (rank + 1 + threadIdx.x) % a.world, rank) + t;
       raise_flags(s_flags, P, a.epoch);
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
       }
       __syncthreads();
       if (wait_flags(a, rank, s_flags, s_peers, 1, kPhGather, &s_abort)) return;
-      do_gather<Tout, CW>(a, rank, j, (int)t);
+      do_gather<Tout, CW, S2>(a, rank, j, (int)t);
     }
     __syncthreads();
   }
@@ -259,7 +264,7 @@ __device__ __forceinline__ int lane_valid(int64_t len, int64_t p0) {
   return d <= 0 ? 0 : (d >= kLaneElems ? kLaneElems : (int)d);
 }
 
-template <typename Tin, int CW>
+template <typename Tin, int CW, class S1>
 __global__ void __launch_bounds__(kThreads) k_scatter(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int CB = Chunk<Tin>::kBytes;
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(FlashArgs a) {
     LaneOf<Tin> v;
     chunk_read_src<Tin>(s0 + st * kThreads * CB, lane, v);
     LaneQuant<CW> q;
-    bad |= lane_quantize(a.c1, v, nvalid, q);
+    bad |= quantize_lane<S1>(a.c1, v, nvalid, q);
     store_lane(a.c1, dst, p0, nvalid, q, lane);
     st = (st + 1 == S) ? 0 : st + 1;
   }
@@ -303,7 +308,7 @@ __host__ __device__ inline int reduce_thread_bytes(const DevCodec& c1, int world
   return Chunk<Tin>::kBytes + (world - 1) * code_chunk_bytes(c1);
 }
 
-template <typename Tin, typename Tout, int CW>
+template <typename Tin, typename Tout, int CW, class S1, class S2>
 __global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
@@ -348,10 +353,10 @@ __global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
       LaneOf<Tin> v;
       chunk_read_src<Tin>(base, lane, v);
       LaneQuant<CW> q;
-      bad |= lane_quantize(a.c1, v, nvalid, q);
+      bad |= quantize_lane<S1>(a.c1, v, nvalid, q);
       LaneCodes<CW> L;
       lane_codes_from(a.c1, q, L);
-      lane_decode<false>(a.c1, L, mine.v);
+      decode_lane<S1, false>(a.c1, L, mine.v);
     }
     // fp32 sum in ascending source rank (collectives.py:182-187)
     FloatLane acc;
@@ -379,12 +384,12 @@ __global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
       }
       off += CCB;
       if (s == 0)
-        lane_decode<false>(a.c1, L, acc.v);
+        decode_lane<S1, false>(a.c1, L, acc.v);
       else
-        lane_decode<true>(a.c1, L, acc.v);
+        decode_lane<S1, true>(a.c1, L, acc.v);
     }
     LaneQuant<CW> q2;
-    bad |= lane_quantize(a.c2, acc, nvalid, q2);
+    bad |= quantize_lane<S2>(a.c2, acc, nvalid, q2);
     for (int p = j + 1;; ++p) {  // every peer's gather slot [j]
       if (p == a.world) p = 0;
       if (p == j) break;
@@ -393,14 +398,14 @@ __global__ void __launch_bounds__(kThreads) k_reduce(FlashArgs a) {
     LaneCodes<CW> L2;
     lane_codes_from(a.c2, q2, L2);
     float o[kLaneElems];
-    lane_decode<false>(a.c2, L2, o);  // owner decodes its own payload too (collectives.py:378)
+    decode_lane<S2, false>(a.c2, L2, o);  // owner decodes its own payload too (collectives.py:378)
     if (nvalid > 0) store_chunk(reinterpret_cast<Tout*>(a.out[j]), seg0 + p0, a.M, nvalid, o);
     st = (st + 1 == S) ? 0 : st + 1;
   }
   if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
 }
 
-template <typename Tout, int CW>
+template <typename Tout, int CW, class S2>
 __global__ void __launch_bounds__(kThreads) k_gather(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int CB = code_chunk_bytes(a.c2);
@@ -430,7 +435,7 @@ __global__ void __launch_bounds__(kThreads) k_gather(FlashArgs a) {
       LaneCodes<CW> L;
       code_read(a.c2, s0 + st * kThreads * CB, p0, L);
       float o[kLaneElems];
-      lane_decode<false>(a.c2, L, o);
+      decode_lane<S2, false>(a.c2, L, o);
       store_chunk(out, seg0 + p0, a.M, nvalid, o);
     }
     st = (st + 1 == S) ? 0 : st + 1;

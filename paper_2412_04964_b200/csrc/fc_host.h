@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cmath>
 #include <cstdio>
 #include <string>
 
@@ -62,6 +63,21 @@ inline bool fast_group(const fc_codec& c) {
   return c.group_size == 32 || c.group_size == 64 || c.group_size == 128 || c.group_size == 256;
 }
 
+inline double half_bits_value(uint32_t b) {
+  const int e = (int)((b >> 10) & 31u), m = (int)(b & 1023u);
+  return e == 0 ? std::ldexp((double)m, -24) : std::ldexp((double)(1024 + m), e - 25);
+}
+// smallest positive-or-zero fp16 pattern whose value is >= floor (0x7C00 = inf if none):
+// the reference's "nextafter(h, +inf) while h < floor" (codec.py:246-247) after RN16
+inline uint32_t floor16_of(double floor) {
+  uint32_t lo = 0, hi = 0x7C00;  // answer in [lo, hi]
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) / 2;
+    if (half_bits_value(mid) >= floor) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
 inline DevCodec dev_codec(const fc_codec& c, const fc_layout& L) {
   DevCodec d{};
   d.kind = c.kind;
@@ -85,7 +101,9 @@ inline DevCodec dev_codec(const fc_codec& c, const fc_layout& L) {
       d.qdiv = (double)((1 << c.bits) - 1);
     }
   }
+  d.qinv = d.qdiv > 0 ? 1.0 / d.qdiv : 0.0;
   d.floor = c.scale_floor;
+  d.floor16 = floor16_of(c.scale_floor);
   d.scales_off = L.scales_offset;
   d.zeros_off = L.zeros_offset;
   return d;

@@ -13,9 +13,17 @@
 
 #include "fc_comm.h"
 #include "fc_flash.cuh"
+#include "fc_stream.cuh"
 
 namespace fc {
 
+
+constexpr int kSpecGen = 0, kSpecA4 = 1, kSpecA8 = 2;
+inline int spec_id(const fc_codec& c) {
+  if (c.kind != FC_KIND_INT || c.symmetric || c.rounding != FC_ROUND_NEAREST_EVEN) return kSpecGen;
+  if (c.group_size != 32 && c.group_size != 64 && c.group_size != 128 && c.group_size != 256) return kSpecGen;
+  return storage_bits(c) == 4 ? kSpecA4 : kSpecA8;
+}
 
 struct Plan {
   int64_t seg = 0, R = 0, rounds = 0;
@@ -57,9 +65,9 @@ inline uint8_t* h_gath_slot(const fc_comm* c, int owner, int src) {
   return c->blk[owner] + (int64_t)(c->world + src) * c->slot_bytes;
 }
 
-template <typename Tin, typename Tout, int CW>
+template <typename Tin, typename Tout, int CW, class S1, class S2>
 fc_status launch_fused(const fc_comm* c, FlashArgs a, int rank_lo, int rank_hi, int device, cudaStream_t st) {
-  auto kern = k_flash_fused<Tin, Tout, CW>;
+  auto kern = k_flash_fused<Tin, Tout, CW, S1, S2>;
   int occ = 0;
   FC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0));
   const int cap = std::max(1, occ) * num_sms(device);
@@ -200,41 +208,105 @@ inline dim3 grid2d(const void* kern, int dev, int smem, int tiles, int ydim) {
 
 constexpr int kStageBudget = 200 * 1024;  // dynamic smem per CTA for the cp.async rings
 
-template <typename Tin, int CW>
+template <typename Tin, int CW, class S1>
 fc_status launch_scatter(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
-  const void* kern = (const void*)k_scatter<Tin, CW>;
+  const void* kern = (const void*)k_scatter<Tin, CW, S1>;
   a.stages = Chunk<Tin>::kBytes <= 64 ? 4 : 3;
   const int smem = a.stages * kThreads * Chunk<Tin>::kBytes;
   FC_TRY(ensure_smem(kern, dev, smem));
-  k_scatter<Tin, CW><<<grid2d(kern, dev, smem, a.tiles, (a.rank_hi - a.rank_lo) * (a.world - 1)), kThreads, smem, st>>>(a);
+  k_scatter<Tin, CW, S1><<<grid2d(kern, dev, smem, a.tiles, (a.rank_hi - a.rank_lo) * (a.world - 1)), kThreads, smem, st>>>(a);
   ++g_launch_count;
   return FC_OK;
 }
 
-template <typename Tin, typename Tout, int CW>
+template <typename Tin, typename Tout, int CW, class S1, class S2>
 fc_status launch_reduce(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
-  const void* kern = (const void*)k_reduce<Tin, Tout, CW>;
+  const void* kern = (const void*)k_reduce<Tin, Tout, CW, S1, S2>;
   const int tb = reduce_thread_bytes<Tin>(a.c1, a.world) * kThreads;
   a.stages = a.stage_hint > 0 ? a.stage_hint : std::max(1, std::min(3, kStageBudget / tb));
   const int smem = a.stages * tb;
   FC_TRY(ensure_smem(kern, dev, smem));
-  k_reduce<Tin, Tout, CW><<<grid2d(kern, dev, smem, a.tiles, a.rank_hi - a.rank_lo), kThreads, smem, st>>>(a);
+  k_reduce<Tin, Tout, CW, S1, S2><<<grid2d(kern, dev, smem, a.tiles, a.rank_hi - a.rank_lo), kThreads, smem, st>>>(a);
   ++g_launch_count;
   return FC_OK;
 }
 
-template <typename Tout, int CW>
+template <typename Tout, int CW, class S2>
 fc_status launch_gather(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
-  const void* kern = (const void*)k_gather<Tout, CW>;
+  const void* kern = (const void*)k_gather<Tout, CW, S2>;
   a.stages = 4;
   const int smem = a.stages * kThreads * code_chunk_bytes(a.c2);
   FC_TRY(ensure_smem(kern, dev, smem));
-  k_gather<Tout, CW><<<grid2d(kern, dev, smem, a.tiles, (a.rank_hi - a.rank_lo) * (a.world - 1)), kThreads, smem, st>>>(a);
+  k_gather<Tout, CW, S2><<<grid2d(kern, dev, smem, a.tiles, (a.rank_hi - a.rank_lo) * (a.world - 1)), kThreads, smem, st>>>(a);
   ++g_launch_count;
   return FC_OK;
 }
 
-template <typename Tin, typename Tout, int CW>
+// ---------------------------------------------------------------- stream launches (fc_stream.cuh)
+
+inline unsigned stream_grid(const void* kern, int dev, int threads, int smem, int64_t items, int cap = 0) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  if (cap > 0) occ = std::min(occ, cap);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)occ * num_sms(dev)));
+}
+
+constexpr int kQStages = 4;
+constexpr int kDStages = 6;
+
+template <typename Tin, class S1>
+fc_status launch_qstream(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
+  if constexpr (sizeof(Tin) != 2 || !S1::kFast) {
+    return fail(FC_ERR_CONFIG, "stream kernels need 16-bit inputs and a compile-time codec");
+  } else {
+  const void* kern = (const void*)k_qstream<Tin, S1>;
+  a.stages = a.q_hint > 0 ? a.q_hint : kQStages;
+  const int smem = a.stages * (kTileElems * 2 + 16);
+  FC_TRY(ensure_smem(kern, dev, smem));
+  k_qstream<Tin, S1><<<stream_grid(kern, dev, kStreamThreads, smem, items, a.cta_cap), kStreamThreads, smem, st>>>(a);
+  ++g_launch_count;
+  return FC_OK;
+  }
+}
+
+// two stages when that lets two CTAs share an SM, else as many as fit (<= 4)
+inline int rstream_stages(const FlashArgs& a) {
+  const int sb = (int)rstage_bytes(a.c1, a.world) + 16;
+  if (2 * (2 * sb + 1024) <= 228 * 1024) return 2;
+  return std::min(4, kStageBudget / sb);
+}
+
+template <typename Tin, typename Tout, class S1, class S2>
+fc_status launch_rstream(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
+  if constexpr (sizeof(Tin) != 2 || !S1::kFast || !S2::kFast) {
+    return fail(FC_ERR_CONFIG, "stream kernels need 16-bit inputs and a compile-time codec");
+  } else {
+  const void* kern = (const void*)k_rstream<Tin, Tout, S1, S2>;
+  a.stages = a.stage_hint > 0 ? (int)a.stage_hint : rstream_stages(a);
+  const int smem = a.stages * ((int)rstage_bytes(a.c1, a.world) + 16);
+  FC_TRY(ensure_smem(kern, dev, smem));
+  k_rstream<Tin, Tout, S1, S2><<<stream_grid(kern, dev, kStreamThreads, smem, items, a.cta_cap), kStreamThreads, smem, st>>>(a);
+  ++g_launch_count;
+  return FC_OK;
+  }
+}
+
+template <typename Tout, class S2>
+fc_status launch_dstream(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
+  if constexpr (!S2::kFast) {
+    return fail(FC_ERR_CONFIG, "stream kernels need a compile-time codec");
+  } else {
+    const void* kern = (const void*)k_dstream<Tout, S2>;
+    a.stages = a.d_hint > 0 ? a.d_hint : kDStages;
+    const int smem = a.stages * ((int)dstage_bytes(a.c2) + 16);
+    FC_TRY(ensure_smem(kern, dev, smem));
+    k_dstream<Tout, S2><<<stream_grid(kern, dev, kStreamThreads, smem, items, a.cta_cap), kStreamThreads, smem, st>>>(a);
+    ++g_launch_count;
+    return FC_OK;
+  }
+}
+
+template <typename Tin, typename Tout, int CW, class S1, class S2>
 fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, int64_t n, const fc_flash_cfg* cfg,
                        cudaStream_t* st, int only_rank /* -1: local world */) {
   const int N = c->world;
@@ -254,6 +326,9 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
   a.flags_cap = c->flags_cap;
   a.timeout_ns = (uint64_t)c->timeout_ms * 1000000ull;
   a.stage_hint = (int)c->reduce_stages;
+  a.q_hint = (int)c->q_stages;
+  a.d_hint = (int)c->d_stages;
+  a.cta_cap = (int)c->ctas_per_sm;
   a.c1 = dev_codec(cfg->stage1, p.L1);
   a.c2 = dev_codec(cfg->stage2, p.L2);
   for (int r = 0; r < N; ++r) {
@@ -261,8 +336,21 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
     a.out[r] = outs[r];
     a.blk[r] = c->blk[r];
   }
+  a.mode = 0;
+  a.cerr = nullptr;
   bool single_dev = true;
   for (int r = 1; r < N; ++r) single_dev &= c->devices[r] == c->devices[0];
+  // streaming kernels (bulk-copy fed, fc_stream.cuh) for compile-time schemes and 16-bit inputs;
+  // fast == 2 keeps the cp.async-staged kernels (A/B testing)
+  bool use_stream = false;
+  if constexpr (S1::kFast && S2::kFast && sizeof(Tin) == 2) {
+    use_stream = p.fast && c->fast == 1;
+    if (use_stream) {
+      FlashArgs t = a;
+      t.world = N;
+      use_stream = rstream_stages(t) >= 2;
+    }
+  }
 
   for (int64_t k = 0; k < p.rounds; ++k) {
     a.sub_off = k * p.R;
@@ -276,15 +364,23 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
       FC_CUDA_TRY(cudaSetDevice(dev));
       cudaStream_t s = st[r];
       if (p.fast && c->fused != 0) {
-        FC_TRY((launch_fused<Tin, Tout, CW>(c, a, r, r + 1, dev, s)));
+        FC_TRY((launch_fused<Tin, Tout, CW, S1, S2>(c, a, r, r + 1, dev, s)));
       } else if (p.fast) {
         a.rank_lo = r;
         a.rank_hi = r + 1;
-        FC_TRY((launch_scatter<Tin, CW>(a, dev, s, (int64_t)(N - 1) * a.tiles)));
-        FC_TRY(ipc_barrier(c, a, r, 0, s));
-        FC_TRY((launch_reduce<Tin, Tout, CW>(a, dev, s, a.tiles)));
-        FC_TRY(ipc_barrier(c, a, r, 1, s));
-        FC_TRY((launch_gather<Tout, CW>(a, dev, s, (int64_t)(N - 1) * a.tiles)));
+        if (use_stream) {
+          FC_TRY((launch_qstream<Tin, S1>(a, dev, s, (int64_t)(N - 1) * a.tiles)));
+          FC_TRY(ipc_barrier(c, a, r, 0, s));
+          FC_TRY((launch_rstream<Tin, Tout, S1, S2>(a, dev, s, a.tiles)));
+          FC_TRY(ipc_barrier(c, a, r, 1, s));
+          FC_TRY((launch_dstream<Tout, S2>(a, dev, s, (int64_t)(N - 1) * a.tiles)));
+        } else {
+          FC_TRY((launch_scatter<Tin, CW, S1>(a, dev, s, (int64_t)(N - 1) * a.tiles)));
+          FC_TRY(ipc_barrier(c, a, r, 0, s));
+          FC_TRY((launch_reduce<Tin, Tout, CW, S1, S2>(a, dev, s, a.tiles)));
+          FC_TRY(ipc_barrier(c, a, r, 1, s));
+          FC_TRY((launch_gather<Tout, CW, S2>(a, dev, s, (int64_t)(N - 1) * a.tiles)));
+        }
       } else {
         FC_TRY(gen_phase_scatter<Tin>(c, a, r, s));
         FC_TRY(ipc_barrier(c, a, r, 0, s));
@@ -299,11 +395,11 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
     if (p.fast && (c->fused == 1 || (c->fused == -1 && !single_dev))) {
       if (single_dev) {
         FC_CUDA_TRY(cudaSetDevice(c->devices[0]));
-        FC_TRY((launch_fused<Tin, Tout, CW>(c, a, 0, N, c->devices[0], st[0])));
+        FC_TRY((launch_fused<Tin, Tout, CW, S1, S2>(c, a, 0, N, c->devices[0], st[0])));
       } else {
         for (int r = 0; r < N; ++r) {
           FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
-          FC_TRY((launch_fused<Tin, Tout, CW>(c, a, r, r + 1, c->devices[r], st[r])));
+          FC_TRY((launch_fused<Tin, Tout, CW, S1, S2>(c, a, r, r + 1, c->devices[r], st[r])));
         }
       }
     } else if (p.fast && single_dev) {
@@ -311,29 +407,48 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
       FC_CUDA_TRY(cudaSetDevice(dev));
       a.rank_lo = 0;
       a.rank_hi = N;
-      FC_TRY((launch_scatter<Tin, CW>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
-      FC_TRY((launch_reduce<Tin, Tout, CW>(a, dev, st[0], (int64_t)N * a.tiles)));
-      FC_TRY((launch_gather<Tout, CW>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+      const int64_t dm = c->stream_mask;  // debug: bit k keeps kernel k on the staged path
+      if (use_stream && !(dm & 1))
+        FC_TRY((launch_qstream<Tin, S1>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+      else
+        FC_TRY((launch_scatter<Tin, CW, S1>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+      if (use_stream && !(dm & 2))
+        FC_TRY((launch_rstream<Tin, Tout, S1, S2>(a, dev, st[0], (int64_t)N * a.tiles)));
+      else
+        FC_TRY((launch_reduce<Tin, Tout, CW, S1, S2>(a, dev, st[0], (int64_t)N * a.tiles)));
+      if (use_stream && !(dm & 4))
+        FC_TRY((launch_dstream<Tout, S2>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+      else
+        FC_TRY((launch_gather<Tout, CW, S2>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
     } else if (p.fast) {
       for (int r = 0; r < N; ++r) {
         FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
         a.rank_lo = r;
         a.rank_hi = r + 1;
-        FC_TRY((launch_scatter<Tin, CW>(a, c->devices[r], st[r], (int64_t)(N - 1) * a.tiles)));
+        if (use_stream)
+          FC_TRY((launch_qstream<Tin, S1>(a, c->devices[r], st[r], (int64_t)(N - 1) * a.tiles)));
+        else
+          FC_TRY((launch_scatter<Tin, CW, S1>(a, c->devices[r], st[r], (int64_t)(N - 1) * a.tiles)));
       }
       FC_TRY(cross_sync(c, st));
       for (int r = 0; r < N; ++r) {
         FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
         a.rank_lo = r;
         a.rank_hi = r + 1;
-        FC_TRY((launch_reduce<Tin, Tout, CW>(a, c->devices[r], st[r], a.tiles)));
+        if (use_stream)
+          FC_TRY((launch_rstream<Tin, Tout, S1, S2>(a, c->devices[r], st[r], a.tiles)));
+        else
+          FC_TRY((launch_reduce<Tin, Tout, CW, S1, S2>(a, c->devices[r], st[r], a.tiles)));
       }
       FC_TRY(cross_sync(c, st));
       for (int r = 0; r < N; ++r) {
         FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
         a.rank_lo = r;
         a.rank_hi = r + 1;
-        FC_TRY((launch_gather<Tout, CW>(a, c->devices[r], st[r], (int64_t)(N - 1) * a.tiles)));
+        if (use_stream)
+          FC_TRY((launch_dstream<Tout, S2>(a, c->devices[r], st[r], (int64_t)(N - 1) * a.tiles)));
+        else
+          FC_TRY((launch_gather<Tout, CW, S2>(a, c->devices[r], st[r], (int64_t)(N - 1) * a.tiles)));
       }
     } else {
       for (int r = 0; r < N; ++r) {
@@ -366,8 +481,14 @@ template <typename Tin, typename Tout>
 fc_status run_typed(fc_comm* c, const void* const* ins, void* const* outs, int64_t n, const fc_flash_cfg* cfg,
                     cudaStream_t* st, int only_rank) {
   if (cfg->stage1.kind == FC_KIND_FP16 || cfg->stage2.kind == FC_KIND_FP16)
-    return run_typed_cw<Tin, Tout, 16>(c, ins, outs, n, cfg, st, only_rank);
-  return run_typed_cw<Tin, Tout, 8>(c, ins, outs, n, cfg, st, only_rank);
+    return run_typed_cw<Tin, Tout, 16, GenSpec, GenSpec>(c, ins, outs, n, cfg, st, only_rank);
+  if (c->fast) {  // compile-time schemes of the FlashConfig presets (from_bits 4 / 8 / 6)
+    const int a = spec_id(cfg->stage1), b = spec_id(cfg->stage2);
+    if (a == kSpecA4 && b == kSpecA4) return run_typed_cw<Tin, Tout, 8, SpecA4, SpecA4>(c, ins, outs, n, cfg, st, only_rank);
+    if (a == kSpecA8 && b == kSpecA8) return run_typed_cw<Tin, Tout, 8, SpecA8, SpecA8>(c, ins, outs, n, cfg, st, only_rank);
+    if (a == kSpecA4 && b == kSpecA8) return run_typed_cw<Tin, Tout, 8, SpecA4, SpecA8>(c, ins, outs, n, cfg, st, only_rank);
+  }
+  return run_typed_cw<Tin, Tout, 8, GenSpec, GenSpec>(c, ins, outs, n, cfg, st, only_rank);
 }
 
 template <typename Tin, typename Tout>

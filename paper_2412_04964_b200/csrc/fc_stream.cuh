@@ -1,0 +1,644 @@
+// Streaming phase kernels of the Flash All-Reduce (and the single-GPU codec)
+// for the compile-time lane codecs of fc_lane.cuh and 16-bit inputs.
+//
+// Work is a flat list of items (job, 8192-element tile) walked by persistent
+// CTAs. Quantize-type kernels (k_qstream: stage-1 scatter / codec quantize,
+// k_rstream: reduce) are fed by a dedicated producer warp that issues bulk
+// copies (cp.async.bulk, TMA engine) of whole tiles into an S-stage
+// shared-memory ring guarded by full/empty mbarriers; the 8 consumer warps
+// only compute. A consumer thread owns 32 contiguous elements (a group of
+// g elements spans g/32 lanes); it reads its 64 B from shared memory as four
+// 16-B vectors in a lane-rotated order (vector (q + rot) & 3 at step q,
+// rot = (lane >> 1) & 3), which makes every LDS.128 conflict-free; the
+// rotation is undone on the 4 (INT4) / 8 (INT8) packed code words, or on the
+// input words when decoded values must line up with other ranks' (reduce).
+// Codes leave as one/two coalesced 16-B stores per lane (a warp writes 512 B
+// contiguous), straight into the destination rank's slot (peer memory over
+// NVLink when the ranks are different GPUs).
+//
+// The dequantize-type kernel (k_dstream: all-gather decode / codec
+// dequantize) needs no group statistics, so it uses the transposed mapping:
+// thread t decodes 8-element blocks t, t+256, t+512, t+768 of a tile, which
+// makes both the code loads and the 16-B output stores coalesced.
+#pragma once
+
+#include "fc_flash.cuh"
+#include "fc_lane.cuh"
+#include "fc_tma.cuh"
+
+namespace fc {
+
+constexpr int kConsumerWarps = kThreads / 32;  // 8
+constexpr int kStreamThreads = kThreads + 32;  // + one producer warp
+
+// ------------------------------------------------------------------ jobs
+
+// quantize job y: source elements, element limit (elements at or past it
+// read as 0, collectives.py:145-149), destination slot, error word
+template <typename Tin>
+struct QJob {
+  const Tin* src;
+  int64_t limit;
+  uint8_t* dst;
+  uint32_t* err;
+  uint32_t ecode;
+};
+
+template <typename Tin>
+__device__ __forceinline__ QJob<Tin> qjob(const FlashArgs& a, int y) {
+  QJob<Tin> q;
+  if (a.mode == 1) {
+    q.src = reinterpret_cast<const Tin*>(a.in[0]);
+    q.limit = a.M;
+    q.dst = reinterpret_cast<uint8_t*>(a.out[0]);
+    q.err = a.cerr;
+    q.ecode = make_err(kErrNonFinite, 0, 0, 0);
+    return q;
+  }
+  int r, j;
+  pair_of(a, y, r, j);
+  const int64_t off = (int64_t)j * a.seg + a.sub_off;
+  q.src = reinterpret_cast<const Tin*>(a.in[r]) + off;
+  q.limit = a.M - off;
+  q.dst = recv_slot(a, j, r);
+  q.err = errw(a, r);
+  q.ecode = make_err(kErrNonFinite, kPhScatter, j, r);
+  return q;
+}
+
+__device__ __forceinline__ int64_t clamp0(int64_t v) { return v < 0 ? 0 : v; }
+
+// elements of tile t of a job that are real data (inside the round and below the limit)
+__device__ __forceinline__ int64_t tile_valid(int64_t len, int64_t limit, int64_t e0) {
+  return clamp0(min((int64_t)kTileElems, min(len - e0, limit - e0)));
+}
+
+// ------------------------------------------------------------------ stores
+
+template <class Spec>
+__device__ __forceinline__ void store_codes(const DevCodec& c, uint8_t* buf, int64_t p0, int nvalid,
+                                            const LaneQuant<8>& q, int lane) {
+  if (nvalid <= 0) return;
+  uint8_t* cp = buf + p0 * Spec::SB / 8;
+  st_v4(cp, make_uint4(q.w[0], q.w[1], q.w[2], q.w[3]));
+  if constexpr (Spec::SB == 8) st_v4(cp + 16, make_uint4(q.w[4], q.w[5], q.w[6], q.w[7]));
+  if ((lane & (c.lpg - 1)) == 0) {
+    const int64_t grp = p0 >> c.gshift;
+    reinterpret_cast<__half*>(buf + c.scales_off)[grp] = q.s16;
+    if constexpr (!Spec::SYM) buf[c.zeros_off + grp] = q.z8;
+  }
+}
+
+// undo the lane rotation of packed code words
+template <class Spec>
+__device__ __forceinline__ void unrotate_codes(uint32_t* w, int rot) {
+  if constexpr (Spec::SB == 4) {
+    unrotate4(w, rot);
+  } else {
+    uint32_t e[4] = {w[0], w[2], w[4], w[6]}, o[4] = {w[1], w[3], w[5], w[7]};
+    unrotate4(e, rot);
+    unrotate4(o, rot);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      w[2 * i] = e[i];
+      w[2 * i + 1] = o[i];
+    }
+  }
+}
+
+// read this thread's 64-B input chunk (rotated order) from a staged tile
+template <typename Tin>
+__device__ __forceinline__ void read_rotated(uint32_t tile, const uint32_t qoff[4], PackedLane<Tin>& L) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 u = lds128_(tile + qoff[q]);
+    L.w[4 * q] = u.x;
+    L.w[4 * q + 1] = u.y;
+    L.w[4 * q + 2] = u.z;
+    L.w[4 * q + 3] = u.w;
+  }
+}
+
+// put rotated input words back in element order (16 words = 4 vectors)
+template <typename Tin>
+__device__ __forceinline__ void unrotate_input(PackedLane<Tin>& L, int rot) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t v[4] = {L.w[c], L.w[4 + c], L.w[8 + c], L.w[12 + c]};
+    unrotate4(v, rot);
+    L.w[c] = v[0];
+    L.w[4 + c] = v[1];
+    L.w[8 + c] = v[2];
+    L.w[12 + c] = v[3];
+  }
+}
+
+// ------------------------------------------------------------------ item ranges
+
+// Each CTA walks a contiguous range of the flat item list (job-major,
+// tile-minor), so the (job, tile) pair advances by increment — no division
+// per item — and consecutive items of a CTA are consecutive tiles of one job.
+struct ItemRange {
+  int begin, end;  // flat items [begin, end)
+  int y, t;        // (job, tile) of `begin`
+};
+__device__ __forceinline__ ItemRange item_range(int items, int tiles) {
+  const int per = (items + (int)gridDim.x - 1) / (int)gridDim.x;
+  ItemRange r;
+  r.begin = min(items, (int)blockIdx.x * per);
+  r.end = min(items, r.begin + per);
+  r.y = r.begin / tiles;
+  r.t = r.begin - r.y * tiles;
+  return r;
+}
+__device__ __forceinline__ void item_next(int& y, int& t, int tiles) {
+  if (++t == tiles) {
+    t = 0;
+    ++y;
+  }
+}
+
+// ------------------------------------------------------------------ quantize stream
+
+// stage-1 scatter (mode 0: every (rank, peer) pair of [rank_lo, rank_hi)) or
+// codec quantize (mode 1)
+template <typename Tin, class S1>
+__global__ void __launch_bounds__(kStreamThreads) k_qstream(FlashArgs a) {
+  static_assert(sizeof(Tin) == 2, "16-bit inputs");
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr uint32_t STAGE = kTileElems * 2;
+  const int S = a.stages;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t full0 = sbase + S * STAGE, empty0 = full0 + 8 * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
+  const ItemRange R = item_range(njobs * a.tiles, a.tiles);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kConsumerWarps) {  // producer warp: one lane issues the bulk copies
+    if (lane == 0) {
+      int y = R.y, t = R.t, cy = -1, st = 0;
+      uint32_t ph = 0;
+      QJob<Tin> jb;
+      for (int i = R.begin; i < R.end; ++i) {
+        if (i - R.begin >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        if (y != cy) {
+          jb = qjob<Tin>(a, y);
+          cy = y;
+        }
+        const int64_t e0 = (int64_t)t * kTileElems;
+        const uint32_t bytes = (uint32_t)(tile_valid(a.sub_len, jb.limit, e0) * 2) & ~15u;
+        mbar_arrive_expect_tx(full0 + 8 * st, bytes);
+        if (bytes) bulk_g2s(sbase + st * STAGE, jb.src + e0, bytes, full0 + 8 * st);
+        item_next(y, t, a.tiles);
+        if (++st == S) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  const int rot = (lane >> 1) & 3;
+  uint32_t qoff[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) qoff[q] = threadIdx.x * 64 + 16 * ((q + rot) & 3);
+  int y = R.y, t = R.t, cy = -1, st = 0;
+  uint32_t ph = 0;
+  QJob<Tin> jb;
+  for (int i = R.begin; i < R.end; ++i) {
+    if (y != cy) {
+      jb = qjob<Tin>(a, y);
+      cy = y;
+    }
+    const int64_t p0 = (int64_t)t * kTileElems + threadIdx.x * kLaneElems;
+    const int nvalid = lane_valid(a.sub_len, p0);
+    const bool staged = nvalid == kLaneElems && p0 + kLaneElems <= jb.limit;
+    PackedLane<Tin> L;
+    mbar_wait(full0 + 8 * st, ph);
+    if (staged)
+      read_rotated(sbase + st * STAGE, qoff, L);
+    else
+      load_lane_src(jb.src, p0, jb.limit, nvalid, L);
+    LaneQuant<8> q;
+    const bool bad = quantize_lane<S1>(a.c1, L, nvalid, q);
+    // release the stage only after the shared loads were consumed: an LDS still
+    // in flight at the arrive could otherwise read the next tile's bulk copy
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);
+    if (staged) unrotate_codes<S1>(q.w, rot);
+    store_codes<S1>(a.c1, jb.dst, p0, nvalid, q, lane);
+    if (bad && jb.err) atomicOr(jb.err, jb.ecode);
+    item_next(y, t, a.tiles);
+    if (++st == S) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ reduce stream
+
+// bytes of one peer's staged piece of a tile: codes, scales, zeros (16-B aligned parts)
+__host__ __device__ inline uint32_t peer_codes_bytes(const DevCodec& c) { return kTileElems * c.sb / 8; }
+__host__ __device__ inline uint32_t peer_scale_bytes(const DevCodec& c) { return ((kTileElems / c.g) * 2 + 15) & ~15u; }
+__host__ __device__ inline uint32_t peer_meta_bytes(const DevCodec& c) {
+  const uint32_t groups = kTileElems / c.g;
+  return peer_scale_bytes(c) + (c.sym ? 0u : ((groups + 15) & ~15u));
+}
+__host__ __device__ inline uint32_t rstage_bytes(const DevCodec& c1, int world) {
+  return kTileElems * 2 + (uint32_t)(world - 1) * (peer_codes_bytes(c1) + peer_meta_bytes(c1));
+}
+
+__device__ __forceinline__ uint32_t up16(int64_t v) { return (uint32_t)((v + 15) & ~(int64_t)15); }
+
+// one received stage-1 lane chunk from the staged peer region `src`
+template <class S1>
+__device__ __forceinline__ void read_peer(const DevCodec& c1, uint32_t src, uint32_t PC, uint32_t SCB, uint32_t gl,
+                                          LaneCodes<8>& C) {
+  const uint32_t cp = src + threadIdx.x * (kLaneElems * S1::SB / 8);
+  const uint4 u = lds128_(cp);
+  C.w[0] = u.x;
+  C.w[1] = u.y;
+  C.w[2] = u.z;
+  C.w[3] = u.w;
+  if constexpr (S1::SB == 8) {
+    const uint4 u2 = lds128_(cp + 16);
+    C.w[4] = u2.x;
+    C.w[5] = u2.y;
+    C.w[6] = u2.z;
+    C.w[7] = u2.w;
+  }
+  unsigned short sh;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(src + PC + 2 * gl));
+  C.s = __half2float(__ushort_as_half(sh));
+  float zf;
+  if constexpr (S1::SYM) {
+    zf = (float)(1 << (c1.bits - 1));
+    const uint32_t xr = rep_xor(c1);
+#pragma unroll
+    for (int w = 0; w < S1::SB; ++w) C.w[w] ^= xr;
+  } else {
+    uint32_t zz;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(src + PC + SCB + gl));
+    zf = (float)zz;
+  }
+  C.mz = 8388608.0f + zf;
+}
+
+// owner j of [rank_lo, rank_hi): own segment QDQ + N-1 received pieces ->
+// fp32 sum (ascending source rank) -> stage-2 quantize -> every peer's
+// gather slot [j] + own output
+template <typename Tin, typename Tout, class S1, class S2>
+__global__ void __launch_bounds__(kStreamThreads) k_rstream(FlashArgs a) {
+  static_assert(sizeof(Tin) == 2, "16-bit inputs");
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int S = a.stages;
+  const uint32_t SBY = rstage_bytes(a.c1, a.world);
+  const uint32_t PC = peer_codes_bytes(a.c1), PM = peer_meta_bytes(a.c1), SCB = peer_scale_bytes(a.c1);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t full0 = sbase + S * SBY, empty0 = full0 + 8 * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ItemRange R = item_range((a.rank_hi - a.rank_lo) * a.tiles, a.tiles);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      int y = R.y, t = R.t, st = 0;
+      uint32_t ph = 0;
+      for (int i = R.begin; i < R.end; ++i) {
+        if (i - R.begin >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        const int j = a.rank_lo + y;
+        const int64_t e0 = (int64_t)t * kTileElems;
+        const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
+        const uint32_t own = (uint32_t)(tile_valid(a.sub_len, a.M - seg0, e0) * 2) & ~15u;
+        const int64_t v = clamp0(min((int64_t)kTileElems, a.sub_len - e0));
+        const int64_t grp0 = e0 >> a.c1.gshift, ng = (v + a.c1.g - 1) >> a.c1.gshift;
+        const uint32_t cb = v > 0 ? up16(v * a.c1.sb / 8) : 0u, sb = v > 0 ? up16(ng * 2) : 0u;
+        const uint32_t zb = (v > 0 && !a.c1.sym) ? up16(ng) : 0u;
+        const uint32_t st_base = sbase + st * SBY;
+        const uint32_t bar = full0 + 8 * st;
+        mbar_arrive_expect_tx(bar, own + (uint32_t)(a.world - 1) * (cb + sb + zb));
+        if (own) bulk_g2s(st_base, reinterpret_cast<const Tin*>(a.in[j]) + seg0 + e0, own, bar);
+        uint32_t dst = st_base + kTileElems * 2;
+        for (int s = 0; s < a.world; ++s) {
+          if (s == j) continue;
+          const uint8_t* slot = recv_slot(a, j, s);
+          if (cb) bulk_g2s(dst, slot + e0 * a.c1.sb / 8, cb, bar);
+          if (sb) bulk_g2s(dst + PC, slot + a.c1.scales_off + grp0 * 2, sb, bar);
+          if (zb) bulk_g2s(dst + PC + SCB, slot + a.c1.zeros_off + grp0, zb, bar);
+          dst += PC + PM;
+        }
+        item_next(y, t, a.tiles);
+        if (++st == S) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  const int rot = (lane >> 1) & 3;
+  uint32_t qoff[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) qoff[q] = threadIdx.x * 64 + 16 * ((q + rot) & 3);
+  const uint32_t gl = (uint32_t)((threadIdx.x * kLaneElems) >> a.c1.gshift);
+  int y = R.y, t = R.t, st = 0;
+  uint32_t ph = 0;
+  for (int i = R.begin; i < R.end; ++i) {
+    const int j = a.rank_lo + y;
+    const int64_t p0 = (int64_t)t * kTileElems + threadIdx.x * kLaneElems;
+    const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
+    const int nvalid = lane_valid(a.sub_len, p0);
+    const bool staged = nvalid == kLaneElems && seg0 + p0 + kLaneElems <= a.M;
+    const uint32_t st_base = sbase + st * SBY;
+    mbar_wait(full0 + 8 * st, ph);
+    // own piece: stage-1 QDQ in registers (collectives.py:364-365)
+    PairLane<S1::SB> acc, mine;
+    bool bad;
+    {
+      PackedLane<Tin> L;
+      if (staged) {
+        read_rotated(st_base, qoff, L);
+        unrotate_input(L, rot);
+      } else {
+        load_lane_src(reinterpret_cast<const Tin*>(a.in[j]) + seg0, p0, a.M - seg0, nvalid, L);
+      }
+      LaneQuant<8> q;
+      bad = quantize_lane<S1>(a.c1, L, nvalid, q);
+      LaneCodes<8> C;
+      lane_codes_from(a.c1, q, C);
+      decode_pairs<S1, false>(C, mine);
+    }
+    // fp32 sum in ascending source rank (collectives.py:182-187)
+    uint32_t src = st_base + kTileElems * 2;
+    if (j == 0) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc.p[e] = mine.p[e];
+    }
+    for (int s = 0; s < a.world; ++s) {
+      if (s == j) {
+        if (s != 0) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc.p[e] = f2_add(acc.p[e], mine.p[e]);
+        }
+        continue;
+      }
+      LaneCodes<8> C;
+      if (nvalid > 0) {
+        read_peer<S1>(a.c1, src, PC, SCB, gl, C);
+      } else {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) C.w[w] = 0;
+        C.s = 0.0f;
+        C.mz = 0.0f;
+      }
+      src += PC + PM;
+      if (s == 0)
+        decode_pairs<S1, false>(C, acc);
+      else
+        decode_pairs<S1, true>(C, acc);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);
+    LaneQuant<8> q2;
+    bad |= quantize_lane<S2>(a.c2, acc, nvalid, q2);
+    for (int p = j + 1;; ++p) {  // every peer's gather slot [j]
+      if (p == a.world) p = 0;
+      if (p == j) break;
+      store_codes<S2>(a.c2, gath_slot(a, p, j), p0, nvalid, q2, lane);
+    }
+    LaneCodes<8> L2;
+    lane_codes_from(a.c2, q2, L2);
+    PairLane<S2::SB> o;
+    decode_pairs<S2, false>(L2, o);  // owner decodes its own payload too (collectives.py:378)
+    if (nvalid > 0) {
+      float ov[kLaneElems];
+#pragma unroll
+      for (int e = 0; e < kLaneElems; ++e) ov[e] = o.get(e);
+      store_chunk(reinterpret_cast<Tout*>(a.out[j]), seg0 + p0, a.M, nvalid, ov);
+    }
+    if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
+    item_next(y, t, a.tiles);
+    if (++st == S) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ dequantize stream
+
+template <typename Tout>
+__device__ __forceinline__ void store8(Tout* p, const float v[8]) {
+  if constexpr (sizeof(Tout) == 4) {
+    st_v4(p, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])));
+    st_v4(p + 4, make_uint4(__float_as_uint(v[4]), __float_as_uint(v[5]), __float_as_uint(v[6]), __float_as_uint(v[7])));
+  } else {
+    st_v4(p, make_uint4(pack2(v[0], v[1], (Tout*)nullptr), pack2(v[2], v[3], (Tout*)nullptr),
+                        pack2(v[4], v[5], (Tout*)nullptr), pack2(v[6], v[7], (Tout*)nullptr)));
+  }
+}
+
+// decode the 8 stored codes of one block into v[0..7] (element order)
+template <class Spec>
+__device__ __forceinline__ void decode8(uint2 cw, float s, float mz, float v[8]) {
+  const uint64_t S2 = f2_splat(s), NMZ2 = f2_splat(-mz);
+  auto two = [&](uint32_t ma, uint32_t mb, float& x, float& y) {
+    uint64_t M;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(M) : "r"(ma), "r"(mb));
+    f2_unpack(f2_mul(f2_add(M, NMZ2), S2), x, y);
+  };
+  if constexpr (Spec::SB == 4) {
+    const uint32_t lo = cw.x & 0x0F0F0F0Fu, hi = (cw.x >> 4) & 0x0F0F0F0Fu;
+    two(__byte_perm(lo, 0x4B000000u, 0x7440u), __byte_perm(hi, 0x4B000000u, 0x7440u), v[0], v[1]);
+    two(__byte_perm(lo, 0x4B000000u, 0x7441u), __byte_perm(hi, 0x4B000000u, 0x7441u), v[2], v[3]);
+    two(__byte_perm(lo, 0x4B000000u, 0x7442u), __byte_perm(hi, 0x4B000000u, 0x7442u), v[4], v[5]);
+    two(__byte_perm(lo, 0x4B000000u, 0x7443u), __byte_perm(hi, 0x4B000000u, 0x7443u), v[6], v[7]);
+  } else {
+    two(__byte_perm(cw.x, 0x4B000000u, 0x7440u), __byte_perm(cw.x, 0x4B000000u, 0x7441u), v[0], v[1]);
+    two(__byte_perm(cw.x, 0x4B000000u, 0x7442u), __byte_perm(cw.x, 0x4B000000u, 0x7443u), v[2], v[3]);
+    two(__byte_perm(cw.y, 0x4B000000u, 0x7440u), __byte_perm(cw.y, 0x4B000000u, 0x7441u), v[4], v[5]);
+    two(__byte_perm(cw.y, 0x4B000000u, 0x7442u), __byte_perm(cw.y, 0x4B000000u, 0x7443u), v[6], v[7]);
+  }
+}
+
+// dequantize job y: quantized source, output span
+template <typename Tout>
+struct DJob {
+  const uint8_t* src;
+  Tout* out;
+  int64_t limit;  // valid output elements from `out`
+};
+
+template <typename Tout>
+__device__ __forceinline__ DJob<Tout> djob(const FlashArgs& a, int y) {
+  DJob<Tout> d;
+  if (a.mode == 1) {
+    d.src = reinterpret_cast<const uint8_t*>(a.in[0]);
+    d.out = reinterpret_cast<Tout*>(a.out[0]);
+    d.limit = a.M;
+    return d;
+  }
+  int r, j;
+  pair_of(a, y, r, j);
+  const int64_t off = (int64_t)j * a.seg + a.sub_off;
+  d.src = gath_slot(a, r, j);
+  d.out = reinterpret_cast<Tout*>(a.out[r]) + off;
+  d.limit = a.M - off;
+  return d;
+}
+
+// bytes of one staged code tile of the decode stream: codes, scales, zeros
+__host__ __device__ inline uint32_t dstage_bytes(const DevCodec& c) {
+  return peer_codes_bytes(c) + peer_meta_bytes(c);
+}
+
+// all-gather decode (mode 0: rank r's gather slot [j] -> out[r][segment j]
+// for every pair of [rank_lo, rank_hi)) or codec dequantize (mode 1).
+// A producer warp bulk-copies each tile's codes/scales/zeros into an S-stage
+// ring; consumer thread t decodes 8-element blocks t + 256*b (b = 0..3) of
+// the tile: conflict-free shared loads and coalesced 16-B output stores.
+template <typename Tout, class S2>
+__global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int kBlocks = kTileElems / 8 / kThreads;  // 4
+  const DevCodec& c = a.c2;
+  const int S = a.stages;
+  const uint32_t SBY = dstage_bytes(c), PC = peer_codes_bytes(c), SCB = peer_scale_bytes(c);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t full0 = sbase + S * SBY, empty0 = full0 + 8 * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
+  const ItemRange R = item_range(njobs * a.tiles, a.tiles);
+  const int gs = c.gshift;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      int y = R.y, t = R.t, cy = -1, st = 0;
+      uint32_t ph = 0;
+      DJob<Tout> d;
+      for (int i = R.begin; i < R.end; ++i) {
+        if (i - R.begin >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        if (y != cy) {
+          d = djob<Tout>(a, y);
+          cy = y;
+        }
+        const int64_t e0 = (int64_t)t * kTileElems;
+        const int64_t v = clamp0(min((int64_t)kTileElems, min(a.sub_len - e0, d.limit - e0)));
+        const int64_t grp0 = e0 >> gs, ng = (v + c.g - 1) >> gs;
+        const uint32_t cb = v > 0 ? up16(v * S2::SB / 8) : 0u, sb = v > 0 ? up16(ng * 2) : 0u;
+        const uint32_t zb = (v > 0 && !S2::SYM) ? up16(ng) : 0u;
+        const uint32_t dst = sbase + st * SBY, bar = full0 + 8 * st;
+        mbar_arrive_expect_tx(bar, cb + sb + zb);
+        if (cb) bulk_g2s(dst, d.src + e0 * S2::SB / 8, cb, bar);
+        if (sb) bulk_g2s(dst + PC, d.src + c.scales_off + grp0 * 2, sb, bar);
+        if (zb) bulk_g2s(dst + PC + SCB, d.src + c.zeros_off + grp0, zb, bar);
+        item_next(y, t, a.tiles);
+        if (++st == S) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  const uint32_t xr = rep_xor(c);
+  const float zsym = S2::SYM ? 8388608.0f + (float)(1 << (c.bits - 1)) : 0.0f;
+  const uint32_t code_off = threadIdx.x * S2::SB;                // bytes of 8 codes of SB bits
+  const uint32_t grp_off = (uint32_t)(threadIdx.x * 8) >> gs;    // tile-local group of block 0
+  const uint32_t grp_step = (uint32_t)(kThreads * 8) >> gs;      // groups per block step
+  int y = R.y, t = R.t, cy = -1, st = 0;
+  uint32_t ph = 0;
+  DJob<Tout> d;
+  for (int i = R.begin; i < R.end; ++i) {
+    if (y != cy) {
+      d = djob<Tout>(a, y);
+      cy = y;
+    }
+    const int64_t e0 = (int64_t)t * kTileElems;
+    const int64_t v = min(a.sub_len - e0, d.limit - e0);  // valid elements from e0
+    const uint32_t tile = sbase + st * SBY;
+    Tout* obase = d.out + e0 + threadIdx.x * 8;
+    uint2 cw[kBlocks];
+    float sc[kBlocks], mz[kBlocks];
+    mbar_wait(full0 + 8 * st, ph);
+#pragma unroll
+    for (int b = 0; b < kBlocks; ++b) {
+      const uint32_t ca = tile + code_off + b * kThreads * S2::SB;
+      if constexpr (S2::SB == 4) {
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw[b].x) : "r"(ca));
+        cw[b].y = 0;
+      } else {
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(cw[b].x), "=r"(cw[b].y) : "r"(ca));
+      }
+      const uint32_t g = grp_off + b * grp_step;
+      unsigned short sh;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(tile + PC + 2 * g));
+      sc[b] = __half2float(__ushort_as_half(sh));
+      if constexpr (S2::SYM) {
+        mz[b] = zsym;
+      } else {
+        uint32_t zz;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(tile + PC + SCB + g));
+        mz[b] = __uint_as_float(0x4B000000u | zz);
+      }
+    }
+    float val[kBlocks][8];
+#pragma unroll
+    for (int b = 0; b < kBlocks; ++b) {
+      uint2 w = cw[b];
+      if constexpr (S2::SYM) {
+        w.x ^= xr;
+        w.y ^= xr;
+      }
+      decode8<S2>(w, sc[b], mz[b], val[b]);
+    }
+    // release the stage after the shared loads were consumed (see k_qstream)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);
+    if (v >= kTileElems) {  // whole tile: no per-block checks
+#pragma unroll
+      for (int b = 0; b < kBlocks; ++b) store8(obase + b * kThreads * 8, val[b]);
+    } else {
+#pragma unroll
+      for (int b = 0; b < kBlocks; ++b) {
+        const int64_t e = (int64_t)(threadIdx.x + b * kThreads) * 8;
+        Tout* o = obase + b * kThreads * 8;
+        if (e + 8 <= v) {
+          store8(o, val[b]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (e + q < v) o[q] = DT<Tout>::from_f(val[b][q]);
+        }
+      }
+    }
+    item_next(y, t, a.tiles);
+    if (++st == S) {
+      st = 0;
+      ph ^= 1;
+    }
+  }
+}
+
+}  // namespace fc

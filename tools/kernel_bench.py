@@ -75,15 +75,17 @@ def flash_sweep(quick=False):
         w = cfg.stage1_codec.wire_byte_len(seg)
         alg = tp * (2 * e * M + 2 * (tp - 1) * 2 * w)
         for mode, opts in (("fused", {}), ("split", {_lib.OPT_FUSED: 0}),
-                           ("split_rs1", {_lib.OPT_FUSED: 0, _lib.OPT_REDUCE_STAGES: 1}),
+                           ("split_old", {_lib.OPT_FUSED: 0, _lib.OPT_FAST: 2}),
                            ("split_rs2", {_lib.OPT_FUSED: 0, _lib.OPT_REDUCE_STAGES: 2}),
+                           ("split_rs3", {_lib.OPT_FUSED: 0, _lib.OPT_REDUCE_STAGES: 3}),
                            ("fused_lag16", {_lib.OPT_LAG: 16})):
-            if quick and mode not in ("fused", "split", "split_rs1"):
+            if quick and mode not in ("fused", "split", "split_old", "split_rs2"):
                 continue
             comm.set_option(_lib.OPT_FUSED, 1)
             comm.set_option(_lib.OPT_CTAS, 0)
             comm.set_option(_lib.OPT_LAG, 0)
             comm.set_option(_lib.OPT_REDUCE_STAGES, 0)
+            comm.set_option(_lib.OPT_FAST, 1)
             for k, v in opts.items():
                 comm.set_option(k, v)
             t = timeit(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), iters=10, warm=3)
@@ -96,6 +98,34 @@ def flash_sweep(quick=False):
         torch.cuda.empty_cache()
 
 
+def tune_sweep():
+    """Ring depths / CTA caps of the streaming split kernels at C2 (8 logical ranks)."""
+    M, tp, e = 8 * 1024 * 8192, 8, 2
+    cfg = fc.FlashConfig.from_bits(4)
+    seg = M // tp
+    comm = FlashComm.local([0] * tp, slot_bytes_for(seg, cfg.stage1_codec, cfg.stage2_codec))
+    comm.set_option(_lib.OPT_FUSED, 0)
+    ins = [torch.randn(M, device="cuda").to(torch.bfloat16) for _ in range(tp)]
+    outs = [torch.empty_like(t) for t in ins]
+    w = cfg.stage1_codec.wire_byte_len(seg)
+    alg = tp * (2 * e * M + 2 * (tp - 1) * 2 * w)
+    grid = [dict()]
+    grid += [{_lib.OPT_SCATTER_STAGES: q} for q in (2, 3, 6, 8)]
+    grid += [{_lib.OPT_GATHER_STAGES: d} for d in (3, 4, 8, 12)]
+    grid += [{_lib.OPT_REDUCE_STAGES: r} for r in (1, 3, 4)]
+    grid += [{_lib.OPT_CTAS_PER_SM: c} for c in (1, 2, 3)]
+    for opts in grid:
+        for o in (_lib.OPT_SCATTER_STAGES, _lib.OPT_GATHER_STAGES, _lib.OPT_REDUCE_STAGES, _lib.OPT_CTAS_PER_SM):
+            comm.set_option(o, 0)
+        for k, v in opts.items():
+            comm.set_option(k, v)
+        t = timeit(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), iters=10, warm=3)
+        comm.check()
+        print(json.dumps({"kernel": "flash_split_tune", "opts": {str(k): v for k, v in opts.items()}, "ms": t,
+                          "frac": alg / t / 1e6 / PEAK}))
+    comm.close()
+
+
 if __name__ == "__main__":
     what = [a for a in sys.argv[1:] if not a.startswith("--")] or ["codec", "flash"]
     quick = "--quick" in sys.argv
@@ -103,3 +133,5 @@ if __name__ == "__main__":
         codec_sweep(quick)
     if "flash" in what:
         flash_sweep(quick)
+    if "tune" in what:
+        tune_sweep()
