@@ -139,6 +139,89 @@ __device__ __forceinline__ void lane_stats(const PairLane<SB>& L, int nvalid, fl
   lane_stats<SYM>(F, nvalid, lo, hi);
 }
 
+// ------------------------------------------------------------------ statistics
+
+__device__ __forceinline__ float fmin3_nan(float a, float b, float c) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmax3_nan(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// min/max (SYM: -, absmax) of a full 32-element fp32 lane with 3-input FMNMX3
+template <bool SYM, class Src>
+__device__ __forceinline__ void stats32_f32(const Src& L, float& lo, float& hi) {
+  float v[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = SYM ? fabsf(L.get(k)) : L.get(k);
+  float a[11], b[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    a[i] = fmin3_nan(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+    b[i] = fmax3_nan(v[3 * i], v[3 * i + 1], v[3 * i + 2]);
+  }
+  a[10] = fmin_nan(v[30], v[31]);
+  b[10] = fmax_nan(v[30], v[31]);
+  const float a0 = fmin3_nan(a[0], a[1], a[2]), a1 = fmin3_nan(a[3], a[4], a[5]), a2 = fmin3_nan(a[6], a[7], a[8]);
+  const float b0 = fmax3_nan(b[0], b[1], b[2]), b1 = fmax3_nan(b[3], b[4], b[5]), b2 = fmax3_nan(b[6], b[7], b[8]);
+  lo = fmin3_nan(fmin3_nan(a0, a1, a2), a[9], a[10]);
+  hi = fmax3_nan(fmax3_nan(b0, b1, b2), b[9], b[10]);
+}
+
+// group-wide min/max over lpg lanes (uniform), NaN-propagating
+__device__ __forceinline__ void group_minmax(float& lo, float& hi, int lpg) {
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    if (o < lpg) {
+      lo = fmin_nan(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax_nan(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+  }
+}
+// bf16-exact bounds: (lo, -hi) travel as one bf16x2 word, one shuffle + one HMNMX2 per step
+__device__ __forceinline__ void group_minmax_bf16(float& lo, float& hi, int lpg) {
+  uint32_t w = (__float_as_uint(lo) >> 16) | (__float_as_uint(-hi) & 0xFFFF0000u);
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    if (o < lpg) {
+      const uint32_t u = __shfl_xor_sync(0xffffffffu, w, o);
+      asm("min.NaN.bf16x2 %0, %1, %2;" : "=r"(w) : "r"(w), "r"(u));
+    }
+  }
+  lo = __uint_as_float(w << 16);
+  hi = -__uint_as_float(w & 0xFFFF0000u);
+}
+
+// full-lane statistics + group reduction for each source kind
+template <bool SYM, typename T>
+__device__ __forceinline__ void group_stats(const DevCodec& c, const PackedLane<T>& L, float& lo, float& hi) {
+  lane_stats<SYM>(L, kLaneElems, lo, hi);
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (SYM) lo = -hi;
+    group_minmax_bf16(lo, hi, c.lpg);
+  } else {
+    group_minmax(lo, hi, c.lpg);
+  }
+}
+template <bool SYM>
+__device__ __forceinline__ void group_stats(const DevCodec& c, const FloatLane& L, float& lo, float& hi) {
+  struct G {
+    const FloatLane& l;
+    __device__ float get(int k) const { return l.v[k]; }
+  } g{L};
+  stats32_f32<SYM>(g, lo, hi);
+  group_minmax(lo, hi, c.lpg);
+}
+template <bool SYM, int SB>
+__device__ __forceinline__ void group_stats(const DevCodec& c, const PairLane<SB>& L, float& lo, float& hi) {
+  stats32_f32<SYM>(L, lo, hi);
+  group_minmax(lo, hi, c.lpg);
+}
+
 // ------------------------------------------------------------------ group parameters
 
 struct GroupQ {
@@ -220,15 +303,8 @@ __device__ __forceinline__ void lane_codes_packed(const Src& L, const GroupQ& g,
 template <class Spec, int CW, class Src>
 __device__ __forceinline__ bool lane_quantize_fast(const DevCodec& c, const Src& L, LaneQuant<CW>& q) {
   float lo, hi;
-  if constexpr (Spec::SYM) {
-    lane_stats<true>(L, kLaneElems, lo, hi);
-    hi = group_allreduce_max(hi, c.lpg);
-    lo = -hi;
-  } else {
-    lane_stats<false>(L, kLaneElems, lo, hi);
-    lo = group_allreduce_min(lo, c.lpg);
-    hi = group_allreduce_max(hi, c.lpg);
-  }
+  group_stats<Spec::SYM>(c, L, lo, hi);
+  if constexpr (Spec::SYM) lo = -hi;
   const bool bad = !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
   GroupQ g;
   group_params<Spec>(c, lo, hi, g);
@@ -253,17 +329,20 @@ __device__ __forceinline__ bool lane_quantize_fast(const DevCodec& c, const Src&
 
 // Dispatch: the fast path for full chunks of a compile-time scheme, the
 // generic lane codec otherwise (tails, unusual schemes, fp16 passthrough).
+// The fast/generic choice is warp-uniform (__all_sync): both codecs reduce the
+// group bounds with full-warp shuffles, which every lane must execute at the
+// same instruction.
 template <class Spec, int CW, class Src>
 __device__ __forceinline__ bool quantize_lane(const DevCodec& c, const Src& L, int nvalid, LaneQuant<CW>& q) {
   if constexpr (Spec::kFast) {
-    if (nvalid == kLaneElems) return lane_quantize_fast<Spec>(c, L, q);
+    if (__all_sync(0xffffffffu, nvalid == kLaneElems)) return lane_quantize_fast<Spec>(c, L, q);
   }
   return lane_quantize(c, L, nvalid, q);
 }
 template <class Spec, int CW, int SB>
 __device__ __forceinline__ bool quantize_lane(const DevCodec& c, const PairLane<SB>& L, int nvalid, LaneQuant<CW>& q) {
   if constexpr (Spec::kFast) {
-    if (nvalid == kLaneElems) return lane_quantize_fast<Spec>(c, L, q);
+    if (__all_sync(0xffffffffu, nvalid == kLaneElems)) return lane_quantize_fast<Spec>(c, L, q);
   }
   FloatLane F;
   to_float_lane(L, F);

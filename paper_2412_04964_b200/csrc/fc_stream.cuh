@@ -296,7 +296,7 @@ __device__ __forceinline__ void read_peer(const DevCodec& c1, uint32_t src, uint
 // fp32 sum (ascending source rank) -> stage-2 quantize -> every peer's
 // gather slot [j] + own output
 template <typename Tin, typename Tout, class S1, class S2>
-__global__ void __launch_bounds__(kStreamThreads) k_rstream(FlashArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
   static_assert(sizeof(Tin) == 2, "16-bit inputs");
   extern __shared__ __align__(16) uint8_t smem[];
   const int S = a.stages;
@@ -382,34 +382,21 @@ __global__ void __launch_bounds__(kStreamThreads) k_rstream(FlashArgs a) {
       lane_codes_from(a.c1, q, C);
       decode_pairs<S1, false>(C, mine);
     }
-    // fp32 sum in ascending source rank (collectives.py:182-187)
+    // fp32 sum in ascending source rank (collectives.py:182-187): acc = ((0 + d_0) + d_1) + ...
+    // (0 + x == x exactly for every decoded x, none is -0)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc.p[e] = 0ull;
     uint32_t src = st_base + kTileElems * 2;
-    if (j == 0) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) acc.p[e] = mine.p[e];
-    }
     for (int s = 0; s < a.world; ++s) {
-      if (s == j) {
-        if (s != 0) {
+      if (s == j) {  // uniform
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc.p[e] = f2_add(acc.p[e], mine.p[e]);
-        }
+        for (int e = 0; e < 16; ++e) acc.p[e] = f2_add(acc.p[e], mine.p[e]);
         continue;
       }
       LaneCodes<8> C;
-      if (nvalid > 0) {
-        read_peer<S1>(a.c1, src, PC, SCB, gl, C);
-      } else {
-#pragma unroll
-        for (int w = 0; w < 8; ++w) C.w[w] = 0;
-        C.s = 0.0f;
-        C.mz = 0.0f;
-      }
+      read_peer<S1>(a.c1, src, PC, SCB, gl, C);  // lanes past the round read stale bytes (never stored)
       src += PC + PM;
-      if (s == 0)
-        decode_pairs<S1, false>(C, acc);
-      else
-        decode_pairs<S1, true>(C, acc);
+      decode_pairs<S1, true>(C, acc);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * st);
