@@ -45,11 +45,31 @@ CONFIGS = {
 
 
 def load_peaks() -> dict:
+    """HBM copy peak: MEASURED_PEAKS.json (driver-written on this pool) if present,
+    else the fallback of B200_PROFILING.md (6.65 TB/s)."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
-        with open(p) as fh:
-            d = json.load(fh)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+        try:
+            with open(p) as fh:
+                d = json.load(fh)
+            flat = {}
+
+            def walk(o, pre=""):
+                if isinstance(o, dict):
+                    for k, v in o.items():
+                        walk(v, pre + k + ".")
+                elif isinstance(o, (int, float)):
+                    flat[pre[:-1]] = float(o)
+
+            walk(d)
+            for k in ("hbm_gbs", "hbm.gbs", "hbm_GBps"):
+                if k in flat:
+                    return {"hbm_gbs": flat[k], "source": f"measured (MEASURED_PEAKS.json {k})"}
+            for k, v in flat.items():
+                if "hbm" in k.lower() and "gb" in k.lower() and v > 100:
+                    return {"hbm_gbs": v, "source": f"measured (MEASURED_PEAKS.json {k})"}
+        except Exception:
+            pass
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
@@ -115,35 +135,62 @@ def wire_len(bits: int, group: int, n: int) -> int:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference itself (baseline/_ref) if installed, else the oracle port
+# CPU baseline: the reference's algorithm (oracle port, test infrastructure) on
+# the host cores. Owners' segments are independent (collectives.py:355-386) and
+# results are chunk-transparent at group multiples (collectives.py:14-16), so
+# the sample is split into (owner, piece) jobs run by a fork pool on every core.
+
+_REF = {}
 
 
-def cpu_reference_step(tp: int, elems: int, bits: int, group: int, seed: int = 0):
+def _ref_job(job):
+    from oracle import flash_oracle as orc
+
+    j, lo, hi = job
+    xs, c1, c2, seg = _REF["xs"], _REF["c1"], _REF["c2"], _REF["seg"]
+    parts = [orc.dequantize(orc.quantize(x[j * seg + lo: j * seg + hi], c1)) for x in xs]
+    red = orc.sequential_sum(parts)  # ascending source rank (collectives.py:182-187)
+    return orc.dequantize(orc.quantize(red, c2))
+
+
+def cpu_reference_run(tp: int, elems: int, bits: int, group: int, workers: int, seed: int = 0):
+    """One flash all-reduce of `tp` ranks x `elems` elements through the oracle
+    port, split over `workers` processes. Returns (seconds, output of rank 0)."""
+    import multiprocessing as mp
+
     import numpy as np
 
-    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    from oracle import flash_oracle as orc
+
     rng = np.random.default_rng(seed)
-    xs = [rng.standard_normal(elems).astype(np.float32) for _ in range(tp)]
-    if os.path.isdir(os.path.join(ref_dir, "qcollectives")):
-        sys.path.insert(0, ref_dir)
-        import qcollectives as qc  # the unmodified reference, installed offline
-
-        cfg = qc.FlashConfig.from_bits(bits, group_size=group)
-        t0 = time.perf_counter()
-        qc.flash_all_reduce(xs, cfg)
-        return time.perf_counter() - t0, "reference", tp, "qcollectives.flash_all_reduce (one Python thread per rank, GIL-bound)"
-    from oracle import flash_oracle as orc  # port (test infrastructure), only as the CPU baseline
-
+    seg = -(-elems // tp)
+    xs = [np.pad(rng.standard_normal(elems).astype(np.float32), (0, tp * seg - elems)) for _ in range(tp)]
     c = orc.Codec(bits=bits, group_size=group)
+    _REF.update(xs=xs, c1=c, c2=c, seg=seg)
+    pieces = max(1, -(-workers // tp))
+    per = -(-(-(-seg // pieces)) // group) * group
+    jobs = [(j, lo, min(seg, lo + per)) for j in range(tp) for lo in range(0, seg, per)]
     t0 = time.perf_counter()
-    orc.flash_all_reduce(xs, c, c)
-    return time.perf_counter() - t0, "port", 1, "oracle/flash_oracle.py numpy restatement (single thread)"
+    if workers <= 1:
+        outs = [_ref_job(jb) for jb in jobs]
+    else:
+        with mp.get_context("fork").Pool(workers) as pool:
+            outs = pool.map(_ref_job, jobs, chunksize=1)
+    dt = time.perf_counter() - t0
+    return dt, np.concatenate(outs)[:elems]
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 def cpu_sample_elems(cfg: dict) -> int:
-    # bounded sample: 1/64 of the C2 per-rank tensor (1,048,576 elements), ~few s of CPU
+    # bounded sample: 1/16 of the C2 per-rank tensor (4,194,304 elements per rank)
     m = math.prod(cfg["shape"])
-    return max(cfg["tp"] * 1024, min(m, 1 << 20))
+    return max(cfg["tp"] * 1024, min(m, 1 << 22))
 
 
 def run_reference(args, cfg):
@@ -152,20 +199,23 @@ def run_reference(args, cfg):
         return
     elems = cpu_sample_elems(cfg)
     e = 2
+    workers = host_threads()
     times = []
-    kind = cores = note = None
     for i in range(args.warmup + args.steps):
-        dt, kind, cores, note = cpu_reference_step(cfg["tp"], elems, cfg["bits"], cfg["group"], seed=i)
+        dt, _ = cpu_reference_run(cfg["tp"], elems, cfg["bits"], cfg["group"], workers, seed=i)
         if i >= args.warmup:
             times.append(dt)
     t = statistics.mean(times)
     val = cfg["tp"] * e * elems / t / 1e9
-    sample = f"{cfg['tp']} ranks x {elems} elements (fp32 arrays of bf16-sized work; {elems / math.prod(cfg['shape']):.4f} of the per-rank tensor)"
+    sample = (f"{cfg['tp']} ranks x {elems} elements per rank ({elems / math.prod(cfg['shape']):.4f} of the "
+              f"per-rank tensor), fp32 arrays of bf16-valued work")
+    note = (f"oracle/flash_oracle.py numpy restatement of qcollectives.flash_all_reduce (the reference is Python "
+            f"and cannot travel to the GPU box), (owner, piece) jobs on a {workers}-process fork pool")
     line = {"impl": "reference", "metric": args.metric, "value": val, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["desc"], "tp": cfg["tp"], "sample": sample},
-            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": workers, "kind": "port", "sample": sample,
                              "host_cpus": os.cpu_count(), "note": note},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -179,6 +229,51 @@ def _dtype(name):
     import torch
 
     return {"bf16": torch.bfloat16, "fp16": torch.float16}[name]
+
+
+def _events_time(fn, steps, stream):
+    """(average ms, list of per-step ms) of `steps` calls, CUDA events on `stream`."""
+    import torch
+
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    torch.cuda.synchronize()
+    evs[0].record(stream)
+    for i in range(steps):
+        fn()
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]
+    return evs[0].elapsed_time(evs[-1]) / steps, per
+
+
+def graph_time(fn, reps, stream) -> float:
+    """Average device ms of one `fn` call: `reps` calls captured in a CUDA graph,
+    the graph replayed 5 times between CUDA events."""
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        for _ in range(reps):
+            fn()
+    gr.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(5):
+        gr.replay()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / (5 * reps)
+
+
+def load_traffic() -> dict:
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return {}
 
 
 def bench_local(args, cfg, peaks):
@@ -201,43 +296,51 @@ def bench_local(args, cfg, peaks):
         comm.set_option(_lib.OPT_CTAS, args.ctas)
     if args.lag:
         comm.set_option(_lib.OPT_LAG, args.lag)
-    if args.split:
-        comm.set_option(_lib.OPT_FUSED, 0)
     if args.fused:
         comm.set_option(_lib.OPT_FUSED, 1)
     g = torch.Generator(device=dev).manual_seed(1234)
     ins = [torch.randn(m, device=dev, generator=g).to(dt) for _ in range(tp)]
     outs = [torch.empty(m, device=dev, dtype=dt) for _ in range(tp)]
     stream = torch.cuda.current_stream(dev)
+    step = lambda: comm.all_reduce_local(ins, fcfg, outs=outs, check=False)  # noqa: E731
     for _ in range(args.warmup):
-        comm.all_reduce_local(ins, fcfg, outs=outs, check=False)
+        step()
     comm.check()
     launches_per_step = comm.get_option(_lib.OPT_LAST_LAUNCHES)
     clocks = ClockSampler(0)
     clocks.start()
-    torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    t0.record(stream)
-    evs[0].record(stream)
-    for i in range(args.steps):
-        comm.all_reduce_local(ins, fcfg, outs=outs, check=False)
-        evs[i + 1].record(stream)
-    t1.record(stream)
-    torch.cuda.synchronize()
+    ms, per = _events_time(step, args.steps, stream)
     clk = clocks.stop()
     comm.check()
-    total_ms = t0.elapsed_time(t1)
-    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-    ms = total_ms / args.steps
-    # algorithmic HBM bytes of one step (all TP ranks on this GPU), SURVEY §8(d):
-    # per rank 2*e*M + 2*(N-1)*(W1(seg)+W2(seg))
-    w = wire_len(cfg["bits"], cfg["group"], seg)
-    alg_bytes = tp * (2 * e * m + 2 * (tp - 1) * 2 * w)
-    kernel_ms = total_ms / (args.steps * launches_per_step)
-    achieved = alg_bytes / launches_per_step / (kernel_ms * 1e-3) / 1e9
     value = tp * e * m / (ms * 1e-3) / 1e9
+
+    # ---- per-phase kernels (measurement option: one phase per call), CUDA events on the launch stream
+    b1 = wire_len(cfg["bits"], cfg["group"], seg) / seg
+    b2 = b1
+    phase_bytes = {"scatter": tp * (tp - 1) * seg * (e + b1),
+                   "reduce": tp * seg * (2 * e + (tp - 1) * (b1 + b2)),
+                   "gather": tp * (tp - 1) * seg * (b2 + e)}
+    phase_kernel = {"scatter": "k_qstream", "reduce": "k_rstream", "gather": "k_dstream"}
+    phases = {}
+    for bit, name in ((1, "scatter"), (2, "reduce"), (4, "gather")):
+        comm.set_option(_lib.OPT_PHASES, bit)
+        for _ in range(2):
+            step()
+        pms, _ = _events_time(step, max(5, args.steps), stream)
+        phases[name] = {"kernel": phase_kernel[name], "us": pms * 1e3, "alg_bytes": phase_bytes[name],
+                        "gbs": phase_bytes[name] / (pms * 1e-3) / 1e9,
+                        "frac": phase_bytes[name] / (pms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+    comm.set_option(_lib.OPT_PHASES, 0)
+    dom = max(phases, key=lambda k: phases[k]["us"])
+    traffic = load_traffic().get(phases[dom]["kernel"])
+    alg_step = sum(phase_bytes.values())
+    roofline = {"bound": "hbm", "kernel": phases[dom]["kernel"], "achieved": phases[dom]["gbs"],
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": phases[dom]["frac"],
+                "traffic": traffic, "alg_bytes_per_launch": phases[dom]["alg_bytes"],
+                "kernel_us": phases[dom]["us"], "peak_source": peaks["source"],
+                "step": {"alg_bytes": alg_step, "achieved": alg_step / (ms * 1e-3) / 1e9,
+                         "frac": alg_step / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "t_roof_us": alg_step / peaks["hbm_gbs"] / 1e3}}
 
     # ---- e2e: reference-facing call with HOST buffers (pinned), H2D + D2H inside the timed region
     host_in = [t.cpu().pin_memory() for t in ins]
@@ -245,38 +348,72 @@ def bench_local(args, cfg, peaks):
     e2e_steps = max(1, min(args.steps, 5))
     fc.flash_all_reduce(host_in, fcfg, comm=comm)  # warm
     torch.cuda.synchronize()
-    a0 = torch.cuda.Event(enable_timing=True)
-    a1 = torch.cuda.Event(enable_timing=True)
-    a0.record(stream)
-    for _ in range(e2e_steps):
+
+    def e2e_step():
         run = fc.flash_all_reduce(host_in, fcfg, comm=comm)
         host_out.copy_(run.outputs[0], non_blocking=True)
-    a1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = a0.elapsed_time(a1) / e2e_steps
+
+    e2e_ms, _ = _events_time(e2e_step, e2e_steps, stream)
     e2e = {"value": tp * e * m / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
            "h2d_bytes_per_step": tp * e * m, "d2h_bytes_per_step": e * m,
            "path": "flash_all_reduce(list of pinned host bf16 tensors) -> C-ABI fc_flash_all_reduce_local -> D2H of rank 0"}
+    comm.close()
+    del outs
+
+    # ---- C5: single-GPU codec kernels on the same activation (HBM roofline), C-ABI calls
+    # captured in a CUDA graph so the timing is device time only
+    import ctypes as C
+
+    codec = {}
+    x = ins[0]
+    xo = torch.empty(m, device=dev, dtype=dt)
+    sdt = {torch.bfloat16: _lib.DTYPE_BF16, torch.float16: _lib.DTYPE_F16}[dt]
+    for bits in (4, 8):
+        cc = fc.CodecConfig(bits=bits, group_size=cfg["group"])
+        L = cc.device_layout(m)
+        qbuf = torch.empty(int(L.total_bytes), dtype=torch.uint8, device=dev)
+        cfc = cc.to_fc()
+        qf = lambda: _lib.check(_lib.lib().fc_quantize(  # noqa: E731
+            x.data_ptr(), sdt, m, C.byref(cfc), qbuf.data_ptr(), None, torch.cuda.current_stream().cuda_stream))
+        df = lambda: _lib.check(_lib.lib().fc_dequantize(  # noqa: E731
+            qbuf.data_ptr(), m, C.byref(cfc), xo.data_ptr(), sdt, torch.cuda.current_stream().cuda_stream))
+        qms, dms = graph_time(qf, 10, stream), graph_time(df, 10, stream)
+        ab = e * m + int(L.wire_bytes)
+        codec[f"int{bits}_g{cfg['group']}"] = {
+            "quantize_us": qms * 1e3, "quantize_gbs": ab / (qms * 1e-3) / 1e9,
+            "dequantize_us": dms * 1e3, "dequantize_gbs": ab / (dms * 1e-3) / 1e9,
+            "frac_quantize": ab / (qms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "frac_dequantize": ab / (dms * 1e-3) / 1e9 / peaks["hbm_gbs"], "alg_bytes": ab}
+    del ins, xo
+    torch.cuda.empty_cache()
+
+    # ---- C4: decode-regime latency (TP=8 emulated, bs x 8192 bf16 per rank), one all-reduce
+    # per CUDA-graph node (device time; the host launch path is not in the number)
+    decode = {}
+    for bs in (8, 64):
+        md = bs * 8192
+        dcomm = FlashComm.local([0] * tp, slot_bytes_for(-(-md // tp), fcfg.stage1_codec, fcfg.stage2_codec))
+        dins = [torch.randn(md, device=dev, generator=g).to(dt) for _ in range(tp)]
+        douts = [torch.empty_like(t) for t in dins]
+        dstep = lambda: dcomm.all_reduce_local(dins, fcfg, outs=douts, check=False)  # noqa: E731
+        dms = graph_time(dstep, 20, stream)
+        dcomm.check()
+        decode[f"bs{bs}"] = {"latency_us": dms * 1e3, "elems_per_rank": md, "timing": "CUDA graph of 20 calls"}
+        dcomm.close()
 
     # ---- CPU baseline on the host cores (bounded sample)
     cpu = None
     if not args.no_cpu:
         elems = cpu_sample_elems(cfg)
-        dts = []
-        for i in range(2):
-            d, kind, cores, note = cpu_reference_step(tp, elems, cfg["bits"], cfg["group"], seed=i)
-            dts.append(d)
+        workers = host_threads()
+        dts = [cpu_reference_run(tp, elems, cfg["bits"], cfg["group"], workers, seed=i)[0] for i in range(2)]
         cv = tp * e * elems / min(dts) / 1e9
-        cpu = {"value": cv, "unit": "GB/s", "cores": cores, "kind": kind, "host_cpus": os.cpu_count(),
+        cpu = {"value": cv, "unit": "GB/s", "cores": workers, "kind": "port", "host_cpus": os.cpu_count(),
                "sample": f"{tp} ranks x {elems} elements per rank ({elems / m:.4f} of the per-rank tensor), best of 2",
-               "note": note, "gpu_speedup": value / cv}
+               "note": "oracle/flash_oracle.py numpy restatement of the reference, (owner, piece) jobs on a process pool",
+               "gpu_speedup": value / cv}
 
-    traffic = None
-    tp_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp_path):
-        with open(tp_path) as fh:
-            traffic = json.load(fh).get(f"{args.config}_fused")
-    line = {
+    return {
         "metric": args.metric, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic (torch.randn, seed 1234)",
@@ -287,15 +424,10 @@ def bench_local(args, cfg, peaks):
                    "mode": "fused" if args.fused else "phase-split (auto: all ranks share one GPU)"},
         "latency_us": ms * 1e3, "latency_us_median": statistics.median(per) * 1e3,
         "algbw_gbs": e * m / (ms * 1e-3) / 1e9,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                     "alg_bytes_per_launch": alg_bytes / launches_per_step, "kernel_ms": kernel_ms,
-                     "peak_source": peaks["source"]},
+        "roofline": roofline, "phases": phases, "codec_c5": codec, "decode_c4": decode,
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(args.steps * launches_per_step),
         "clocks": clk, "nccl_bf16": None,
     }
-    comm.close()
-    return line
 
 
 def bench_dist(args, cfg, peaks):
@@ -399,7 +531,6 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--lag", type=int, default=0)
-    ap.add_argument("--split", action="store_true", help="phase-split kernels instead of the fused kernel")
     ap.add_argument("--fused", action="store_true", help="force the fused flag-synchronised kernel")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()

@@ -407,19 +407,26 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
       FC_CUDA_TRY(cudaSetDevice(dev));
       a.rank_lo = 0;
       a.rank_hi = N;
-      const int64_t dm = c->stream_mask;  // debug: bit k keeps kernel k on the staged path
-      if (use_stream && !(dm & 1))
-        FC_TRY((launch_qstream<Tin, S1>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
-      else
-        FC_TRY((launch_scatter<Tin, CW, S1>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
-      if (use_stream && !(dm & 2))
-        FC_TRY((launch_rstream<Tin, Tout, S1, S2>(a, dev, st[0], (int64_t)N * a.tiles)));
-      else
-        FC_TRY((launch_reduce<Tin, Tout, CW, S1, S2>(a, dev, st[0], (int64_t)N * a.tiles)));
-      if (use_stream && !(dm & 4))
-        FC_TRY((launch_dstream<Tout, S2>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
-      else
-        FC_TRY((launch_gather<Tout, CW, S2>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+      const int64_t dm = c->stream_mask;  // testing: bit k keeps phase k on the staged kernel
+      const int64_t pm = c->phases ? c->phases : 7;  // measurement: run only the selected phases
+      if (pm & 1) {
+        if (use_stream && !(dm & 1))
+          FC_TRY((launch_qstream<Tin, S1>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+        else
+          FC_TRY((launch_scatter<Tin, CW, S1>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+      }
+      if (pm & 2) {
+        if (use_stream && !(dm & 2))
+          FC_TRY((launch_rstream<Tin, Tout, S1, S2>(a, dev, st[0], (int64_t)N * a.tiles)));
+        else
+          FC_TRY((launch_reduce<Tin, Tout, CW, S1, S2>(a, dev, st[0], (int64_t)N * a.tiles)));
+      }
+      if (pm & 4) {
+        if (use_stream && !(dm & 4))
+          FC_TRY((launch_dstream<Tout, S2>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+        else
+          FC_TRY((launch_gather<Tout, CW, S2>(a, dev, st[0], (int64_t)N * (N - 1) * a.tiles)));
+      }
     } else if (p.fast) {
       for (int r = 0; r < N; ++r) {
         FC_CUDA_TRY(cudaSetDevice(c->devices[r]));

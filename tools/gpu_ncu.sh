@@ -15,4 +15,5 @@ for r in split codec; do
   sz=$(stat -c %s /tmp/ncu/prof_$r.ncu-rep 2>/dev/null || echo 0)
   if [ "$sz" -lt 20000000 ]; then cp /tmp/ncu/prof_$r.ncu-rep gpurun_out/; fi
 done
+python tools/make_traffic.py /tmp/ncu/prof_split.ncu-rep gpurun_out/ncu_traffic.json > /dev/null 2>&1
 cat gpurun_out/ncu_split_summary.txt gpurun_out/ncu_codec_summary.txt

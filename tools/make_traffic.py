@@ -1,0 +1,30 @@
+"""profiles/ncu_traffic.json: DRAM bytes (read + write) per launch of each
+streaming kernel, from one `ncu --set full` report (bench.py's roofline.traffic).
+usage: python tools/make_traffic.py report.ncu-rep [out.json]"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep = sys.argv[1]
+out = sys.argv[2] if len(sys.argv) > 2 else "profiles/ncu_traffic.json"
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr = rows[0]
+res = {}
+for r in rows[2:]:
+    d = dict(zip(hdr, r))
+    name = d.get("Kernel Name", "")
+    short = name.split("<")[0].split("(")[0].split()[-1]
+    try:
+        # ncu reports MB in the raw page for dram__bytes_*.sum (unit row says Mbyte)
+        unit = dict(zip(hdr, rows[1])).get("dram__bytes_read.sum", "byte")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+        b = (float(d["dram__bytes_read.sum"].replace(",", "")) + float(d["dram__bytes_write.sum"].replace(",", ""))) * scale
+    except (KeyError, ValueError):
+        continue
+    res.setdefault(short, b)
+with open(out, "w") as fh:
+    json.dump(res, fh, indent=1)
+print(json.dumps(res))

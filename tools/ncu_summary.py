@@ -15,7 +15,9 @@ keys = {
     "gpu__time_duration.sum": "dur",
     "dram__bytes_read.sum": "dram_rd",
     "dram__bytes_write.sum": "dram_wr",
-    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram%",
+    "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram%",
+    "dram__bytes.sum.peak_sustained": "dram_peak_B/cyc",
+    "dram__bytes.sum.per_second": "dram_B/s",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm%",
     "smsp__inst_executed.sum": "inst",
     "launch__registers_per_thread": "regs",
