@@ -322,6 +322,7 @@ def bench_local(args, cfg, peaks):
                    "gather": tp * (tp - 1) * seg * (b2 + e)}
     phase_kernel = {"scatter": "k_qstream", "reduce": "k_rstream", "gather": "k_dstream"}
     phases = {}
+    comm.set_option(_lib.OPT_FUSED, 0)  # phase kernels are timed on the split path
     for bit, name in ((1, "scatter"), (2, "reduce"), (4, "gather")):
         comm.set_option(_lib.OPT_PHASES, bit)
         for _ in range(2):
@@ -331,6 +332,7 @@ def bench_local(args, cfg, peaks):
                         "gbs": phase_bytes[name] / (pms * 1e-3) / 1e9,
                         "frac": phase_bytes[name] / (pms * 1e-3) / 1e9 / peaks["hbm_gbs"]}
     comm.set_option(_lib.OPT_PHASES, 0)
+    comm.set_option(_lib.OPT_FUSED, 1 if args.fused else -1)
     dom = max(phases, key=lambda k: phases[k]["us"])
     traffic = load_traffic().get(phases[dom]["kernel"])
     alg_step = sum(phase_bytes.values())

@@ -124,8 +124,9 @@ FC_API fc_status fc_comm_ipc_open(fc_comm* comm, const void* handles /* world * 
 FC_API fc_status fc_comm_destroy(fc_comm* comm);
 
 typedef enum {
-  FC_OPT_FUSED = 0,        /* 1: one persistent kernel with per-tile flags; 0: phase-split; -1 (default):
-                              fused except when every rank shares one GPU (no link to overlap) */
+  FC_OPT_FUSED = 0,        /* 1: one persistent kernel with per-tile flags (the streaming fused kernel when
+                              the scheme has a compile-time codec, else the staged one); 0: phase-split;
+                              -1 (default): fused across GPUs, phase-split when all ranks share one GPU */
   FC_OPT_CTAS = 1,         /* CTAs per rank for the fused kernel (0 = auto) */
   FC_OPT_TIMEOUT_MS = 2,   /* flag-wait timeout -> ProtocolError (fabric.py:158-178); default 5000 */
   FC_OPT_LAG = 3,          /* fused schedule: tiles between a tile's scatter and its reduce (0 = auto) */
@@ -136,7 +137,8 @@ typedef enum {
   FC_OPT_GATHER_STAGES = 8, /* ring depth of the streaming gather / dequantize kernel (0 = auto) */
   FC_OPT_CTAS_PER_SM = 9,   /* cap on resident CTAs per SM of the streaming kernels (0 = occupancy) */
   FC_OPT_STREAM_MASK = 10,  /* testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels */
-  FC_OPT_PHASES = 11        /* measurement only: run just these phases (bit 0/1/2) of a one-GPU split call */
+  FC_OPT_PHASES = 11,       /* measurement only: run just these phases (bit 0/1/2) of a one-GPU split call */
+  FC_OPT_ROLE_WEIGHTS = 12  /* fused stream kernel CTA roles: scatter | reduce << 8 | gather << 16 (sum <= 16) */
 } fc_option;
 FC_API fc_status fc_comm_set_option(fc_comm* comm, int32_t option, int64_t value);
 FC_API fc_status fc_comm_get_option(fc_comm* comm, int32_t option, int64_t* value);

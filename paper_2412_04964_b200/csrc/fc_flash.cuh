@@ -39,6 +39,10 @@ struct FlashArgs {
   int stage_hint;           // host-side override of the reduce ring depth (0 = auto)
   int q_hint, d_hint;       // ring depths of the streaming scatter / gather kernels (0 = auto)
   int cta_cap;              // resident CTAs per SM cap for the streaming kernels (0 = occupancy)
+  int role_period;          // fused stream kernel: CTA role pattern length (<= 16)
+  uint32_t role_pat;        // 2 bits per slot: 0 scatter, 1 reduce, 2 gather
+  int q_stages_f, r_stages_f, d_stages_f;  // fused stream kernel ring depths per role
+  int sys_scope;            // flags cross GPUs: system-scope fences; else gpu scope (one GPU)
   DevCodec c1, c2;
   int mode;                 // 0: flash all-reduce; 1: single-GPU codec job (in[0] -> out[0], c1)
   uint32_t* cerr;           // mode 1: error word

@@ -306,6 +306,70 @@ fc_status launch_dstream(FlashArgs a, int dev, cudaStream_t st, int64_t items) {
   }
 }
 
+// Fused streaming kernel (fc_stream.cuh k_fstream): role pattern from weights
+// (scatter : reduce : gather CTAs), interleaved over the period.
+inline void role_pattern(int wq, int wr, int wd, FlashArgs& a) {
+  const int w[3] = {std::max(0, wq), std::max(0, wr), std::max(0, wd)};
+  int per = w[0] + w[1] + w[2];
+  if (per <= 0 || per > 16) {
+    per = 8;
+  }
+  const int ww[3] = {per == w[0] + w[1] + w[2] ? w[0] : 3, per == w[0] + w[1] + w[2] ? w[1] : 2,
+                     per == w[0] + w[1] + w[2] ? w[2] : 3};
+  // largest-remainder interleave: slot k gets the role furthest behind its share
+  double acc[3] = {0, 0, 0};
+  uint32_t pat = 0;
+  for (int k = 0; k < per; ++k) {
+    int best = -1;
+    double bv = -1e9;
+    for (int r = 0; r < 3; ++r) {
+      if (ww[r] == 0) continue;
+      const double v = (double)ww[r] * (k + 1) / per - acc[r];
+      if (v > bv) {
+        bv = v;
+        best = r;
+      }
+    }
+    acc[best] += 1.0;
+    pat |= (uint32_t)best << (2 * k);
+  }
+  a.role_period = per;
+  a.role_pat = pat;
+}
+
+template <typename Tin, typename Tout, class S1, class S2>
+fc_status launch_fstream(const fc_comm* c, FlashArgs a, int rank_lo, int rank_hi, int dev, cudaStream_t st) {
+  if constexpr (sizeof(Tin) != 2 || !S1::kFast || !S2::kFast) {
+    return fail(FC_ERR_CONFIG, "stream kernels need 16-bit inputs and a compile-time codec");
+  } else {
+    const void* kern = (const void*)k_fstream<Tin, Tout, S1, S2>;
+    a.rank_lo = rank_lo;
+    a.rank_hi = rank_hi;
+    a.sys_scope = 0;
+    for (int r = 0; r < c->world; ++r) a.sys_scope |= (c->ipc || c->devices[r] != dev) ? 1 : 0;
+    const int rsb = (int)rstage_bytes(a.c1, a.world) + 16;
+    a.r_stages_f = a.stage_hint > 0 ? a.stage_hint : 2;
+    const int budget = std::max(a.r_stages_f * rsb, 64 * 1024);
+    a.q_stages_f = a.q_hint > 0 ? a.q_hint : std::max(2, std::min(6, budget / (kTileElems * 2 + 16)));
+    a.d_stages_f = a.d_hint > 0 ? a.d_hint : std::max(2, std::min(8, budget / ((int)dstage_bytes(a.c2) + 16)));
+    const int smem = std::max({a.r_stages_f * rsb, a.q_stages_f * (kTileElems * 2 + 16),
+                               a.d_stages_f * ((int)dstage_bytes(a.c2) + 16)});
+    FC_TRY(ensure_smem(kern, dev, smem));
+    const int64_t w = c->role_weights;
+    role_pattern((int)(w & 0xFF), (int)((w >> 8) & 0xFF), (int)((w >> 16) & 0xFF), a);
+    int occ = 0;
+    FC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kStreamThreads, smem));
+    if (a.cta_cap > 0) occ = std::min(occ, a.cta_cap);
+    if (occ < 1) return fail(FC_ERR_CUDA, "fused stream kernel does not fit on an SM");
+    int grid = occ * num_sms(dev);
+    grid = std::max(a.role_period, grid / a.role_period * a.role_period);
+    void* args[] = {&a};
+    FC_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kStreamThreads), args, smem, st));
+    ++g_launch_count;
+    return FC_OK;
+  }
+}
+
 template <typename Tin, typename Tout, int CW, class S1, class S2>
 fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, int64_t n, const fc_flash_cfg* cfg,
                        cudaStream_t* st, int only_rank /* -1: local world */) {
@@ -363,7 +427,9 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
       const int dev = c->devices[r];
       FC_CUDA_TRY(cudaSetDevice(dev));
       cudaStream_t s = st[r];
-      if (p.fast && c->fused != 0) {
+      if (use_stream && c->fused != 0) {
+        FC_TRY((launch_fstream<Tin, Tout, S1, S2>(c, a, r, r + 1, dev, s)));
+      } else if (p.fast && c->fused != 0) {
         FC_TRY((launch_fused<Tin, Tout, CW, S1, S2>(c, a, r, r + 1, dev, s)));
       } else if (p.fast) {
         a.rank_lo = r;
@@ -392,7 +458,20 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
       continue;
     }
     // ---------------- local world: this process drives every rank
-    if (p.fast && (c->fused == 1 || (c->fused == -1 && !single_dev))) {
+    // default (-1): phase-split when every rank shares one GPU (nothing crosses a link, and the
+    // per-tile flag chains of the fused kernel cost more than the two kernel boundaries); fused
+    // across GPUs so NVLink stores overlap the HBM streaming
+    if (use_stream && (c->fused == 1 || (c->fused == -1 && !single_dev))) {
+      if (single_dev) {
+        FC_CUDA_TRY(cudaSetDevice(c->devices[0]));
+        FC_TRY((launch_fstream<Tin, Tout, S1, S2>(c, a, 0, N, c->devices[0], st[0])));
+      } else {
+        for (int r = 0; r < N; ++r) {
+          FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+          FC_TRY((launch_fstream<Tin, Tout, S1, S2>(c, a, r, r + 1, c->devices[r], st[r])));
+        }
+      }
+    } else if (p.fast && (c->fused == 1 || (c->fused == -1 && !single_dev))) {
       if (single_dev) {
         FC_CUDA_TRY(cudaSetDevice(c->devices[0]));
         FC_TRY((launch_fused<Tin, Tout, CW, S1, S2>(c, a, 0, N, c->devices[0], st[0])));

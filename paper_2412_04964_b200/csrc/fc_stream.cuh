@@ -133,118 +133,6 @@ __device__ __forceinline__ void unrotate_input(PackedLane<Tin>& L, int rot) {
   }
 }
 
-// ------------------------------------------------------------------ item ranges
-
-// Each CTA walks a contiguous range of the flat item list (job-major,
-// tile-minor), so the (job, tile) pair advances by increment — no division
-// per item — and consecutive items of a CTA are consecutive tiles of one job.
-struct ItemRange {
-  int begin, end;  // flat items [begin, end)
-  int y, t;        // (job, tile) of `begin`
-};
-__device__ __forceinline__ ItemRange item_range(int items, int tiles) {
-  const int per = (items + (int)gridDim.x - 1) / (int)gridDim.x;
-  ItemRange r;
-  r.begin = min(items, (int)blockIdx.x * per);
-  r.end = min(items, r.begin + per);
-  r.y = r.begin / tiles;
-  r.t = r.begin - r.y * tiles;
-  return r;
-}
-__device__ __forceinline__ void item_next(int& y, int& t, int tiles) {
-  if (++t == tiles) {
-    t = 0;
-    ++y;
-  }
-}
-
-// ------------------------------------------------------------------ quantize stream
-
-// stage-1 scatter (mode 0: every (rank, peer) pair of [rank_lo, rank_hi)) or
-// codec quantize (mode 1)
-template <typename Tin, class S1>
-__global__ void __launch_bounds__(kStreamThreads) k_qstream(FlashArgs a) {
-  static_assert(sizeof(Tin) == 2, "16-bit inputs");
-  extern __shared__ __align__(16) uint8_t smem[];
-  constexpr uint32_t STAGE = kTileElems * 2;
-  const int S = a.stages;
-  const uint32_t sbase = smem_u32(smem);
-  const uint32_t full0 = sbase + S * STAGE, empty0 = full0 + 8 * S;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
-  const ItemRange R = item_range(njobs * a.tiles, a.tiles);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, kConsumerWarps);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == kConsumerWarps) {  // producer warp: one lane issues the bulk copies
-    if (lane == 0) {
-      int y = R.y, t = R.t, cy = -1, st = 0;
-      uint32_t ph = 0;
-      QJob<Tin> jb;
-      for (int i = R.begin; i < R.end; ++i) {
-        if (i - R.begin >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
-        if (y != cy) {
-          jb = qjob<Tin>(a, y);
-          cy = y;
-        }
-        const int64_t e0 = (int64_t)t * kTileElems;
-        const uint32_t bytes = (uint32_t)(tile_valid(a.sub_len, jb.limit, e0) * 2) & ~15u;
-        mbar_arrive_expect_tx(full0 + 8 * st, bytes);
-        if (bytes) bulk_g2s(sbase + st * STAGE, jb.src + e0, bytes, full0 + 8 * st);
-        item_next(y, t, a.tiles);
-        if (++st == S) {
-          st = 0;
-          ph ^= 1;
-        }
-      }
-    }
-    return;
-  }
-  const int rot = (lane >> 1) & 3;
-  uint32_t qoff[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) qoff[q] = threadIdx.x * 64 + 16 * ((q + rot) & 3);
-  int y = R.y, t = R.t, cy = -1, st = 0;
-  uint32_t ph = 0;
-  QJob<Tin> jb;
-  for (int i = R.begin; i < R.end; ++i) {
-    if (y != cy) {
-      jb = qjob<Tin>(a, y);
-      cy = y;
-    }
-    const int64_t p0 = (int64_t)t * kTileElems + threadIdx.x * kLaneElems;
-    const int nvalid = lane_valid(a.sub_len, p0);
-    const bool staged = nvalid == kLaneElems && p0 + kLaneElems <= jb.limit;
-    PackedLane<Tin> L;
-    mbar_wait(full0 + 8 * st, ph);
-    if (staged)
-      read_rotated(sbase + st * STAGE, qoff, L);
-    else
-      load_lane_src(jb.src, p0, jb.limit, nvalid, L);
-    LaneQuant<8> q;
-    const bool bad = quantize_lane<S1>(a.c1, L, nvalid, q);
-    // release the stage only after the shared loads were consumed: an LDS still
-    // in flight at the arrive could otherwise read the next tile's bulk copy
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * st);
-    if (staged) unrotate_codes<S1>(q.w, rot);
-    store_codes<S1>(a.c1, jb.dst, p0, nvalid, q, lane);
-    if (bad && jb.err) atomicOr(jb.err, jb.ecode);
-    item_next(y, t, a.tiles);
-    if (++st == S) {
-      st = 0;
-      ph ^= 1;
-    }
-  }
-}
-
-// ------------------------------------------------------------------ reduce stream
-
 // bytes of one peer's staged piece of a tile: codes, scales, zeros (16-B aligned parts)
 __host__ __device__ inline uint32_t peer_codes_bytes(const DevCodec& c) { return kTileElems * c.sb / 8; }
 __host__ __device__ inline uint32_t peer_scale_bytes(const DevCodec& c) { return ((kTileElems / c.g) * 2 + 15) & ~15u; }
@@ -292,20 +180,93 @@ __device__ __forceinline__ void read_peer(const DevCodec& c1, uint32_t src, uint
   C.mz = 8388608.0f + zf;
 }
 
-// owner j of [rank_lo, rank_hi): own segment QDQ + N-1 received pieces ->
-// fp32 sum (ascending source rank) -> stage-2 quantize -> every peer's
-// gather slot [j] + own output
-template <typename Tin, typename Tout, class S1, class S2>
-__global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
-  static_assert(sizeof(Tin) == 2, "16-bit inputs");
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int S = a.stages;
-  const uint32_t SBY = rstage_bytes(a.c1, a.world);
-  const uint32_t PC = peer_codes_bytes(a.c1), PM = peer_meta_bytes(a.c1), SCB = peer_scale_bytes(a.c1);
-  const uint32_t sbase = smem_u32(smem);
-  const uint32_t full0 = sbase + S * SBY, empty0 = full0 + 8 * S;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const ItemRange R = item_range((a.rank_hi - a.rank_lo) * a.tiles, a.tiles);
+// ------------------------------------------------------------------ item iterators
+
+// Phase-split kernels: each CTA walks a contiguous range of the job-major item
+// list, so (job y, tile t) advance by increment and consecutive items of a CTA
+// are consecutive tiles of one job.
+struct RangeIter {
+  int i, end, y, t, tiles;
+  __device__ __forceinline__ RangeIter(int items, int tiles_, int cta, int nctas) : tiles(tiles_) {
+    const int per = (items + nctas - 1) / nctas;
+    i = min(items, cta * per);
+    end = min(items, i + per);
+    y = i / tiles;
+    t = i - y * tiles;
+  }
+  __device__ __forceinline__ bool ok() const { return i < end; }
+  __device__ __forceinline__ void next() {
+    ++i;
+    if (++t == tiles) {
+      t = 0;
+      ++y;
+    }
+  }
+};
+
+// Fused kernel: tile-major items (t = i / P, y = i % P) dealt round-robin to the
+// CTAs of a role, so every role sweeps the tiles in step and a tile's
+// producers run ahead of its consumers.
+struct RoundIter {
+  int i, items, y, t, P, dy, dt, step;
+  __device__ __forceinline__ RoundIter(int items_, int P_, int first, int step_)
+      : i(first), items(items_), P(P_), step(step_) {
+    t = first / P;
+    y = first - t * P;
+    dt = step / P;
+    dy = step - dt * P;
+  }
+  __device__ __forceinline__ bool ok() const { return i < items; }
+  __device__ __forceinline__ void next() {
+    i += step;
+    t += dt;
+    y += dy;
+    if (y >= P) {
+      y -= P;
+      ++t;
+    }
+  }
+};
+
+// ------------------------------------------------------------------ cross-CTA / cross-GPU flags (fused)
+
+// lanes [0, n) of the calling warp each wait for flags[lane] to reach the
+// epoch; a wait past the timeout (or an error raised elsewhere) latches a
+// ProtocolError in the error word and gives up (results then are garbage,
+// the call reports the error). Returns false when aborted.
+__device__ __forceinline__ bool warp_wait_flags(const FlashArgs& a, int rank, const uint32_t* flag, int peer,
+                                                bool active, uint32_t phase) {
+  bool ok = true;
+  if (active) {
+    const uint64_t t0 = globaltimer();
+    volatile uint32_t* ew = errw(a, rank);
+    uint32_t spins = 0;
+    while ((int32_t)((a.sys_scope ? ld_acquire_sys(flag) : ld_acquire_gpu(flag)) - a.epoch) < 0) {
+      if ((*ew >> 28) == kErrTimeout) {
+        ok = false;
+        break;
+      }
+      if ((++spins & 63u) == 0 && globaltimer() - t0 > a.timeout_ns) {
+        atomicCAS(errw(a, rank), 0u, make_err(kErrTimeout, phase, peer, rank));
+        ok = false;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  // the data behind the flags is read by bulk copies (async proxy)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  return ok;
+}
+
+// consumer warps only (named barrier 1): every consumer thread's stores of this
+// item happen before thread 0's system-scope fence and flag stores
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
+
+// ------------------------------------------------------------------ ring setup
+
+__device__ __forceinline__ void ring_init(uint32_t full0, uint32_t empty0, int S) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full0 + 8 * s, 1);
@@ -314,14 +275,117 @@ __global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == kConsumerWarps) {
+}
+__device__ __forceinline__ void ring_next(int& st, uint32_t& ph, int S) {
+  if (++st == S) {
+    st = 0;
+    ph ^= 1;
+  }
+}
+
+// ------------------------------------------------------------------ quantize role
+
+// stage-1 scatter (mode 0: (rank, peer) job y of [rank_lo, rank_hi)) or codec
+// quantize (mode 1). FUSED: raise rflag[j][r][t] after each tile's stores.
+template <typename Tin, class S1, bool FUSED, class Iter>
+__device__ __forceinline__ void q_role(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
+  static_assert(sizeof(Tin) == 2, "16-bit inputs");
+  constexpr uint32_t STAGE = kTileElems * 2;
+  const uint32_t full0 = sbase + S * STAGE, empty0 = full0 + 8 * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ring_init(full0, empty0, S);
+  if (warp == kConsumerWarps) {  // producer warp: one lane issues the bulk copies
     if (lane == 0) {
-      int y = R.y, t = R.t, st = 0;
+      int st = 0, k = 0, cy = -1;
       uint32_t ph = 0;
-      for (int i = R.begin; i < R.end; ++i) {
-        if (i - R.begin >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
-        const int j = a.rank_lo + y;
-        const int64_t e0 = (int64_t)t * kTileElems;
+      QJob<Tin> jb;
+      for (Iter it = it0; it.ok(); it.next(), ++k) {
+        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        if (it.y != cy) {
+          jb = qjob<Tin>(a, it.y);
+          cy = it.y;
+        }
+        const int64_t e0 = (int64_t)it.t * kTileElems;
+        const uint32_t bytes = (uint32_t)(tile_valid(a.sub_len, jb.limit, e0) * 2) & ~15u;
+        mbar_arrive_expect_tx(full0 + 8 * st, bytes);
+        if (bytes) bulk_g2s(sbase + st * STAGE, jb.src + e0, bytes, full0 + 8 * st);
+        ring_next(st, ph, S);
+      }
+    }
+    return;
+  }
+  const int rot = (lane >> 1) & 3;
+  uint32_t qoff[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) qoff[q] = threadIdx.x * 64 + 16 * ((q + rot) & 3);
+  int st = 0, cy = -1;
+  uint32_t ph = 0;
+  QJob<Tin> jb;
+  for (Iter it = it0; it.ok(); it.next()) {
+    if (it.y != cy) {
+      jb = qjob<Tin>(a, it.y);
+      cy = it.y;
+    }
+    const int64_t p0 = (int64_t)it.t * kTileElems + threadIdx.x * kLaneElems;
+    const int nvalid = lane_valid(a.sub_len, p0);
+    const bool staged = nvalid == kLaneElems && p0 + kLaneElems <= jb.limit;
+    PackedLane<Tin> L;
+    mbar_wait(full0 + 8 * st, ph);
+    if (staged)
+      read_rotated(sbase + st * STAGE, qoff, L);
+    else
+      load_lane_src(jb.src, p0, jb.limit, nvalid, L);
+    LaneQuant<8> q;
+    const bool bad = quantize_lane<S1>(a.c1, L, nvalid, q);
+    // release the stage only after the shared loads were consumed: an LDS still
+    // in flight at the arrive could otherwise read the next tile's bulk copy
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);
+    if (staged) unrotate_codes<S1>(q.w, rot);
+    store_codes<S1>(a.c1, jb.dst, p0, nvalid, q, lane);
+    if (bad && jb.err) atomicOr(jb.err, jb.ecode);
+    if constexpr (FUSED) {
+      consumers_sync();
+      if (threadIdx.x == 0) {
+        int r, j;
+        pair_of(a, it.y, r, j);
+        if (a.sys_scope) {
+          __threadfence_system();
+          st_relaxed_sys(rflag(a, j, r) + it.t, a.epoch);
+        } else {
+          st_release_gpu(rflag(a, j, r) + it.t, a.epoch);  // bar.sync + release: cumulative over the CTA's stores
+        }
+      }
+    }
+    ring_next(st, ph, S);
+  }
+}
+
+// ------------------------------------------------------------------ reduce role
+
+// owner j = rank_lo + y: own segment QDQ + N-1 received pieces -> fp32 sum
+// (ascending source rank) -> stage-2 quantize -> every peer's gather slot [j]
+// + own output. FUSED: wait rflag[j][*][t] before the copies, raise
+// gflag[p][j][t] for every peer p after the stores.
+template <typename Tin, typename Tout, class S1, class S2, bool FUSED, class Iter>
+__device__ __forceinline__ void r_role(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
+  static_assert(sizeof(Tin) == 2, "16-bit inputs");
+  const uint32_t SBY = rstage_bytes(a.c1, a.world);
+  const uint32_t PC = peer_codes_bytes(a.c1), PM = peer_meta_bytes(a.c1), SCB = peer_scale_bytes(a.c1);
+  const uint32_t full0 = sbase + S * SBY, empty0 = full0 + 8 * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ring_init(full0, empty0, S);
+  if (warp == kConsumerWarps) {
+    int st = 0, k = 0;
+    uint32_t ph = 0;
+    for (Iter it = it0; it.ok(); it.next(), ++k) {
+      const int j = a.rank_lo + it.y;
+      if constexpr (FUSED) {  // lanes s != j wait for rank s's stage-1 piece of tile t
+        warp_wait_flags(a, j, rflag(a, j, lane) + it.t, lane, lane < a.world && lane != j, kPhReduce);
+      }
+      if (lane == 0) {
+        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        const int64_t e0 = (int64_t)it.t * kTileElems;
         const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
         const uint32_t own = (uint32_t)(tile_valid(a.sub_len, a.M - seg0, e0) * 2) & ~15u;
         const int64_t v = clamp0(min((int64_t)kTileElems, a.sub_len - e0));
@@ -341,12 +405,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
           if (zb) bulk_g2s(dst + PC + SCB, slot + a.c1.zeros_off + grp0, zb, bar);
           dst += PC + PM;
         }
-        item_next(y, t, a.tiles);
-        if (++st == S) {
-          st = 0;
-          ph ^= 1;
-        }
       }
+      __syncwarp();
+      ring_next(st, ph, S);
     }
     return;
   }
@@ -355,11 +416,11 @@ __global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) qoff[q] = threadIdx.x * 64 + 16 * ((q + rot) & 3);
   const uint32_t gl = (uint32_t)((threadIdx.x * kLaneElems) >> a.c1.gshift);
-  int y = R.y, t = R.t, st = 0;
+  int st = 0;
   uint32_t ph = 0;
-  for (int i = R.begin; i < R.end; ++i) {
-    const int j = a.rank_lo + y;
-    const int64_t p0 = (int64_t)t * kTileElems + threadIdx.x * kLaneElems;
+  for (Iter it = it0; it.ok(); it.next()) {
+    const int j = a.rank_lo + it.y;
+    const int64_t p0 = (int64_t)it.t * kTileElems + threadIdx.x * kLaneElems;
     const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
     const int nvalid = lane_valid(a.sub_len, p0);
     const bool staged = nvalid == kLaneElems && seg0 + p0 + kLaneElems <= a.M;
@@ -418,15 +479,25 @@ __global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
       store_chunk(reinterpret_cast<Tout*>(a.out[j]), seg0 + p0, a.M, nvalid, ov);
     }
     if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
-    item_next(y, t, a.tiles);
-    if (++st == S) {
-      st = 0;
-      ph ^= 1;
+    if constexpr (FUSED) {
+      consumers_sync();
+      if (threadIdx.x == 0) {
+        if (a.sys_scope) {
+          __threadfence_system();
+          for (int p = 0; p < a.world; ++p)
+            if (p != j) st_relaxed_sys(gflag(a, p, j) + it.t, a.epoch);
+        } else {
+          __threadfence();
+          for (int p = 0; p < a.world; ++p)
+            if (p != j) st_relaxed_sys(gflag(a, p, j) + it.t, a.epoch);
+        }
+      }
     }
+    ring_next(st, ph, S);
   }
 }
 
-// ------------------------------------------------------------------ dequantize stream
+// ------------------------------------------------------------------ dequantize role
 
 template <typename Tout>
 __device__ __forceinline__ void store8(Tout* p, const float v[8]) {
@@ -493,44 +564,38 @@ __host__ __device__ inline uint32_t dstage_bytes(const DevCodec& c) {
   return peer_codes_bytes(c) + peer_meta_bytes(c);
 }
 
-// all-gather decode (mode 0: rank r's gather slot [j] -> out[r][segment j]
-// for every pair of [rank_lo, rank_hi)) or codec dequantize (mode 1).
-// A producer warp bulk-copies each tile's codes/scales/zeros into an S-stage
-// ring; consumer thread t decodes 8-element blocks t + 256*b (b = 0..3) of
-// the tile: conflict-free shared loads and coalesced 16-B output stores.
-template <typename Tout, class S2>
-__global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+// all-gather decode (mode 0: rank r's gather slot [j] -> out[r][segment j],
+// job y = (r, j) of [rank_lo, rank_hi)) or codec dequantize (mode 1). A
+// producer warp bulk-copies each tile's codes/scales/zeros into the ring;
+// consumer thread t decodes 8-element blocks t + 256*b (b = 0..3) of the
+// tile: conflict-free shared loads and coalesced 16-B output stores.
+// FUSED: wait gflag[r][j][t] before the copies.
+template <typename Tout, class S2, bool FUSED, class Iter>
+__device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
   constexpr int kBlocks = kTileElems / 8 / kThreads;  // 4
   const DevCodec& c = a.c2;
-  const int S = a.stages;
   const uint32_t SBY = dstage_bytes(c), PC = peer_codes_bytes(c), SCB = peer_scale_bytes(c);
-  const uint32_t sbase = smem_u32(smem);
   const uint32_t full0 = sbase + S * SBY, empty0 = full0 + 8 * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
-  const ItemRange R = item_range(njobs * a.tiles, a.tiles);
   const int gs = c.gshift;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, kConsumerWarps);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
+  ring_init(full0, empty0, S);
   if (warp == kConsumerWarps) {
-    if (lane == 0) {
-      int y = R.y, t = R.t, cy = -1, st = 0;
-      uint32_t ph = 0;
-      DJob<Tout> d;
-      for (int i = R.begin; i < R.end; ++i) {
-        if (i - R.begin >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
-        if (y != cy) {
-          d = djob<Tout>(a, y);
-          cy = y;
+    int st = 0, k = 0, cy = -1;
+    uint32_t ph = 0;
+    DJob<Tout> d;
+    for (Iter it = it0; it.ok(); it.next(), ++k) {
+      if constexpr (FUSED) {
+        int r, j;
+        pair_of(a, it.y, r, j);
+        warp_wait_flags(a, r, gflag(a, r, j) + it.t, j, lane == 0, kPhGather);
+      }
+      if (lane == 0) {
+        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        if (it.y != cy) {
+          d = djob<Tout>(a, it.y);
+          cy = it.y;
         }
-        const int64_t e0 = (int64_t)t * kTileElems;
+        const int64_t e0 = (int64_t)it.t * kTileElems;
         const int64_t v = clamp0(min((int64_t)kTileElems, min(a.sub_len - e0, d.limit - e0)));
         const int64_t grp0 = e0 >> gs, ng = (v + c.g - 1) >> gs;
         const uint32_t cb = v > 0 ? up16(v * S2::SB / 8) : 0u, sb = v > 0 ? up16(ng * 2) : 0u;
@@ -540,12 +605,9 @@ __global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
         if (cb) bulk_g2s(dst, d.src + e0 * S2::SB / 8, cb, bar);
         if (sb) bulk_g2s(dst + PC, d.src + c.scales_off + grp0 * 2, sb, bar);
         if (zb) bulk_g2s(dst + PC + SCB, d.src + c.zeros_off + grp0, zb, bar);
-        item_next(y, t, a.tiles);
-        if (++st == S) {
-          st = 0;
-          ph ^= 1;
-        }
       }
+      __syncwarp();
+      ring_next(st, ph, S);
     }
     return;
   }
@@ -554,15 +616,15 @@ __global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
   const uint32_t code_off = threadIdx.x * S2::SB;                // bytes of 8 codes of SB bits
   const uint32_t grp_off = (uint32_t)(threadIdx.x * 8) >> gs;    // tile-local group of block 0
   const uint32_t grp_step = (uint32_t)(kThreads * 8) >> gs;      // groups per block step
-  int y = R.y, t = R.t, cy = -1, st = 0;
+  int st = 0, cy = -1;
   uint32_t ph = 0;
   DJob<Tout> d;
-  for (int i = R.begin; i < R.end; ++i) {
-    if (y != cy) {
-      d = djob<Tout>(a, y);
-      cy = y;
+  for (Iter it = it0; it.ok(); it.next()) {
+    if (it.y != cy) {
+      d = djob<Tout>(a, it.y);
+      cy = it.y;
     }
-    const int64_t e0 = (int64_t)t * kTileElems;
+    const int64_t e0 = (int64_t)it.t * kTileElems;
     const int64_t v = min(a.sub_len - e0, d.limit - e0);  // valid elements from e0
     const uint32_t tile = sbase + st * SBY;
     Tout* obase = d.out + e0 + threadIdx.x * 8;
@@ -600,7 +662,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
       }
       decode8<S2>(w, sc[b], mz[b], val[b]);
     }
-    // release the stage after the shared loads were consumed (see k_qstream)
+    // release the stage after the shared loads were consumed (see q_role)
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * st);
     if (v >= kTileElems) {  // whole tile: no per-block checks
@@ -620,12 +682,69 @@ __global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
         }
       }
     }
-    item_next(y, t, a.tiles);
-    if (++st == S) {
-      st = 0;
-      ph ^= 1;
-    }
+    ring_next(st, ph, S);
   }
+}
+
+// ------------------------------------------------------------------ phase-split kernels
+
+template <typename Tin, class S1>
+__global__ void __launch_bounds__(kStreamThreads) k_qstream(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
+  q_role<Tin, S1, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+}
+
+template <typename Tin, typename Tout, class S1, class S2>
+__global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  r_role<Tin, Tout, S1, S2, false>(a, smem_u32(smem), a.stages,
+                                   RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+}
+
+template <typename Tout, class S2>
+__global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
+  d_role<Tout, S2, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+}
+
+// ------------------------------------------------------------------ fused kernel
+
+// One cooperative launch: CTA roles interleaved by blockIdx with the pattern
+// a.role_pat (2 bits per slot, a.role_period slots: 0 scatter, 1 reduce, 2
+// gather). Each role walks its items tile-major and round-robin over the role's
+// CTAs, synchronised with the other roles (and, across GPUs, other ranks) only
+// through the per-tile epoch flags; all CTAs are resident, waits only target
+// producers that never wait on their consumers, so the schedule cannot deadlock.
+template <typename Tin, typename Tout, class S1, class S2>
+__global__ void __launch_bounds__(kStreamThreads, 2) k_fstream(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int per = a.role_period;
+  const int slot = (int)blockIdx.x % per, rep = (int)blockIdx.x / per;
+  int cnt[3] = {0, 0, 0}, idx = 0, role = 0;
+  for (int k = 0; k < per; ++k) {
+    const int rk = (a.role_pat >> (2 * k)) & 3;
+    if (k == slot) {
+      role = rk;
+      idx = cnt[rk];
+    }
+    ++cnt[rk];
+  }
+  const int reps = ((int)gridDim.x + per - 1) / per;
+  // CTAs of this role: cnt[role] per full period (the last partial period contributes its share)
+  int nrole = 0;
+  for (int k = 0; k < per; ++k)
+    if (((a.role_pat >> (2 * k)) & 3) == role) nrole += (reps - 1) + (k < (int)gridDim.x - (reps - 1) * per ? 1 : 0);
+  const int first = rep * cnt[role] + idx;
+  const int npairs = (a.rank_hi - a.rank_lo) * (a.world - 1), nown = a.rank_hi - a.rank_lo;
+  const uint32_t sb = smem_u32(smem);
+  if (role == 0)
+    q_role<Tin, S1, true>(a, sb, a.q_stages_f, RoundIter(npairs * a.tiles, npairs, first, nrole));
+  else if (role == 1)
+    r_role<Tin, Tout, S1, S2, true>(a, sb, a.r_stages_f, RoundIter(nown * a.tiles, nown, first, nrole));
+  else
+    d_role<Tout, S2, true>(a, sb, a.d_stages_f, RoundIter(npairs * a.tiles, npairs, first, nrole));
 }
 
 }  // namespace fc

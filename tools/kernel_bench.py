@@ -126,6 +126,28 @@ def tune_sweep():
     comm.close()
 
 
+def fused_tune():
+    """Role weights (scatter:reduce:gather CTAs) of the fused streaming kernel at C2."""
+    M, tp, e = 8 * 1024 * 8192, 8, 2
+    cfg = fc.FlashConfig.from_bits(4)
+    seg = M // tp
+    comm = FlashComm.local([0] * tp, slot_bytes_for(seg, cfg.stage1_codec, cfg.stage2_codec))
+    comm.set_option(_lib.OPT_FUSED, 1)
+    ins = [torch.randn(M, device="cuda").to(torch.bfloat16) for _ in range(tp)]
+    outs = [torch.empty_like(t) for t in ins]
+    w = cfg.stage1_codec.wire_byte_len(seg)
+    alg = tp * (2 * e * M + 2 * (tp - 1) * 2 * w)
+    for q, r, d in ((3, 2, 3), (4, 3, 4), (5, 3, 5), (6, 4, 6), (5, 4, 5), (4, 2, 4), (6, 3, 5), (5, 3, 6), (3, 3, 3), (7, 4, 5)):
+        comm.set_option(_lib.OPT_ROLE_WEIGHTS, q | (r << 8) | (d << 16))
+        for cap in (0, 1):
+            comm.set_option(_lib.OPT_CTAS_PER_SM, cap)
+            t = timeit(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), iters=5, warm=2)
+            comm.check()
+            print(json.dumps({"kernel": "flash_fused_tune", "w": [q, r, d], "cta_cap": cap, "ms": t,
+                              "frac": alg / t / 1e6 / PEAK}), flush=True)
+    comm.close()
+
+
 if __name__ == "__main__":
     what = [a for a in sys.argv[1:] if not a.startswith("--")] or ["codec", "flash"]
     quick = "--quick" in sys.argv
@@ -135,3 +157,5 @@ if __name__ == "__main__":
         flash_sweep(quick)
     if "tune" in what:
         tune_sweep()
+    if "fusedtune" in what:
+        fused_tune()
