@@ -393,6 +393,7 @@ fc_status run_typed_cw(fc_comm* c, const void* const* ins, void* const* outs, in
   a.q_hint = (int)c->q_stages;
   a.d_hint = (int)c->d_stages;
   a.cta_cap = (int)c->ctas_per_sm;
+  a.dbg = (int)c->stream_mask;
   a.c1 = dev_codec(cfg->stage1, p.L1);
   a.c2 = dev_codec(cfg->stage2, p.L2);
   for (int r = 0; r < N; ++r) {

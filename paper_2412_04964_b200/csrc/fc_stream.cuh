@@ -390,10 +390,15 @@ __device__ __forceinline__ void r_role(const FlashArgs& a, uint32_t sbase, int S
         const uint32_t own = (uint32_t)(tile_valid(a.sub_len, a.M - seg0, e0) * 2) & ~15u;
         const int64_t v = clamp0(min((int64_t)kTileElems, a.sub_len - e0));
         const int64_t grp0 = e0 >> a.c1.gshift, ng = (v + a.c1.g - 1) >> a.c1.gshift;
-        const uint32_t cb = v > 0 ? up16(v * a.c1.sb / 8) : 0u, sb = v > 0 ? up16(ng * 2) : 0u;
-        const uint32_t zb = (v > 0 && !a.c1.sym) ? up16(ng) : 0u;
+        const uint32_t cb = v > 0 ? up16(v * a.c1.sb / 8) : 0u;
+        uint32_t sb = v > 0 ? up16(ng * 2) : 0u;
+        uint32_t zb = (v > 0 && !a.c1.sym) ? up16(ng) : 0u;
         const uint32_t st_base = sbase + st * SBY;
         const uint32_t bar = full0 + 8 * st;
+        if (a.dbg & 8) {  // timing experiment only: no metadata copies (wrong results)
+          sb = 0;
+          zb = 0;
+        }
         mbar_arrive_expect_tx(bar, own + (uint32_t)(a.world - 1) * (cb + sb + zb));
         if (own) bulk_g2s(st_base, reinterpret_cast<const Tin*>(a.in[j]) + seg0 + e0, own, bar);
         uint32_t dst = st_base + kTileElems * 2;
