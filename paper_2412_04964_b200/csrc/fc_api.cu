@@ -13,9 +13,19 @@
 
 #include "fc_comm.h"
 #include "fc_flash.cuh"
-#include "fc_run.cuh"
 
 namespace fc {
+
+// the flash all-reduce instantiations live in the generated fc_run_*.cu units
+#define FC_EXTERN_RUN(TI, TO)                                                                                    \
+  extern template fc_status run_typed<TI, TO>(fc_comm*, const void* const*, void* const*, int64_t, const fc_flash_cfg*, \
+                                               cudaStream_t*, int);
+FC_EXTERN_RUN(float, float)
+FC_EXTERN_RUN(__half, float)
+FC_EXTERN_RUN(__half, __half)
+FC_EXTERN_RUN(__nv_bfloat16, float)
+FC_EXTERN_RUN(__nv_bfloat16, __nv_bfloat16)
+#undef FC_EXTERN_RUN
 
 static thread_local std::string g_err;
 thread_local int64_t g_launch_count = 0;

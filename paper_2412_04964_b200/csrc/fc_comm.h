@@ -43,6 +43,10 @@ struct fc_comm {
 };
 
 namespace fc {
+inline uint8_t* h_recv_slot(const fc_comm* c, int owner, int src) { return c->blk[owner] + (int64_t)src * c->slot_bytes; }
+inline uint8_t* h_gath_slot(const fc_comm* c, int owner, int src) {
+  return c->blk[owner] + (int64_t)(c->world + src) * c->slot_bytes;
+}
 // run_typed<Tin, Tout>: instantiated in fc_run_{f32,f16,bf16}.cu
 template <typename Tin, typename Tout>
 fc_status run_typed(fc_comm* c, const void* const* ins, void* const* outs, int64_t n, const fc_flash_cfg* cfg,

@@ -70,18 +70,24 @@ __device__ __forceinline__ uint64_t f2_splat(float a) { return f2_pack(a, a); }
 // Compile-time codec scheme. GenSpec = the generic runtime-flag lane codec.
 struct GenSpec {
   static constexpr bool kFast = false;
+  static constexpr bool kLegacy = true;  // the cp.async-staged kernels are compiled for this scheme
   static constexpr int SB = 0;
   static constexpr bool SYM = false, CEIL = false;
 };
 template <int SB_, bool SYM_, bool CEIL_>
 struct IntSpec {
   static constexpr bool kFast = true;
+  static constexpr bool kLegacy = !SYM_ && !CEIL_;  // staged kernels only for the asym-nearest presets
   static constexpr int SB = SB_;  // storage bits: 4 (bits 2..4) or 8 (bits 5..8)
   static constexpr bool SYM = SYM_;
   static constexpr bool CEIL = CEIL_;
 };
 using SpecA4 = IntSpec<4, false, false>;  // INT4 asym nearest (FlashConfig.from_bits(4))
 using SpecA8 = IntSpec<8, false, false>;  // INT8 asym nearest (from_bits(8), INT6 stage 2)
+using SpecS4 = IntSpec<4, true, false>;   // symmetric, bits 2..4
+using SpecS8 = IntSpec<8, true, false>;   // symmetric, bits 5..8
+using SpecC4 = IntSpec<4, false, true>;   // asym, ceil rounding (codec.py:288-289)
+using SpecC8 = IntSpec<8, false, true>;
 
 // ------------------------------------------------------------------ element access
 

@@ -245,3 +245,34 @@ def test_stream_kernels_match_staged_tp8(bits):
                     assert torch.equal(outs[r].view(torch.int32), ref[r].view(torch.int32)), (mask, r)
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("mode", ["fused", "split"])
+@pytest.mark.parametrize("bits,g,sym,rnd", [(4, 128, True, "nearest-even"), (8, 64, True, "nearest-even"),
+                                            (4, 256, False, "ceil"), (8, 32, False, "ceil"),
+                                            (3, 128, False, "nearest-even"), (6, 128, True, "nearest-even")])
+def test_compile_time_schemes_vs_oracle(bits, g, sym, rnd, mode):
+    """Symmetric / ceil / odd-bit schemes on the compile-time (streaming) kernels,
+    bit-exact against the oracle: outputs and both stages' wire messages."""
+    n, m = 4, 4 * 8192 * 5 + 4 * 24
+    rng = np.random.default_rng(bits * 31 + g)
+    xs = [(rng.standard_normal(m) * 3).astype(np.float32) for _ in range(n)]
+    for x in xs:
+        x[::301] *= 25
+    xs = [orc.round_to_bf16(x) for x in xs]  # the GPU sees exactly these bf16 values
+    codec = fc.CodecConfig(bits=bits, group_size=g, symmetric=sym, rounding=rnd)
+    cfg = fc.FlashConfig.uniform(codec)
+    comm = _comm(n, -(-m // n), cfg, mode)
+    ts = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in xs]
+    run = fc.flash_all_reduce(ts, cfg, comm=comm, out_dtype=torch.float32)
+    oc = orc.Codec(bits=bits, group_size=g, symmetric=sym, rounding=rnd)
+    res = orc.flash_all_reduce(xs, oc, oc)
+    for o in run.outputs:
+        assert np.array_equal(_bits(o.cpu().numpy()), _bits(res.outputs[0]))
+    for j in range(n):
+        p = (j + 1) % n
+        assert comm.slot(p, 2, j, codec).to_bytes() == res.stage2[j].wire_bytes(), f"stage-2 {j}"
+        s = (j + 1) % n
+        if mode == "split":
+            assert comm.slot(j, 1, s, codec).to_bytes() == res.stage1[j][s].wire_bytes(), f"stage-1 {j}<-{s}"
+    comm.close()
