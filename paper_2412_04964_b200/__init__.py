@@ -27,6 +27,7 @@ from .collectives import (
 )
 from .comm import FabricTopology, FlashComm, TrafficLedger, flash_ledger
 from .errors import ConfigError, CudaError, DomainError, IntegrityError, ProtocolError, QCollectivesError
+from . import tp  # noqa: F401  (registers torch.ops.flashcomm.all_reduce_)
 
 __version__ = "0.1.0"
 

@@ -28,7 +28,8 @@ struct FlashArgs {
   int ctas_per_rank;        // fused kernel
   int lag;                  // fused schedule lag (steps)
   int tiles;                // ceil(sub_len / kTileElems)
-  uint32_t epoch;
+  uint32_t epoch;           // host epoch of this round (used when epoch_dev is null)
+  const uint32_t* epoch_dev;  // device epoch counter of the launching rank (CUDA-graph safe), bumped per round
   int64_t M;                // elements per rank (unpadded)
   int64_t seg;              // ceil(M / world)
   int64_t sub_off, sub_len; // this round's sub-range of every segment
@@ -78,6 +79,15 @@ __device__ __forceinline__ uint32_t* errw(const FlashArgs& a, int owner) {
 __device__ __forceinline__ uint32_t* barflag(const FlashArgs& a, int owner, int phase, int src) {
   return errw(a, owner) + 16 + phase * kMaxRanks + src;
 }
+
+// epoch of this round: read from the device counter (bumped by k_epoch_bump
+// earlier on the same stream, so every CTA of the launch reads the same value
+// and a replayed CUDA graph advances it) or the host value
+__device__ __forceinline__ uint32_t flag_epoch(const FlashArgs& a) {
+  return a.epoch_dev ? *reinterpret_cast<const volatile uint32_t*>(a.epoch_dev) : a.epoch;
+}
+
+static __global__ void k_epoch_bump(uint32_t* e) { *e += 1u; }
 
 enum Phase : uint32_t { kPhScatter = 1, kPhReduce = 2, kPhGather = 3, kPhBarrier = 4 };
 
@@ -159,10 +169,11 @@ __device__ __forceinline__ bool wait_flags(const FlashArgs& a, int rank, uint32_
                                            int nflags, uint32_t phase, int* s_abort) {
   if ((int)threadIdx.x < nflags) {
     const uint32_t* f = flags[threadIdx.x];
+    const uint32_t ep = flag_epoch(a);
     const uint64_t t0 = globaltimer();
     volatile uint32_t* ew = errw(a, rank);
     uint32_t spins = 0;
-    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+    while ((int32_t)(ld_acquire_sys(f) - ep) < 0) {
       if ((*ew >> 28) == kErrTimeout) {  // another CTA of this rank gave up
         *s_abort = 1;
         break;
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
       const int j = (rank + 1 + slot) % a.world;
       do_scatter<Tin, CW, S1>(a, rank, j, (int)t);
       if (threadIdx.x == 0) s_flags[0] = rflag(a, j, rank) + t;
-      raise_flags(s_flags, 1, a.epoch);
+      raise_flags(s_flags, 1, flag_epoch(a));
     } else if (slot == P) {
       const int64_t t = k - a.lag;
       if (t < 0 || t >= a.tiles) continue;
@@ -232,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_flash_fused(FlashArgs a) {
       do_reduce<Tin, Tout, CW, S1, S2>(a, rank, (int)t);
       __syncthreads();
       if (threadIdx.x < P) s_flags[threadIdx.x] = gflag(a, (rank + 1 + threadIdx.x) % a.world, rank) + t;
-      raise_flags(s_flags, P, a.epoch);
+      raise_flags(s_flags, P, flag_epoch(a));
     } else {
       const int64_t t = k - 2 * a.lag;
       if (t < 0 || t >= a.tiles) continue;
@@ -453,12 +464,13 @@ static __global__ void k_barrier(FlashArgs a, int rank, int phase) {
   const int p = threadIdx.x;
   __threadfence_system();
   __syncwarp();
-  if (p < a.world && p != rank) st_relaxed_sys(barflag(a, p, phase, rank), a.epoch);
+  const uint32_t ep = flag_epoch(a);
+  if (p < a.world && p != rank) st_relaxed_sys(barflag(a, p, phase, rank), ep);
   if (p < a.world && p != rank) {
     const uint32_t* f = barflag(a, rank, phase, p);
     const uint64_t t0 = globaltimer();
     volatile uint32_t* ew = errw(a, rank);
-    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0) {
+    while ((int32_t)(ld_acquire_sys(f) - ep) < 0) {
       if ((*ew >> 28) == kErrTimeout) break;
       if (globaltimer() - t0 > a.timeout_ns) {
         atomicCAS(errw(a, rank), 0u, make_err(kErrTimeout, kPhBarrier, p, rank));

@@ -241,7 +241,8 @@ __device__ __forceinline__ bool warp_wait_flags(const FlashArgs& a, int rank, co
     const uint64_t t0 = globaltimer();
     volatile uint32_t* ew = errw(a, rank);
     uint32_t spins = 0;
-    while ((int32_t)((a.sys_scope ? ld_acquire_sys(flag) : ld_acquire_gpu(flag)) - a.epoch) < 0) {
+    const uint32_t ep = flag_epoch(a);
+    while ((int32_t)((a.sys_scope ? ld_acquire_sys(flag) : ld_acquire_gpu(flag)) - ep) < 0) {
       if ((*ew >> 28) == kErrTimeout) {
         ok = false;
         break;
@@ -351,9 +352,9 @@ __device__ __forceinline__ void q_role(const FlashArgs& a, uint32_t sbase, int S
         pair_of(a, it.y, r, j);
         if (a.sys_scope) {
           __threadfence_system();
-          st_relaxed_sys(rflag(a, j, r) + it.t, a.epoch);
+          st_relaxed_sys(rflag(a, j, r) + it.t, flag_epoch(a));
         } else {
-          st_release_gpu(rflag(a, j, r) + it.t, a.epoch);  // bar.sync + release: cumulative over the CTA's stores
+          st_release_gpu(rflag(a, j, r) + it.t, flag_epoch(a));  // bar.sync + release: cumulative over the CTA's stores
         }
       }
     }
@@ -490,11 +491,11 @@ __device__ __forceinline__ void r_role(const FlashArgs& a, uint32_t sbase, int S
         if (a.sys_scope) {
           __threadfence_system();
           for (int p = 0; p < a.world; ++p)
-            if (p != j) st_relaxed_sys(gflag(a, p, j) + it.t, a.epoch);
+            if (p != j) st_relaxed_sys(gflag(a, p, j) + it.t, flag_epoch(a));
         } else {
           __threadfence();
           for (int p = 0; p < a.world; ++p)
-            if (p != j) st_relaxed_sys(gflag(a, p, j) + it.t, a.epoch);
+            if (p != j) st_relaxed_sys(gflag(a, p, j) + it.t, flag_epoch(a));
         }
       }
     }
