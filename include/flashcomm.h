@@ -45,11 +45,15 @@ typedef enum {
 } fc_status;
 
 typedef enum { FC_DTYPE_F32 = 0, FC_DTYPE_F16 = 1, FC_DTYPE_BF16 = 2 } fc_dtype;
-typedef enum { FC_KIND_INT = 0, FC_KIND_FP16 = 1 } fc_codec_kind;
+typedef enum { FC_KIND_INT = 0, FC_KIND_FP16 = 1, FC_KIND_MINIFLOAT = 2 } fc_codec_kind;
+/* minifloat formats (minifloat.py:40-45), in fc_codec.reserved for FC_KIND_MINIFLOAT */
+typedef enum { FC_FMT_E4M3 = 0, FC_FMT_E5M2 = 1, FC_FMT_E2M1 = 2 } fc_minifloat_format;
 typedef enum { FC_ROUND_NEAREST_EVEN = 0, FC_ROUND_CEIL = 1 } fc_rounding;
 
 /* CodecConfig (codec.py:45-73): integer codes (bits 2..8, group-wise
- * asym/sym, nearest-even/ceil) or the fp16 passthrough (codec.py:162). */
+ * asym/sym, nearest-even/ceil), group-scaled minifloat codes (e4m3 / e5m2 /
+ * e2m1: kind FC_KIND_MINIFLOAT, reserved = fc_minifloat_format, bits = code
+ * bits; codec.py:332-351) or the fp16 passthrough (codec.py:162). */
 typedef struct {
   int32_t kind;      /* fc_codec_kind */
   int32_t bits;      /* 2..8 for FC_KIND_INT */
@@ -104,6 +108,16 @@ FC_API fc_status fc_dequantize(const void* src, int64_t n, const fc_codec* codec
                         void* stream);
 /* Synchronizes `stream` and maps a device error word to a status. */
 FC_API fc_status fc_error_word_check(const uint32_t* err_word, void* stream);
+
+/* Blocked Hadamard rotation (rotation.py:61-83): per block of `dim` (power of
+ * two <= 8192) elements of the zero-padded length-n_padded vector x (n valid
+ * elements), forward H(D x) or inverse D(H x), scaled by 1/sqrt(dim)
+ * (normalize) or, for the inverse without normalize, 1/dim; float64
+ * arithmetic, one rounding to out_dtype; the first n_out elements are
+ * written. signs: NULL or `dim` device floats of +-1 (the seeded diagonal). */
+FC_API fc_status fc_hadamard(const void* x, int32_t in_dtype, int64_t n, int64_t n_padded, int32_t dim,
+                             int32_t normalize, const float* signs, int32_t inverse, void* out, int32_t out_dtype,
+                             int64_t n_out, void* stream);
 
 /* ---- communicator: replaces the simulated fabric (fabric.py:111-246) ----
  * Every rank owns one device block: N stage-1 receive slots, N stage-2

@@ -39,12 +39,128 @@ DEFAULT_CHUNK_ELEMS = 64 * 1024  # collectives.py:32
 
 
 # --------------------------------------------------------------------------
+# minifloat formats (restated from minifloat.py:22-124): sign / exponent /
+# mantissa with IEEE-style subnormals, round-to-nearest-even, saturating at
+# the largest finite magnitude (no inf/NaN patterns are produced)
+
+
+@dataclass(frozen=True)
+class MiniFloat:
+    name: str
+    exp_bits: int
+    mantissa_bits: int
+    bias: int
+    max_finite: float
+
+    @property
+    def code_bits(self) -> int:
+        return 1 + self.exp_bits + self.mantissa_bits
+
+    @property
+    def min_normal(self) -> float:
+        return 2.0 ** (1 - self.bias)
+
+    @property
+    def sub_quantum(self) -> float:
+        return 2.0 ** (1 - self.bias - self.mantissa_bits)
+
+
+MINIFLOATS = {f.name: f for f in (MiniFloat("e4m3", 4, 3, 7, 448.0), MiniFloat("e5m2", 5, 2, 15, 57344.0),
+                                  MiniFloat("e2m1", 2, 1, 1, 6.0))}
+
+
+def mf_round(x: np.ndarray, f: MiniFloat) -> np.ndarray:
+    """minifloat.py:58-76: nearest grid value (float64), ties to even, saturating."""
+    x = np.asarray(x, np.float64)
+    a = np.abs(x)
+    _, e2 = np.frexp(a)
+    quantum = np.where(a < f.min_normal, f.sub_quantum, np.exp2(e2 - 1 - f.mantissa_bits))
+    r = np.minimum(np.round(a / quantum) * quantum, f.max_finite)
+    return np.where(x < 0, -r, r)
+
+
+def mf_encode(v: np.ndarray, f: MiniFloat) -> np.ndarray:
+    """minifloat.py:79-100: grid values -> uint8 bit patterns."""
+    v = np.asarray(v, np.float64)
+    sign = (v < 0).astype(np.int64)
+    a = np.abs(v)
+    sub = a < f.min_normal
+    _, e2 = np.frexp(a)
+    e = e2 - 1
+    expc = np.where(sub, 0, e + f.bias).astype(np.int64)
+    mant = np.where(sub, a / f.sub_quantum, (a * np.exp2(-e) - 1.0) * (1 << f.mantissa_bits))
+    code = (sign << (f.exp_bits + f.mantissa_bits)) | (expc << f.mantissa_bits) | np.round(mant).astype(np.int64)
+    return code.astype(np.uint8)
+
+
+def mf_table(f: MiniFloat) -> np.ndarray:
+    """minifloat.py:103-118: float32 value of every code pattern."""
+    out = np.empty(1 << f.code_bits, np.float32)
+    for code in range(out.size):
+        sgn = -1.0 if code >> (f.exp_bits + f.mantissa_bits) else 1.0
+        ec = (code >> f.mantissa_bits) & ((1 << f.exp_bits) - 1)
+        mc = code & ((1 << f.mantissa_bits) - 1)
+        mag = mc * f.sub_quantum if ec == 0 else (1 + mc / (1 << f.mantissa_bits)) * 2.0 ** (ec - f.bias)
+        out[code] = np.float32(sgn * mag)
+    return out
+
+
+# --------------------------------------------------------------------------
+# Hadamard rotation (restated from rotation.py:21-83)
+
+
+@dataclass(frozen=True)
+class Hadamard:
+    dimension: int
+    normalize: bool = True
+    sign_seed: Optional[int] = None
+
+    def signs(self) -> Optional[np.ndarray]:
+        if self.sign_seed is None:
+            return None
+        return np.random.default_rng(self.sign_seed).choice(np.array([-1.0, 1.0]), size=self.dimension)
+
+
+def _fwht(blocks: np.ndarray) -> np.ndarray:
+    rows, dim = blocks.shape
+    y, h = blocks, 1
+    while h < dim:
+        y = y.reshape(rows, dim // (2 * h), 2, h)
+        y = np.stack([y[:, :, 0, :] + y[:, :, 1, :], y[:, :, 0, :] - y[:, :, 1, :]], axis=2).reshape(rows, dim)
+        h *= 2
+    return y
+
+
+def hadamard_apply(x: np.ndarray, hb: Hadamard) -> np.ndarray:
+    """rotation.py:61-71: H(D x) per block of `dimension`, float64, one cast to float32."""
+    b = np.asarray(x, np.float64).ravel().reshape(-1, hb.dimension).copy()
+    sg = hb.signs()
+    if sg is not None:
+        b *= sg
+    y = _fwht(b)
+    if hb.normalize:
+        y = y / np.sqrt(hb.dimension)
+    return y.ravel().astype(np.float32)
+
+
+def hadamard_inverse(x: np.ndarray, hb: Hadamard) -> np.ndarray:
+    """rotation.py:74-83: D(H x) / sqrt(dim) (normalized) or / dim."""
+    y = _fwht(np.asarray(x, np.float64).ravel().reshape(-1, hb.dimension).copy())
+    y = y / np.sqrt(hb.dimension) if hb.normalize else y / hb.dimension
+    sg = hb.signs()
+    if sg is not None:
+        y *= sg
+    return y.ravel().astype(np.float32)
+
+
+# --------------------------------------------------------------------------
 # codec descriptor (mirror of codec.py:45-133, restated)
 
 
 @dataclass(frozen=True)
 class Codec:
-    """kind: 'int' (bits 2..8) or 'fp16' (passthrough)."""
+    """kind: 'int' (bits 2..8), 'fp16' (passthrough) or a minifloat format
+    'e4m3' / 'e5m2' / 'e2m1' (group-scaled, codec.py:332-351)."""
 
     kind: str = "int"
     bits: int = 4
@@ -57,13 +173,15 @@ class Codec:
     def storage_bits(self) -> int:  # codec.py:98-103
         if self.kind == "fp16":
             return 16
+        if self.kind in MINIFLOATS:
+            return 4 if MINIFLOATS[self.kind].code_bits <= 4 else 8
         return 4 if self.bits <= 4 else 8
 
     @property
     def meta_bytes(self) -> int:  # codec.py:105-112
         if self.kind == "fp16":
             return 0
-        return 2 if self.symmetric else 3
+        return 2 if (self.symmetric or self.kind != "int") else 3
 
     def groups(self, n: int) -> int:  # codec.py:123-126
         return 0 if self.kind == "fp16" else -(-n // self.group_size)
@@ -170,6 +288,12 @@ def quantize(x, codec: Codec) -> QSeg:
     n = a.size
     if codec.kind == "fp16":
         return QSeg(a.astype(np.float16).view(np.uint8).copy(), np.empty(0, np.float16), None, n, codec)
+    if codec.kind in MINIFLOATS:  # codec.py:332-351: absmax / max_finite scale, grid rounding, saturating
+        f = MINIFLOATS[codec.kind]
+        amax = np.maximum.reduceat(np.abs(a), _group_starts(n, codec.group_size))
+        s16 = snap_scale_f16(amax / f.max_finite, codec.scale_floor)
+        se = _expand(s16.astype(np.float64), n, codec.group_size)
+        return QSeg(mf_encode(mf_round(a / se, f), f), s16, None, n, codec)
     g, b = codec.group_size, codec.bits
     st = _group_starts(n, g)
     if codec.symmetric:
@@ -196,6 +320,8 @@ def dequantize(q: QSeg) -> np.ndarray:
         return q.codes.view(np.float16).astype(np.float32)
     n, g = q.n, c.group_size
     se = _expand(q.scales.astype(np.float64), n, g)
+    if c.kind in MINIFLOATS:  # codec.py:376-379
+        return (mf_table(MINIFLOATS[c.kind])[q.codes].astype(np.float64) * se).astype(np.float32)
     v = q.codes.astype(np.int64)
     if c.symmetric:
         v = v - ((v >> (c.bits - 1)) & 1) * (1 << c.bits)
@@ -254,8 +380,10 @@ class FlashResult:
 
 
 def flash_all_reduce(tensors: Sequence[np.ndarray], stage1: Codec, stage2: Codec,
-                     chunk: Optional[int] = None) -> FlashResult:
-    """Segment restatement of flash_all_reduce (collectives.py:321-402)."""
+                     chunk: Optional[int] = None, rotation: Optional[Hadamard] = None) -> FlashResult:
+    """Segment restatement of flash_all_reduce (collectives.py:321-402); with
+    `rotation` the padded rank tensors are Hadamard-rotated before and the
+    outputs rotated back after (collectives.py:350-351,390-391)."""
     flats = [np.asarray(t, np.float32).ravel() for t in tensors]
     n = len(flats)
     shape = np.asarray(tensors[0]).shape
@@ -264,11 +392,16 @@ def flash_all_reduce(tensors: Sequence[np.ndarray], stage1: Codec, stage2: Codec
         return FlashResult([flats[0].reshape(shape).copy()], [], [], [], m, 0)
     piece = resolve_chunk(n, stage1, stage2, chunk) // n
     padded = [_padded(f, n)[0] for f in flats]
+    if rotation is not None:
+        padded = [hadamard_apply(p, rotation) for p in padded]
     seg = padded[0].size // n
     st1 = [[quantize(padded[s][j * seg:(j + 1) * seg], stage1) for s in range(n)] for j in range(n)]
     reduced = [sequential_sum([dequantize(q) for q in st1[j]]) for j in range(n)]
     st2 = [quantize(r, stage2) for r in reduced]
-    out = np.concatenate([dequantize(q) for q in st2])[:m].reshape(shape)
+    out = np.concatenate([dequantize(q) for q in st2])
+    if rotation is not None:
+        out = hadamard_inverse(out, rotation)
+    out = out[:m].reshape(shape)
     # wire accounting (costmodel.py:122-128 == fabric ledger of rank 0)
     wire = 0
     off = 0

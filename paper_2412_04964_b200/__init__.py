@@ -27,6 +27,7 @@ from .collectives import (
 )
 from .comm import FabricTopology, FlashComm, TrafficLedger, flash_ledger
 from .errors import ConfigError, CudaError, DomainError, IntegrityError, ProtocolError, QCollectivesError
+from .rotation import HadamardBlock, hadamard_apply, hadamard_inverse
 from . import tp  # noqa: F401  (registers torch.ops.flashcomm.all_reduce_)
 
 __version__ = "0.1.0"
@@ -38,6 +39,7 @@ __all__ = [
     "CudaError",
     "DomainError",
     "FabricTopology",
+    "HadamardBlock",
     "FlashComm",
     "FlashConfig",
     "IntegrityError",
@@ -51,6 +53,8 @@ __all__ = [
     "dequantize",
     "flash_all_reduce",
     "flash_ledger",
+    "hadamard_apply",
+    "hadamard_inverse",
     "int6_flash_pair",
     "mse",
     "quantize",

@@ -44,8 +44,8 @@ def fc_dtype(dt: torch.dtype) -> int:
 @dataclass(frozen=True)
 class CodecConfig:
     """One quantization scheme (codec.py:45-73): exactly one of `bits`
-    (2..8 integer codes) or `number_format` (fp16 passthrough; the minifloat
-    formats are accepted by the config and rejected by the GPU path)."""
+    (2..8 integer codes) or `number_format` (e4m3 / e5m2 / e2m1 group-scaled
+    minifloats, codec.py:332-351, or the fp16 passthrough)."""
 
     bits: Optional[int] = None
     number_format: Optional[str] = None
@@ -128,7 +128,8 @@ class CodecConfig:
     # ---- C ABI view
     def to_fc(self) -> _lib.fc_codec:
         if self.is_minifloat:
-            raise ConfigError(f"{self.number_format} codecs are not implemented on the B200 path yet")
+            return _lib.fc_codec(_lib.KIND_MINIFLOAT, self.code_bits, int(self.group_size), 0, 0,
+                                 _lib.MINIFLOAT_FORMAT_IDS[self.number_format], float(self.scale_floor))
         if self.is_passthrough:
             return _lib.fc_codec(_lib.KIND_FP16, 16, 1, 0, 0, 0, self.scale_floor)
         return _lib.fc_codec(_lib.KIND_INT, int(self.bits), int(self.group_size), int(bool(self.symmetric)),
@@ -248,6 +249,8 @@ class QuantizedTensor:
         s = self.scales.float()
         if not bool(torch.isfinite(s).all()) or bool((s <= 0).any()):
             raise IntegrityError("scales must be finite and positive")
+        if not cfg.is_int:
+            return
         if cfg.storage_bits == 4 and cfg.bits < 4 and self.element_count:
             lo = self.codes & 0x0F
             hi = self.codes >> 4

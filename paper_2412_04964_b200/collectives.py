@@ -157,8 +157,6 @@ def flash_all_reduce(tensors: Sequence, cfg: FlashConfig, topology: Optional[Fab
     raises like the reference: DomainError for NaN/inf input, ProtocolError
     when a rank never arrives within `timeout` seconds.
     """
-    if cfg.rotation is not None:
-        raise ConfigError("Hadamard rotation is not implemented on the B200 path yet")
     flats, shape, m = _rank_tensors(tensors)
     n = len(flats)
     _check_topology(topology, n)
@@ -171,7 +169,17 @@ def flash_all_reduce(tensors: Sequence, cfg: FlashConfig, topology: Optional[Fab
     if comm is None:
         comm = local_comm(devices, slot_bytes_for(seg, cfg.stage1_codec, cfg.stage2_codec))
     comm.set_timeout(timeout if timeout is not None else 3600.0)
-    outs = comm.all_reduce_local(flats, cfg, out_dtype=odt, check=True)
+    if cfg.rotation is not None:
+        # rotate the zero-padded rank tensors (float32), all-reduce, rotate back, trim
+        from .rotation import hadamard_apply, hadamard_inverse
+
+        rot = cfg.rotation
+        rins = [hadamard_apply(f, rot, n * seg) for f in flats]
+        routs = comm.all_reduce_local(rins, cfg, out_dtype=torch.float32, check=True)
+        outs = [hadamard_inverse(o, rot, out_dtype=odt, n_out=m) for o in routs]
+        torch.cuda.synchronize(flats[0].device)
+    else:
+        outs = comm.all_reduce_local(flats, cfg, out_dtype=odt, check=True)
     qdq = int(not cfg.stage1_codec.is_passthrough) + int(not cfg.stage2_codec.is_passthrough)
     return CollectiveRun(
         method="flash",

@@ -53,6 +53,13 @@ fc_status fail(fc_status s, const char* fmt, ...) {
 fc_status validate_codec(const fc_codec* c) {
   if (!c) return fail(FC_ERR_CONFIG, "codec is NULL");
   if (c->kind == FC_KIND_FP16) return FC_OK;
+  if (c->kind == FC_KIND_MINIFLOAT) {
+    if (c->reserved < FC_FMT_E4M3 || c->reserved > FC_FMT_E2M1)
+      return fail(FC_ERR_CONFIG, "minifloat format must be one of ('e4m3', 'e5m2', 'e2m1')");
+    if (c->group_size < 1) return fail(FC_ERR_CONFIG, "group_size must be >= 1");
+    if (!(c->scale_floor > 0)) return fail(FC_ERR_CONFIG, "scale_floor must be positive");
+    return FC_OK;
+  }
   if (c->kind != FC_KIND_INT) return fail(FC_ERR_CONFIG, "unknown codec kind %d", c->kind);
   if (c->bits < 2 || c->bits > 8) return fail(FC_ERR_CONFIG, "bits must be in 2..8, got %d", c->bits);
   if (c->group_size < 1) return fail(FC_ERR_CONFIG, "group_size must be >= 1");
@@ -126,6 +133,21 @@ fc_status fc_codec_layout(const fc_codec* codec, int64_t n, fc_layout* out) {
   if (n < 0 || !out) return fail(FC_ERR_DOMAIN, "invalid element count");
   *out = layout_of(*codec, n);
   return FC_OK;
+}
+
+fc_status fc_hadamard(const void* x, int32_t in_dtype, int64_t n, int64_t n_padded, int32_t dim, int32_t normalize,
+                      const float* signs, int32_t inverse, void* out, int32_t out_dtype, int64_t n_out, void* stream) {
+  if (!x || !out) return fail(FC_ERR_CONFIG, "NULL buffer");
+  if (!dtype_ok(in_dtype) || !dtype_ok(out_dtype)) return fail(FC_ERR_CONFIG, "unsupported dtype");
+  if (dim < 1 || (dim & (dim - 1)) != 0) return fail(FC_ERR_CONFIG, "dimension must be a power of two >= 1, got %d", dim);
+  if (dim > 8192) return fail(FC_ERR_CONFIG, "Hadamard block dimension %d exceeds 8192 on the GPU path", dim);
+  if (n < 0 || n_padded < n || n_out < 0 || n_out > n_padded)
+    return fail(FC_ERR_DOMAIN, "invalid lengths (n=%lld, padded=%lld)", (long long)n, (long long)n_padded);
+  if (n_padded % dim != 0)  // rotation.py:53-58
+    return fail(FC_ERR_DOMAIN, "length %lld is not divisible by block dimension %d", (long long)n_padded, dim);
+  if (n_padded == 0) return FC_OK;
+  return launch_hadamard(x, in_dtype, n, n_padded, dim, normalize, signs, inverse, out, out_dtype, n_out,
+                         (cudaStream_t)stream);
 }
 
 fc_status fc_flash_resolve_chunk(const fc_flash_cfg* cfg, int32_t world, int64_t* chunk_out) {

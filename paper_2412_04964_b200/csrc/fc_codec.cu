@@ -101,6 +101,80 @@ static unsigned resident_grid(const void* kern, int smem, int64_t items, int sms
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)occ * sms));
 }
 
+static int cur_sms();
+
+// --------------------------------------------------------------------------
+// blocked Hadamard rotation (rotation.py:38-83): one CTA per block of `dim`
+// elements at a time, float64 butterflies in shared memory in the reference's
+// order (top = a + b, bottom = a - b, h = 1, 2, 4, ...), one final rounding
+
+template <typename Ti, typename To>
+__global__ void __launch_bounds__(256) k_hadamard(const Ti* __restrict__ x, int64_t n, int64_t n_padded, int dim,
+                                                  int normalize, const float* __restrict__ signs, int inverse,
+                                                  To* __restrict__ out, int64_t n_out) {
+  extern __shared__ __align__(16) double hs[];
+  const double rs = sqrt((double)dim);
+  for (int64_t base = (int64_t)blockIdx.x * dim; base < n_padded; base += (int64_t)gridDim.x * dim) {
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
+      const int64_t gi = base + i;
+      double v = gi < n ? (double)DT<Ti>::to_f(x[gi]) : 0.0;
+      if (!inverse && signs) v *= (double)signs[i];  // H(D x)
+      hs[i] = v;
+    }
+    __syncthreads();
+    for (int h = 1; h < dim; h <<= 1) {
+      for (int k = threadIdx.x; k < dim / 2; k += blockDim.x) {
+        const int i = (k / h) * 2 * h + (k % h);
+        const double a = hs[i], b = hs[i + h];
+        hs[i] = a + b;
+        hs[i + h] = a - b;
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
+      double y = hs[i];
+      if (!inverse) {
+        if (normalize) y = y / rs;
+      } else {
+        y = normalize ? y / rs : y / (double)dim;
+        if (signs) y *= (double)signs[i];  // D(H x)
+      }
+      const int64_t gi = base + i;
+      if (gi < n_out) out[gi] = DT<To>::from_f((float)y);  // float32 result (astype(float32)), then the output dtype
+    }
+    __syncthreads();
+  }
+}
+
+fc_status launch_hadamard(const void* x, int in_dtype, int64_t n, int64_t n_padded, int dim, int normalize,
+                          const float* signs, int inverse, void* out, int out_dtype, int64_t n_out, cudaStream_t st) {
+  const int smem = dim * (int)sizeof(double);
+  const int64_t blocks = n_padded / dim;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(blocks, (int64_t)cur_sms() * 8));
+#define FC_HD(TI, TO)                                                                                        \
+  do {                                                                                                       \
+    const void* k = (const void*)k_hadamard<TI, TO>;                                                         \
+    FC_TRY(ensure_smem_attr(k, smem));                                                                       \
+    k_hadamard<TI, TO><<<grid, 256, smem, st>>>((const TI*)x, n, n_padded, dim, normalize, signs, inverse,    \
+                                                (TO*)out, n_out);                                            \
+  } while (0)
+#define FC_HD_OUT(TI)                                            \
+  switch (out_dtype) {                                           \
+    case FC_DTYPE_F32: FC_HD(TI, float); break;                  \
+    case FC_DTYPE_F16: FC_HD(TI, __half); break;                 \
+    default: FC_HD(TI, __nv_bfloat16); break;                    \
+  }
+  switch (in_dtype) {
+    case FC_DTYPE_F32: FC_HD_OUT(float); break;
+    case FC_DTYPE_F16: FC_HD_OUT(__half); break;
+    default: FC_HD_OUT(__nv_bfloat16); break;
+  }
+#undef FC_HD_OUT
+#undef FC_HD
+  FC_CUDA_TRY(cudaGetLastError());
+  return FC_OK;
+}
+
 // --------------------------------------------------------------------------
 // launchers
 
@@ -179,7 +253,7 @@ static fc_status dequant_stream(const uint8_t* src, int64_t n, const DevCodec& d
 template <typename T>
 static void quant_generic(const T* x, int64_t n, const DevCodec& dc, uint8_t* dst, uint32_t* err, cudaStream_t st) {
   SrcSeg<T> src{x, 0, n};
-  if (dc.kind == FC_KIND_INT) {
+  if (dc.kind != FC_KIND_FP16) {  // int and minifloat codes need per-group scales
     const int64_t groups = (n + dc.g - 1) / dc.g;
     k_gen_params<<<(unsigned)((groups + 255) / 256), 256, 0, st>>>(src, n, dc, dst, err, 0u);
   }

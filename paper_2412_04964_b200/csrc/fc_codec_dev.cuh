@@ -28,7 +28,38 @@ struct SrcF32 {
   __device__ __forceinline__ float operator()(int64_t i) const { return p[i]; }
 };
 
+// ---- minifloat codes (minifloat.py:58-124, codec.py:332-351): grid value of
+// RN64(x / s), ties to even, saturating; IEEE-style subnormals
+__device__ __forceinline__ uint32_t mf_code(const DevCodec& c, float x, float s) {
+  const double q = __ddiv_rn((double)x, (double)s);
+  const double a = fabs(q);
+  const double min_normal = ldexp(1.0, 1 - c.mf_bias), sub_q = ldexp(1.0, 1 - c.mf_bias - c.mf_mant);
+  int e2;
+  frexp(a, &e2);
+  const double quantum = a < min_normal ? sub_q : ldexp(1.0, e2 - 1 - c.mf_mant);
+  const double r = fmin(rint(a / quantum) * quantum, c.mf_max);
+  const uint32_t sign = (q < 0.0 && r > 0.0) ? 1u : 0u;  // encode() tests v < 0 on the signed grid value
+  uint32_t ec, mc;
+  if (r < min_normal) {
+    ec = 0;
+    mc = (uint32_t)(r / sub_q);
+  } else {
+    int er;
+    frexp(r, &er);
+    ec = (uint32_t)(er - 1 + c.mf_bias);
+    mc = (uint32_t)((ldexp(r, -(er - 1)) - 1.0) * (double)(1 << c.mf_mant));
+  }
+  return (sign << (c.mf_exp + c.mf_mant)) | (ec << c.mf_mant) | mc;
+}
+__device__ __forceinline__ float mf_value(const DevCodec& c, uint32_t code) {
+  const uint32_t mc = code & ((1u << c.mf_mant) - 1u), ec = (code >> c.mf_mant) & ((1u << c.mf_exp) - 1u);
+  const float mag = ec == 0 ? (float)mc * ldexpf(1.0f, 1 - c.mf_bias - c.mf_mant)
+                            : (1.0f + (float)mc / (float)(1 << c.mf_mant)) * ldexpf(1.0f, (int)ec - c.mf_bias);
+  return (code >> (c.mf_exp + c.mf_mant)) ? -mag : mag;
+}
+
 __device__ __forceinline__ uint32_t code_of(const DevCodec& c, float v, float s, float zf) {
+  if (c.kind == FC_KIND_MINIFLOAT) return mf_code(c, v, s);
   float t = __fdiv_rn(v, s);
   t = c.ceil_mode ? ceilf(t) : rintf(t);
   t = fminf(fmaxf(t + zf, c.qmin_f), c.qmax_f);
@@ -55,10 +86,11 @@ __global__ void k_gen_params(Src src, int64_t n, DevCodec c, uint8_t* dst, uint3
     const int64_t start = gi * c.g;
     const int64_t end = min(start + (int64_t)c.g, n);
     float lo = INFINITY, hi = -INFINITY, probe = 0.0f;
+    const bool absmax = c.sym || c.kind == FC_KIND_MINIFLOAT;
     for (int64_t p = start; p < end; ++p) {
       const float v = src(p);
       probe = fmaf(v, 0.0f, probe);
-      if (c.sym) {
+      if (absmax) {
         hi = fmaxf(hi, fabsf(v));
       } else {
         lo = fminf(lo, v);
@@ -68,7 +100,7 @@ __global__ void k_gen_params(Src src, int64_t n, DevCodec c, uint8_t* dst, uint3
     if (probe != probe && err) atomicOr(err, make_err(kErrNonFinite, 0, 0, rank));
     __half s16;
     uint8_t z8 = 0;
-    if (c.sym) {
+    if (absmax) {  // sym: absmax / (2^(b-1)-1); minifloat: absmax / max_finite (codec.py:345)
       s16 = snap_scale((double)hi / c.qdiv, c.floor);
     } else {
       s16 = snap_scale(((double)hi - (double)lo) / c.qdiv, c.floor);
@@ -77,7 +109,7 @@ __global__ void k_gen_params(Src src, int64_t n, DevCodec c, uint8_t* dst, uint3
       z8 = (uint8_t)(int)z;
     }
     reinterpret_cast<__half*>(dst + c.scales_off)[gi] = s16;
-    if (!c.sym) dst[c.zeros_off + gi] = z8;
+    if (!absmax) dst[c.zeros_off + gi] = z8;
   }
 }
 
@@ -105,7 +137,7 @@ __global__ void k_gen_codes(Src src, int64_t n, DevCodec c, uint8_t* dst, uint32
       if (p >= n) break;
       const int64_t gi = p / c.g;
       const float s = __half2float(sc[gi]);
-      const float zf = c.sym ? 0.0f : (float)dst[c.zeros_off + gi];
+      const float zf = (c.sym || c.kind == FC_KIND_MINIFLOAT) ? 0.0f : (float)dst[c.zeros_off + gi];
       byte |= code_of(c, src(p), s, zf) << (4 * k);
     }
     dst[u] = (uint8_t)byte;
@@ -122,6 +154,7 @@ __device__ __forceinline__ float gen_value_at(const DevCodec& c, const uint8_t* 
   }
   const int64_t gi = i / c.g;
   const float s = __half2float(reinterpret_cast<const __half*>(src + c.scales_off)[gi]);
+  if (c.kind == FC_KIND_MINIFLOAT) return mf_value(c, code) * s;  // exact (<= 4 x 11 significant bits)
   const float zf = c.sym ? 0.0f : (float)src[c.zeros_off + gi];
   return value_of(c, code, s, zf);
 }

@@ -55,6 +55,9 @@ struct DevCodec {
   uint32_t floor16;  // bit pattern of the smallest fp16 >= floor (0x7C00 if none)
   int64_t scales_off;
   int64_t zeros_off;
+  // minifloat (FC_KIND_MINIFLOAT): e/m bits, bias, largest finite magnitude
+  int mf_exp, mf_mant, mf_bias;
+  double mf_max;
 };
 
 // --------------------------------------------------------------------------

@@ -33,8 +33,25 @@ void set_error(const char* fmt, ...);
 inline int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// minifloat.py:40-45: (exp bits, mantissa bits, bias, max finite)
+struct MiniFmt {
+  int e, m, bias;
+  double max_finite;
+};
+inline MiniFmt minifloat_format(int id) {
+  switch (id) {
+    case FC_FMT_E5M2: return {5, 2, 15, 57344.0};
+    case FC_FMT_E2M1: return {2, 1, 1, 6.0};
+    default: return {4, 3, 7, 448.0};
+  }
+}
+
 inline int storage_bits(const fc_codec& c) {
   if (c.kind == FC_KIND_FP16) return 16;
+  if (c.kind == FC_KIND_MINIFLOAT) {
+    const MiniFmt f = minifloat_format(c.reserved);
+    return 1 + f.e + f.m <= 4 ? 4 : 8;
+  }
   return c.bits <= 4 ? 4 : 8;
 }
 
@@ -53,13 +70,14 @@ inline fc_layout layout_of(const fc_codec& c, int64_t n) {
   const bool has_zero = c.kind == FC_KIND_INT && !c.symmetric;
   L.total_bytes = L.zeros_offset + (has_zero ? align_up(L.groups, 16) : 0);
   if (L.total_bytes == 0) L.total_bytes = 16;
-  const int meta = (c.kind == FC_KIND_FP16) ? 0 : (c.symmetric ? 2 : 3);
+  const int meta = (c.kind == FC_KIND_FP16) ? 0 : ((c.kind == FC_KIND_INT && !c.symmetric) ? 3 : 2);
   L.wire_bytes = L.codes_bytes + L.groups * meta;
   return L;
 }
 
 inline bool fast_group(const fc_codec& c) {
   if (c.kind == FC_KIND_FP16) return true;
+  if (c.kind == FC_KIND_MINIFLOAT) return false;  // minifloat codes run on the generic kernels
   return c.group_size == 32 || c.group_size == 64 || c.group_size == 128 || c.group_size == 256;
 }
 
@@ -102,6 +120,15 @@ inline DevCodec dev_codec(const fc_codec& c, const fc_layout& L) {
     }
   }
   d.qinv = d.qdiv > 0 ? 1.0 / d.qdiv : 0.0;
+  if (c.kind == FC_KIND_MINIFLOAT) {
+    const MiniFmt f = minifloat_format(c.reserved);
+    d.mf_exp = f.e;
+    d.mf_mant = f.m;
+    d.mf_bias = f.bias;
+    d.mf_max = f.max_finite;
+    d.qdiv = f.max_finite;  // raw scale = absmax / max_finite (codec.py:345)
+    d.bits = 1 + f.e + f.m;
+  }
   d.floor = c.scale_floor;
   d.floor16 = floor16_of(c.scale_floor);
   d.scales_off = L.scales_offset;
@@ -121,5 +148,7 @@ fc_status launch_dequantize(const void* src, int64_t n, const fc_codec& c, void*
                             cudaStream_t st, bool allow_fast);
 
 int num_sms(int device);
+fc_status launch_hadamard(const void* x, int in_dtype, int64_t n, int64_t n_padded, int dim, int normalize,
+                          const float* signs, int inverse, void* out, int out_dtype, int64_t n_out, cudaStream_t st);
 
 }  // namespace fc

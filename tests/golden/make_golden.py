@@ -221,6 +221,59 @@ def make_flash(out_path: str) -> None:
     print(f"flash: {len(meta)} cases -> {out_path}")
 
 
+# ---------------------------------------------------------------------------
+# extras: minifloat stage codecs and the Hadamard rotation
+
+MF_CODEC_CASES = [(fmt, g) for fmt in ("e4m3", "e5m2", "e2m1") for g in (32, 96, 128, 256)]
+
+EXTRA_FLASH = [
+    # (n_ranks, m, stage1, stage2, rotation (dim, normalize, seed) or None, family)
+    (4, 40000, ("e4m3", 128), ("e4m3", 128), None, "act"),
+    (8, 65536, ("e2m1", 32), ("e4m3", 32), None, "act"),
+    (2, 10000, ("e5m2", 64), ("e5m2", 64), None, "gauss_bf16"),
+    (4, 40960, (4, 128, False, "nearest-even"), (4, 128, False, "nearest-even"), (128, True, None), "act"),
+    (8, 65536, (4, 128, False, "nearest-even"), (8, 128, False, "nearest-even"), (256, True, 3), "act"),
+    (4, 12288, ("e4m3", 64), ("e4m3", 64), (64, True, 11), "gauss_bf16"),
+    (2, 4096, (8, 128, True, "nearest-even"), (8, 128, True, "nearest-even"), (32, False, 5), "gauss_bf16"),
+]
+
+
+def extra_stage(spec):
+    if isinstance(spec, tuple) and isinstance(spec[0], str):
+        return qc.CodecConfig(number_format=spec[0], group_size=spec[1])
+    return stage_codec(spec)
+
+
+def make_extras(out_path: str) -> None:
+    rng = np.random.default_rng(2412)
+    arrays, mf_meta, fl_meta = {}, [], []
+    for i, (fmt, g) in enumerate(MF_CODEC_CASES):
+        fam = FAMILIES[i % len(FAMILIES)]
+        n = int(rng.choice([997, 1024, 4096]))
+        x = fam_inputs(rng, fam, n)
+        cfg = qc.CodecConfig(number_format=fmt, group_size=g)
+        q = qc.quantize(x, cfg)
+        arrays[f"mf{i}_x"] = x
+        arrays[f"mf{i}_wire"] = np.frombuffer(q.to_bytes(), np.uint8)
+        arrays[f"mf{i}_deq"] = qc.dequantize(q)
+        mf_meta.append(dict(format=fmt, group_size=g, family=fam, n=n))
+    for i, (n, m, s1, s2, rot, fam) in enumerate(EXTRA_FLASH):
+        xs = rank_inputs(rng, fam, n, m)
+        rb = None if rot is None else qc.HadamardBlock(dimension=rot[0], normalize=rot[1], sign_seed=rot[2])
+        cfg = qc.FlashConfig(stage1_codec=extra_stage(s1), stage2_codec=extra_stage(s2), rotation=rb)
+        run = qc.flash_all_reduce(xs, cfg)
+        for o in run.outputs[1:]:
+            assert np.array_equal(o, run.outputs[0])
+        for r, x in enumerate(xs):
+            arrays[f"fl{i}_x{r}"] = x
+        arrays[f"fl{i}_out"] = run.outputs[0]
+        fl_meta.append(dict(n=n, m=m, stage1=s1, stage2=s2, rotation=rot, family=fam,
+                            wire_bytes_per_rank=run.wire_bytes_per_rank))
+    arrays["meta"] = np.frombuffer(json.dumps({"minifloat": mf_meta, "flash": fl_meta}).encode(), np.uint8)
+    np.savez_compressed(out_path, **arrays)
+    print(f"extras: {len(mf_meta)} minifloat codec + {len(fl_meta)} flash cases -> {out_path}")
+
+
 def make_reports(out_path: str) -> None:
     rep = {"rs_vs_ag": {}, "baseline_mse": {}}
     prof = qc.ActivationProfile()
@@ -243,10 +296,12 @@ def make_reports(out_path: str) -> None:
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["codec", "flash", "reports"]
+    which = sys.argv[1:] or ["codec", "flash", "reports", "extras"]
     if "codec" in which:
         make_codec(os.path.join(HERE, "codec.npz"))
     if "flash" in which:
         make_flash(os.path.join(HERE, "flash.npz"))
     if "reports" in which:
         make_reports(os.path.join(HERE, "reports.json"))
+    if "extras" in which:
+        make_extras(os.path.join(HERE, "extras.npz"))

@@ -67,3 +67,19 @@ def flash_wire(i: int, src: int, dst: int) -> list[bytes]:
         out.append(blob[off:off + int(ln)])
         off += int(ln)
     return out
+
+
+@lru_cache(maxsize=None)
+def extras_npz():
+    return np.load(os.path.join(GOLDEN, "extras.npz"))
+
+
+def extras_meta():
+    return json.loads(bytes(extras_npz()["meta"]).decode())
+
+
+def extra_stage(spec) -> orc.Codec:
+    """Stage spec of extras.npz: [format, group] for minifloats, else oracle_stage."""
+    if isinstance(spec, (list, tuple)) and isinstance(spec[0], str):
+        return orc.Codec(kind=spec[0], group_size=spec[1])
+    return oracle_stage(spec)

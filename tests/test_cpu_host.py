@@ -73,8 +73,14 @@ def test_codec_validation_mirrors_reference():
             fc.CodecConfig(**kw)
     bad = _lib.fc_codec(_lib.KIND_INT, 9, 128, 0, 0, 0, 1e-8)
     assert _lib.lib().fc_codec_validate(C.byref(bad)) == 1
-    with pytest.raises(fc.ConfigError):
-        fc.CodecConfig(number_format="e4m3").to_fc()  # minifloats not on the GPU path yet
+    mf = fc.CodecConfig(number_format="e4m3").to_fc()  # minifloats: kind 2, format id in `reserved`
+    assert (mf.kind, mf.bits, mf.reserved) == (_lib.KIND_MINIFLOAT, 8, 0)
+    assert _lib.lib().fc_codec_validate(C.byref(mf)) == 0
+    bad_mf = _lib.fc_codec(_lib.KIND_MINIFLOAT, 8, 128, 0, 0, 7, 1e-8)
+    assert _lib.lib().fc_codec_validate(C.byref(bad_mf)) == 1
+    for fmt, wire in (("e4m3", 1000 + 8 * 2), ("e5m2", 1000 + 8 * 2), ("e2m1", 500 + 8 * 2)):
+        cfg = fc.CodecConfig(number_format=fmt)
+        assert cfg.device_layout(1000).wire_bytes == cfg.wire_byte_len(1000) == wire
 
 
 def test_json_and_names():

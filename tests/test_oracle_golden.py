@@ -155,3 +155,25 @@ def test_snap_scale_edges():
     assert float(s[1]) == float(np.float16(2.0 ** -24))
     assert float(s[2]) == float(np.float16(2.0 ** -24))
     assert float(s[3]) == 1.0
+
+
+def test_oracle_minifloat_codec_matches_reference():
+    """codec.py:332-351 (e4m3 / e5m2 / e2m1): wire bytes and float32 decode."""
+    z, meta = gio.extras_npz(), gio.extras_meta()["minifloat"]
+    assert meta
+    for i, m in enumerate(meta):
+        q = orc.quantize(z[f"mf{i}_x"], orc.Codec(kind=m["format"], group_size=m["group_size"]))
+        assert q.wire_bytes() == bytes(z[f"mf{i}_wire"]), m
+        assert np.array_equal(orc.dequantize(q).view(np.uint32), z[f"mf{i}_deq"].view(np.uint32)), m
+
+
+def test_oracle_flash_minifloat_and_rotation_match_reference():
+    """collectives.py:321-402 with minifloat stages and the Hadamard rotation
+    (rotation.py:61-83), against the reference's own outputs."""
+    z, meta = gio.extras_npz(), gio.extras_meta()["flash"]
+    for i, m in enumerate(meta):
+        xs = [z[f"fl{i}_x{r}"] for r in range(m["n"])]
+        rot = None if m["rotation"] is None else orc.Hadamard(*m["rotation"])
+        res = orc.flash_all_reduce(xs, gio.extra_stage(m["stage1"]), gio.extra_stage(m["stage2"]), rotation=rot)
+        assert np.array_equal(res.outputs[0].view(np.uint32), z[f"fl{i}_out"].view(np.uint32)), m
+        assert res.wire_bytes_per_rank == m["wire_bytes_per_rank"], m
