@@ -405,27 +405,30 @@ template <class Spec, bool ACC, int CW>
 __device__ __forceinline__ void decode_pairs(const LaneCodes<CW>& L, PairLane<Spec::SB>& out) {
   static_assert(Spec::kFast, "compile-time codec");
   const uint64_t S2 = f2_splat(L.s), NMZ2 = f2_splat(-L.mz);
-  auto emit = [&](int idx, uint32_t va, uint32_t vb) {
+  auto emit = [&](int idx, uint32_t va, uint32_t vb, uint64_t nmz, uint64_t sc) {
     uint64_t M;
     asm("mov.b64 %0, {%1,%2};" : "=l"(M) : "r"(va), "r"(vb));
-    const uint64_t D = f2_add(M, NMZ2);  // c - z, exact
-    out.p[idx] = ACC ? f2_fma(D, S2, out.p[idx]) : f2_mul(D, S2);
+    const uint64_t D = f2_add(M, nmz);  // (c - z) or 16 (c - z), exact
+    out.p[idx] = ACC ? f2_fma(D, sc, out.p[idx]) : f2_mul(D, sc);
   };
   if constexpr (Spec::SB == 4) {
+    // high nibbles stay in place (byte = 16 c): decode 16 (c - z) * (s / 16), the same exact
+    // product, and save the shift that would isolate them
+    const uint64_t S16 = f2_splat(L.s * 0.0625f), NMZ16 = f2_splat(-fmaf(L.mz, 16.0f, -125829120.0f));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const uint32_t lo = L.w[i] & 0x0F0F0F0Fu, hi = (L.w[i] >> 4) & 0x0F0F0F0Fu;
-      emit(4 * i + 0, __byte_perm(lo, 0x4B000000u, 0x7440u), __byte_perm(lo, 0x4B000000u, 0x7442u));  // e, e+4
-      emit(4 * i + 2, __byte_perm(lo, 0x4B000000u, 0x7441u), __byte_perm(lo, 0x4B000000u, 0x7443u));  // e+2, e+6
-      emit(4 * i + 1, __byte_perm(hi, 0x4B000000u, 0x7440u), __byte_perm(hi, 0x4B000000u, 0x7442u));  // e+1, e+5
-      emit(4 * i + 3, __byte_perm(hi, 0x4B000000u, 0x7441u), __byte_perm(hi, 0x4B000000u, 0x7443u));  // e+3, e+7
+      const uint32_t lo = L.w[i] & 0x0F0F0F0Fu, hi = L.w[i] & 0xF0F0F0F0u;
+      emit(4 * i + 0, __byte_perm(lo, 0x4B000000u, 0x7440u), __byte_perm(lo, 0x4B000000u, 0x7442u), NMZ2, S2);
+      emit(4 * i + 2, __byte_perm(lo, 0x4B000000u, 0x7441u), __byte_perm(lo, 0x4B000000u, 0x7443u), NMZ2, S2);
+      emit(4 * i + 1, __byte_perm(hi, 0x4B000000u, 0x7440u), __byte_perm(hi, 0x4B000000u, 0x7442u), NMZ16, S16);
+      emit(4 * i + 3, __byte_perm(hi, 0x4B000000u, 0x7441u), __byte_perm(hi, 0x4B000000u, 0x7443u), NMZ16, S16);
     }
   } else {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t v = L.w[i];
-      emit(2 * i + 0, __byte_perm(v, 0x4B000000u, 0x7440u), __byte_perm(v, 0x4B000000u, 0x7442u));  // e, e+2
-      emit(2 * i + 1, __byte_perm(v, 0x4B000000u, 0x7441u), __byte_perm(v, 0x4B000000u, 0x7443u));  // e+1, e+3
+      emit(2 * i + 0, __byte_perm(v, 0x4B000000u, 0x7440u), __byte_perm(v, 0x4B000000u, 0x7442u), NMZ2, S2);  // e, e+2
+      emit(2 * i + 1, __byte_perm(v, 0x4B000000u, 0x7441u), __byte_perm(v, 0x4B000000u, 0x7443u), NMZ2, S2);  // e+1, e+3
     }
   }
 }
