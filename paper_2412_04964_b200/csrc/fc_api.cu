@@ -317,6 +317,7 @@ fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
     case FC_OPT_CTAS_PER_SM: c->ctas_per_sm = std::max<int64_t>(0, std::min<int64_t>(16, value)); break;
     case FC_OPT_STREAM_MASK: c->stream_mask = value & 63; break;
     case FC_OPT_PHASES: c->phases = value & 7; break;
+    case FC_OPT_ONESHOT: c->oneshot = value != 0; break;
     case FC_OPT_ROLE_WEIGHTS: c->role_weights = value; break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
@@ -338,6 +339,7 @@ fc_status fc_comm_get_option(fc_comm* c, int32_t option, int64_t* value) {
     case FC_OPT_CTAS_PER_SM: *value = c->ctas_per_sm; break;
     case FC_OPT_STREAM_MASK: *value = c->stream_mask; break;
     case FC_OPT_PHASES: *value = c->phases; break;
+    case FC_OPT_ONESHOT: *value = c->oneshot; break;
     case FC_OPT_ROLE_WEIGHTS: *value = c->role_weights; break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }

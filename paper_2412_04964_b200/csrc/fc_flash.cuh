@@ -16,6 +16,8 @@
 // registers).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "fc_codec_dev.cuh"
 #include "fc_lane.cuh"
 #include "fc_stage.cuh"
@@ -279,6 +281,36 @@ __device__ __forceinline__ int lane_valid(int64_t len, int64_t p0) {
   const int64_t d = len - p0;
   return d <= 0 ? 0 : (d >= kLaneElems ? kLaneElems : (int)d);
 }
+
+// Small messages on one GPU (decode regime, C4): the three phases in one
+// cooperative launch separated by grid-wide barriers, every item a direct
+// (register) lane codec call — no staging rings, no per-tile flags, one launch
+// instead of three.
+template <typename Tin, typename Tout, int CW, class S1, class S2>
+__global__ void __launch_bounds__(kThreads) k_oneshot(FlashArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int P = a.world - 1, nr = a.rank_hi - a.rank_lo;
+  for (int i = blockIdx.x; i < nr * P * a.tiles; i += gridDim.x) {
+    const int y = i / a.tiles, t = i - y * a.tiles;
+    int r, j;
+    pair_of(a, y, r, j);
+    do_scatter<Tin, CW, S1>(a, r, j, t);
+  }
+  grid.sync();
+  for (int i = blockIdx.x; i < nr * a.tiles; i += gridDim.x) {
+    const int y = i / a.tiles, t = i - y * a.tiles;
+    do_reduce<Tin, Tout, CW, S1, S2>(a, a.rank_lo + y, t);
+  }
+  grid.sync();
+  for (int i = blockIdx.x; i < nr * P * a.tiles; i += gridDim.x) {
+    const int y = i / a.tiles, t = i - y * a.tiles;
+    int r, j;
+    pair_of(a, y, r, j);
+    do_gather<Tout, CW, S2>(a, r, j, t);
+  }
+}
+
 
 template <typename Tin, int CW, class S1>
 __global__ void __launch_bounds__(kThreads) k_scatter(FlashArgs a) {

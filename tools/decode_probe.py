@@ -1,0 +1,31 @@
+"""C4 decode-regime latency probe: one-shot cooperative kernel vs the three
+streaming kernels, CUDA-graph device time, TP=8 emulated on one GPU."""
+import json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_2412_04964_b200 as fc
+from paper_2412_04964_b200 import _lib
+from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for
+from bench import graph_time
+
+dev = torch.device("cuda", 0)
+stream = torch.cuda.current_stream(dev)
+cfg = fc.FlashConfig.from_bits(4)
+for tp in (8, 4, 2):
+    for bs in (1, 8, 16, 32, 64):
+        m = bs * 8192
+        comm = FlashComm.local([0] * tp, slot_bytes_for(-(-m // tp), cfg.stage1_codec, cfg.stage2_codec))
+        ins = [torch.randn(m, device=dev).to(torch.bfloat16) for _ in range(tp)]
+        outs = [torch.empty_like(t) for t in ins]
+        res = {}
+        for name, opts in (("oneshot", {_lib.OPT_ONESHOT: 1}), ("split", {_lib.OPT_ONESHOT: 0}),
+                           ("fused", {_lib.OPT_FUSED: 1})):
+            comm.set_option(_lib.OPT_ONESHOT, 1)
+            comm.set_option(_lib.OPT_FUSED, -1)
+            for k, v in opts.items():
+                comm.set_option(k, v)
+            res[name] = graph_time(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), 20, stream) * 1e3
+            comm.check()
+        print(json.dumps({"tp": tp, "bs": bs, "latency_us": res}), flush=True)
+        comm.close()
