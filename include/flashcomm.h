@@ -139,8 +139,8 @@ FC_API fc_status fc_comm_destroy(fc_comm* comm);
 
 typedef enum {
   FC_OPT_FUSED = 0,        /* 1: one persistent kernel with per-tile flags (the streaming fused kernel when
-                              the scheme has a compile-time codec, else the staged one); 0: phase-split;
-                              -1 (default): fused across GPUs, phase-split when all ranks share one GPU */
+                              the scheme has a compile-time codec, else the staged one); 0 / -1 (default):
+                              phase-split streaming kernels (flag barriers between phases across GPUs) */
   FC_OPT_CTAS = 1,         /* CTAs per rank for the fused kernel (0 = auto) */
   FC_OPT_TIMEOUT_MS = 2,   /* flag-wait timeout -> ProtocolError (fabric.py:158-178); default 5000 */
   FC_OPT_LAG = 3,          /* fused schedule: tiles between a tile's scatter and its reduce (0 = auto) */
