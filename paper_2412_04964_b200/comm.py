@@ -15,6 +15,7 @@ reference ledger formula (collectives.py:152-157, costmodel.py:122-128).
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -140,6 +141,17 @@ def _device_index(d) -> int:
     return int(d)
 
 
+@functools.lru_cache(maxsize=None)
+def _ptr_array(n: int):
+    return C.c_void_p * n
+
+
+@functools.lru_cache(maxsize=256)
+def _cfg_struct(cfg) -> _lib.fc_flash_cfg:
+    return _lib.fc_flash_cfg(cfg.stage1_codec.to_fc(), cfg.stage2_codec.to_fc(),
+                             int(cfg.chunk_size) if cfg.chunk_size is not None else 0)
+
+
 class FlashComm:
     """Peer-buffer manager + topology + flag protocol (see module doc)."""
 
@@ -211,8 +223,9 @@ class FlashComm:
     # ---------------------------------------------------------------- calls
     @staticmethod
     def _cfg(cfg) -> _lib.fc_flash_cfg:
-        return _lib.fc_flash_cfg(cfg.stage1_codec.to_fc(), cfg.stage2_codec.to_fc(),
-                                 int(cfg.chunk_size) if cfg.chunk_size is not None else 0)
+        # FlashConfig is frozen (hashable): the C struct is built once per config
+        # (the C side takes it as const), keeping the per-call host path short
+        return _cfg_struct(cfg)
 
     def all_reduce_local(self, ins: Sequence[torch.Tensor], cfg, outs: Optional[Sequence[torch.Tensor]] = None,
                          out_dtype: Optional[torch.dtype] = None, check: bool = True) -> list:
@@ -228,7 +241,7 @@ class FlashComm:
                 raise ProtocolError(f"rank {r} tensor length {t.numel()} != rank 0 length {n}")
             if t.dtype != dt:
                 raise ProtocolError(f"rank {r} dtype {t.dtype} != rank 0 dtype {dt}")
-            if not t.is_cuda or t.device.index != self.devices[r]:
+            if t.get_device() != self.devices[r]:  # -1 for host tensors
                 raise DomainError(f"rank {r} tensor must live on cuda:{self.devices[r]}")
             if not t.is_contiguous():
                 raise DomainError(f"rank {r} tensor must be contiguous")
@@ -236,9 +249,14 @@ class FlashComm:
         if outs is None:
             outs = [torch.empty(n, dtype=odt, device=t.device) for t in ins]
         N = self.world_size
-        pin = (C.c_void_p * N)(*[t.data_ptr() for t in ins])
-        pout = (C.c_void_p * N)(*[o.data_ptr() for o in outs])
-        pst = (C.c_void_p * N)(*[torch.cuda.current_stream(t.device).cuda_stream for t in ins])
+        arr = _ptr_array(N)
+        pin = arr(*[t.data_ptr() for t in ins])
+        pout = arr(*[o.data_ptr() for o in outs])
+        streams = {}  # one current-stream lookup per distinct device
+        for d in self.devices:
+            if d not in streams:
+                streams[d] = torch.cuda.current_stream(d).cuda_stream
+        pst = arr(*[streams[d] for d in self.devices])
         c = self._cfg(cfg)
         _lib.check(_lib.lib().fc_flash_all_reduce_local(self._h, pin, pout, n, fc_dtype(dt), fc_dtype(odt),
                                                         C.byref(c), pst))

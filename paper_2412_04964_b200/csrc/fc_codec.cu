@@ -96,8 +96,9 @@ static fc_status ensure_smem_attr(const void* kern, int bytes) {
 }
 
 static unsigned resident_grid(const void* kern, int smem, int64_t items, int sms) {
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int occ = std::max(1, occupancy(kern, kThreads, smem, dev));
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)occ * sms));
 }
 
@@ -223,8 +224,9 @@ static FlashArgs codec_args(const void* in, void* out, int64_t n, const DevCodec
 }
 
 static unsigned stream_grid_cur(const void* kern, int threads, int smem, int64_t items) {
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int occ = std::max(1, occupancy(kern, threads, smem, dev));
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)occ * cur_sms()));
 }
 

@@ -6,6 +6,9 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 
 #include "../../include/flashcomm.h"
@@ -148,6 +151,25 @@ fc_status launch_dequantize(const void* src, int64_t n, const fc_codec& c, void*
                             cudaStream_t st, bool allow_fast);
 
 int num_sms(int device);
+
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor, memoised per (kernel, threads,
+// smem, device): the query costs microseconds of host time per launch, which
+// starves the GPU between short kernels (mid-size messages)
+inline int occupancy(const void* kern, int threads, int smem, int dev) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, int>, int> memo;
+  const auto key = std::make_tuple(kern, threads, smem, dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) occ = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  memo[key] = occ;
+  return occ;
+}
 fc_status launch_hadamard(const void* x, int in_dtype, int64_t n, int64_t n_padded, int dim, int normalize,
                           const float* signs, int inverse, void* out, int out_dtype, int64_t n_out, cudaStream_t st);
 
