@@ -153,7 +153,8 @@ typedef enum {
   FC_OPT_STREAM_MASK = 10,  /* testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels */
   FC_OPT_PHASES = 11,       /* measurement only: run just these phases (bit 0/1/2) of a one-GPU split call */
   FC_OPT_ROLE_WEIGHTS = 12, /* fused stream kernel CTA roles: scatter | reduce << 8 | gather << 16 (sum <= 16) */
-  FC_OPT_ONESHOT = 13       /* one GPU: small calls as one cooperative launch with grid barriers (default 1) */
+  FC_OPT_ONESHOT = 13,      /* one GPU: small calls as one cooperative launch with grid barriers (default 1) */
+  FC_OPT_HOST_CHUNK_BYTES = 14 /* fc_flash_all_reduce_host: H2D bytes per rank per pipeline chunk (0 = auto) */
 } fc_option;
 FC_API fc_status fc_comm_set_option(fc_comm* comm, int32_t option, int64_t value);
 FC_API fc_status fc_comm_get_option(fc_comm* comm, int32_t option, int64_t* value);
@@ -164,6 +165,24 @@ FC_API fc_status fc_comm_get_option(fc_comm* comm, int32_t option, int64_t* valu
 FC_API fc_status fc_flash_all_reduce_local(fc_comm* comm, const void* const* ins, void* const* outs, int64_t n,
                                     int32_t in_dtype, int32_t out_dtype, const fc_flash_cfg* cfg,
                                     void* const* streams);
+/* flash_all_reduce on HOST buffers (the reference's call shape: arrays in,
+ * new arrays out, blocking; collectives.py:321-402) for a local communicator.
+ * host_ins[r] / host_outs[r] are rank r's host buffers of n elements;
+ * host_outs[r] may be NULL (rank r's result is not read back). The comm's
+ * device staging is filled chunk by chunk: the H2D copy of chunk k+1, the
+ * flash all-reduce of chunk k (groups keep their segment anchors, so results
+ * equal one whole-tensor call bit for bit) and the D2H copy of chunk k-1 run
+ * concurrently on per-device copy/compute streams. Pinned host memory
+ * (cudaHostAlloc / cudaHostRegister) gives full PCIe bandwidth; pageable
+ * memory works at the driver's staged-copy speed. Device faults are returned
+ * like fc_comm_check. */
+FC_API fc_status fc_flash_all_reduce_host(fc_comm* comm, const void* const* host_ins, void* const* host_outs, int64_t n,
+                                          int32_t in_dtype, int32_t out_dtype, const fc_flash_cfg* cfg);
+/* fc_flash_all_reduce_host, per-rank form (IPC world): this rank's host
+ * buffers; every rank calls it with the same n / cfg / FC_OPT_HOST_CHUNK_BYTES
+ * (the chunk sequence must match across ranks). host_out may be NULL. */
+FC_API fc_status fc_flash_all_reduce_host_rank(fc_comm* comm, const void* host_in, void* host_out, int64_t n,
+                                               int32_t in_dtype, int32_t out_dtype, const fc_flash_cfg* cfg);
 /* flash_all_reduce, per-rank form (IPC world): every rank calls it with the
  * same n/cfg in the same order. in may alias out. */
 FC_API fc_status fc_flash_all_reduce(fc_comm* comm, const void* in, void* out, int64_t n, int32_t in_dtype,

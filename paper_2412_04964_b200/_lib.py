@@ -25,7 +25,7 @@ MINIFLOAT_FORMAT_IDS = {"e4m3": 0, "e5m2": 1, "e2m1": 2}
 ROUND_NEAREST_EVEN, ROUND_CEIL = 0, 1
 OPT_FUSED, OPT_CTAS, OPT_TIMEOUT_MS, OPT_LAG, OPT_FAST, OPT_LAST_LAUNCHES, OPT_REDUCE_STAGES = 0, 1, 2, 3, 4, 5, 6
 OPT_SCATTER_STAGES, OPT_GATHER_STAGES, OPT_CTAS_PER_SM, OPT_STREAM_MASK, OPT_PHASES = 7, 8, 9, 10, 11
-OPT_ROLE_WEIGHTS, OPT_ONESHOT = 12, 13
+OPT_ROLE_WEIGHTS, OPT_ONESHOT, OPT_HOST_CHUNK_BYTES = 12, 13, 14
 
 
 class fc_codec(C.Structure):
@@ -76,6 +76,9 @@ _SIGS = {
     "fc_comm_get_option": (C.c_int, [_P, _I32, C.POINTER(_I64)]),
     "fc_flash_all_reduce_local": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), _I64, _I32, _I32,
                                             C.POINTER(fc_flash_cfg), C.POINTER(_P)]),
+    "fc_flash_all_reduce_host": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_P), _I64, _I32, _I32,
+                                           C.POINTER(fc_flash_cfg)]),
+    "fc_flash_all_reduce_host_rank": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, C.POINTER(fc_flash_cfg)]),
     "fc_flash_all_reduce": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, C.POINTER(fc_flash_cfg), _P]),
     "fc_comm_check": (C.c_int, [_P, _I32]),
     "fc_comm_slot": (C.c_int, [_P, _I32, _I32, _I32, _P, C.POINTER(fc_layout)]),

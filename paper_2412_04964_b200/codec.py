@@ -184,6 +184,18 @@ def as_device_tensor(x, device=None) -> torch.Tensor:
     return t.reshape(-1).contiguous()
 
 
+def as_host_tensor(x) -> torch.Tensor:
+    """Flat contiguous host view of `x` (torch CPU tensor of a supported dtype,
+    else a float32 copy, like as_device_tensor)."""
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32)))
+    if t.dtype not in _TORCH_DTYPES:
+        t = t.to(torch.float32)
+    return t.reshape(-1).contiguous()
+
+
 def _stream_of(t: torch.Tensor) -> int:
     return torch.cuda.current_stream(t.device).cuda_stream
 

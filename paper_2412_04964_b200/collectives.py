@@ -20,7 +20,7 @@ from typing import Optional, Sequence
 
 import torch
 
-from .codec import CodecConfig, PASSTHROUGH_FP16, as_device_tensor, int6_flash_pair
+from .codec import CodecConfig, PASSTHROUGH_FP16, as_device_tensor, as_host_tensor, int6_flash_pair
 from .comm import DEFAULT_TIMEOUT_S, FabricTopology, FlashComm, TrafficLedger, flash_ledger, slot_bytes_for
 from .errors import ConfigError, DomainError, ProtocolError
 
@@ -148,7 +148,7 @@ def local_comm(devices: Sequence[int], slot_bytes: int) -> FlashComm:
 
 def flash_all_reduce(tensors: Sequence, cfg: FlashConfig, topology: Optional[FabricTopology] = None,
                      timeout: float = DEFAULT_TIMEOUT_S, *, out_dtype: Optional[torch.dtype] = None,
-                     comm: Optional[FlashComm] = None) -> CollectiveRun:
+                     comm: Optional[FlashComm] = None, outs: Optional[Sequence] = None) -> CollectiveRun:
     """Two-step quantized all-reduce (collectives.py:321-402) on the GPU.
 
     Outputs are new tensors of the input shape and, unless `out_dtype` is
@@ -156,7 +156,16 @@ def flash_all_reduce(tensors: Sequence, cfg: FlashConfig, topology: Optional[Fab
     bf16/fp16 output is its round-to-nearest-even). Blocks until done and
     raises like the reference: DomainError for NaN/inf input, ProtocolError
     when a rank never arrives within `timeout` seconds.
+
+    Host tensors / arrays in (the reference's own call shape) give host
+    tensors out: one blocking call pipelines the H2D copy, the all-reduce and
+    the D2H copy chunk by chunk (fc_flash_all_reduce_host); `outs` may supply
+    the host output tensors (flat, n elements each) to reuse pinned buffers.
     """
+    if cfg.rotation is None and _all_host(tensors):
+        return _flash_all_reduce_host(tensors, cfg, topology, timeout, out_dtype, comm, outs)
+    if outs is not None:
+        raise ConfigError("outs= is for host tensors (device callers use FlashComm.all_reduce_local)")
     flats, shape, m = _rank_tensors(tensors)
     n = len(flats)
     _check_topology(topology, n)
@@ -191,6 +200,57 @@ def flash_all_reduce(tensors: Sequence, cfg: FlashConfig, topology: Optional[Fab
         reduce_elems_per_rank=(n - 1) * seg,
         gather_elems_per_rank=(n - 1) * seg,
     )
+
+
+def _all_host(tensors: Sequence) -> bool:
+    return len(tensors) > 0 and all(not (isinstance(t, torch.Tensor) and t.is_cuda) for t in tensors)
+
+
+def _flash_all_reduce_host(tensors, cfg, topology, timeout, out_dtype, comm, outs=None) -> CollectiveRun:
+    """Host arrays in, new host arrays out (the reference's own call shape):
+    one blocking C-ABI call (fc_flash_all_reduce_host) pipelines the chunked
+    H2D copy, the flash all-reduce and the D2H copy on the communicator's
+    streams; the result equals the device-buffer call bit for bit."""
+    flats, shape, m = _host_rank_tensors(tensors)
+    n = len(flats)
+    _check_topology(topology, n)
+    odt = out_dtype or flats[0].dtype
+    if n == 1:  # collectives.py:340-341
+        return CollectiveRun("flash", [flats[0].to(odt).clone().reshape(shape)], TrafficLedger.zeros(1), 0, 0, 0, 0, 0)
+    chunk = cfg.resolve_chunk_size(n)  # ConfigError exactly like the reference
+    seg = -(-m // n)
+    dev = torch.cuda.current_device()
+    if comm is None:
+        comm = local_comm([dev] * n, slot_bytes_for(seg, cfg.stage1_codec, cfg.stage2_codec))
+    comm.set_timeout(timeout if timeout is not None else 3600.0)
+    outs = comm.all_reduce_host(flats, cfg, out_dtype=odt, outs=outs)
+    qdq = int(not cfg.stage1_codec.is_passthrough) + int(not cfg.stage2_codec.is_passthrough)
+    return CollectiveRun(
+        method="flash",
+        outputs=[o.reshape(shape) if o is not None else None for o in outs],
+        ledger=flash_ledger(n, seg, chunk // n, cfg.stage1_codec, cfg.stage2_codec),
+        reduce_steps=1,
+        gather_steps=1,
+        qdq_passes=qdq,
+        reduce_elems_per_rank=(n - 1) * seg,
+        gather_elems_per_rank=(n - 1) * seg,
+    )
+
+
+def _host_rank_tensors(tensors: Sequence) -> tuple[list, tuple, int]:
+    if len(tensors) == 0:
+        raise ProtocolError("need at least one rank tensor")
+    shape = tuple(tensors[0].shape) if hasattr(tensors[0], "shape") else (len(tensors[0]),)
+    flats = [as_host_tensor(t) for t in tensors]
+    m = flats[0].numel()
+    for r, f in enumerate(flats):
+        if f.numel() != m:
+            raise ProtocolError(f"rank {r} tensor length {f.numel()} != rank 0 length {m}")
+        if f.dtype != flats[0].dtype:
+            raise ProtocolError(f"rank {r} dtype {f.dtype} != rank 0 dtype {flats[0].dtype}")
+    if m == 0:
+        raise DomainError("rank tensors must be nonempty")
+    return flats, shape, m
 
 
 def all_reduce_exact(tensors: Sequence, topology: Optional[FabricTopology] = None,

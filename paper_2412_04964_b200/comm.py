@@ -264,6 +264,72 @@ class FlashComm:
             self.check()
         return list(outs)
 
+    def all_reduce_host(self, ins: Sequence[torch.Tensor], cfg, out_dtype: Optional[torch.dtype] = None,
+                        read_back: Optional[Sequence[bool]] = None,
+                        outs: Optional[Sequence[Optional[torch.Tensor]]] = None) -> list:
+        """Blocking all-reduce of one HOST tensor per rank (the reference's
+        arrays-in / new-arrays-out call): chunked H2D, the flash all-reduce per
+        chunk and chunked D2H overlap on the communicator's own streams
+        (fc_flash_all_reduce_host). Returns new pinned host tensors (None for
+        ranks with read_back[r] False), or fills `outs` (host tensors of n
+        elements, None to skip a rank). Pinned buffers copy at full PCIe rate."""
+        if self.rank is not None:
+            raise ConfigError("all_reduce_host needs a local communicator")
+        if len(ins) != self.world_size:
+            raise ProtocolError(f"expected {self.world_size} rank tensors, got {len(ins)}")
+        n = ins[0].numel()
+        dt = ins[0].dtype
+        for r, t in enumerate(ins):
+            if t.numel() != n:
+                raise ProtocolError(f"rank {r} tensor length {t.numel()} != rank 0 length {n}")
+            if t.dtype != dt:
+                raise ProtocolError(f"rank {r} dtype {t.dtype} != rank 0 dtype {dt}")
+            if t.is_cuda:
+                raise DomainError(f"rank {r} tensor must be a host tensor")
+            if not t.is_contiguous():
+                raise DomainError(f"rank {r} tensor must be contiguous")
+        odt = out_dtype or dt
+        N = self.world_size
+        if outs is None:
+            outs = [torch.empty(n, dtype=odt, pin_memory=True) if (read_back is None or read_back[r]) else None
+                    for r in range(N)]
+        else:
+            if len(outs) != N:
+                raise ProtocolError(f"expected {N} output tensors, got {len(outs)}")
+            for r, o in enumerate(outs):
+                if o is None:
+                    continue
+                if o.is_cuda or not o.is_contiguous() or o.numel() != n or o.dtype != odt:
+                    raise DomainError(f"rank {r} output must be a contiguous host {odt} tensor of {n} elements")
+            outs = list(outs)
+        arr = _ptr_array(N)
+        pin = arr(*[t.data_ptr() for t in ins])
+        pout = arr(*[o.data_ptr() if o is not None else None for o in outs])
+        _lib.check(_lib.lib().fc_flash_all_reduce_host(self._h, pin, pout, n, fc_dtype(dt), fc_dtype(odt),
+                                                       C.byref(self._cfg(cfg))))
+        return outs
+
+    def all_reduce_host_rank(self, tensor: torch.Tensor, cfg, out: Optional[torch.Tensor] = None,
+                             out_dtype: Optional[torch.dtype] = None, read_back: bool = True):
+        """Per-rank host-buffer form (IPC world): this rank's host tensor in,
+        a new (or the given `out`) host tensor out, chunked H2D / all-reduce /
+        D2H overlapped (fc_flash_all_reduce_host_rank). Blocking; every rank
+        calls it with the same numel / cfg / FC_OPT_HOST_CHUNK_BYTES."""
+        if self.rank is None:
+            raise ConfigError("all_reduce_host_rank needs an IPC communicator (from_process_group)")
+        if tensor.is_cuda or not tensor.is_contiguous():
+            raise DomainError("tensor must be a contiguous host tensor")
+        n = tensor.numel()
+        odt = out_dtype or tensor.dtype
+        if out is None and read_back:
+            out = torch.empty(n, dtype=odt, pin_memory=True)
+        if out is not None and (out.is_cuda or not out.is_contiguous() or out.numel() != n or out.dtype != odt):
+            raise DomainError(f"out must be a contiguous host {odt} tensor of {n} elements")
+        _lib.check(_lib.lib().fc_flash_all_reduce_host_rank(
+            self._h, tensor.data_ptr(), out.data_ptr() if out is not None else None, n, fc_dtype(tensor.dtype),
+            fc_dtype(odt), C.byref(self._cfg(cfg))))
+        return out
+
     def all_reduce(self, tensor: torch.Tensor, cfg, out: Optional[torch.Tensor] = None,
                    out_dtype: Optional[torch.dtype] = None, check: bool = False) -> torch.Tensor:
         """Per-rank form (IPC world): every rank calls with equal numel/cfg.

@@ -294,7 +294,15 @@ fc_status fc_comm_destroy(fc_comm* c) {
     if (c->opened[r] && c->blk[r]) cudaIpcCloseMemHandle(c->blk[r]);
     if (c->scratch[r]) cudaFree(c->scratch[r]);
     if (c->ev[r]) cudaEventDestroy(c->ev[r]);
+    if (c->hs_in[r] || c->hs_out[r] || c->hs_h2d[r]) cudaSetDevice(c->devices[r]);
+    if (c->hs_in[r]) cudaFree(c->hs_in[r]);
+    if (c->hs_out[r]) cudaFree(c->hs_out[r]);
+    if (c->hs_h2d[r]) cudaStreamDestroy(c->hs_h2d[r]);
+    if (c->hs_comp[r]) cudaStreamDestroy(c->hs_comp[r]);
+    if (c->hs_d2h[r]) cudaStreamDestroy(c->hs_d2h[r]);
   }
+  for (cudaEvent_t e : c->hs_ev)
+    if (e) cudaEventDestroy(e);
   cudaGetLastError();
   delete c;
   return FC_OK;
@@ -319,6 +327,7 @@ fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
     case FC_OPT_PHASES: c->phases = value & 7; break;
     case FC_OPT_ONESHOT: c->oneshot = value != 0; break;
     case FC_OPT_ROLE_WEIGHTS: c->role_weights = value; break;
+    case FC_OPT_HOST_CHUNK_BYTES: c->host_chunk_bytes = std::max<int64_t>(0, value); break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
   return FC_OK;
@@ -341,6 +350,7 @@ fc_status fc_comm_get_option(fc_comm* c, int32_t option, int64_t* value) {
     case FC_OPT_PHASES: *value = c->phases; break;
     case FC_OPT_ONESHOT: *value = c->oneshot; break;
     case FC_OPT_ROLE_WEIGHTS: *value = c->role_weights; break;
+    case FC_OPT_HOST_CHUNK_BYTES: *value = c->host_chunk_bytes; break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
   return FC_OK;
@@ -382,6 +392,8 @@ namespace {
         return fail(FC_ERR_CONFIG, "output dtype must equal the input dtype or be float32");    \
     }                                                                                            \
   }()
+
+inline bool dispatch_ok(int in_dt, int out_dt) { return in_dt == out_dt || out_dt == FC_DTYPE_F32; }
 
 inline fc_status check_call(const fc_comm* c, int64_t n, int in_dt, int out_dt, const fc_flash_cfg* cfg) {
   if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
@@ -452,6 +464,188 @@ fc_status fc_comm_check(fc_comm* c, int32_t rank) {
   }
   if (first != FC_OK) g_err = msg;
   return first;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// host-buffer pipeline (fc_flash_all_reduce_host)
+
+namespace {
+
+// grow-only device staging of `bytes` on rank r's device
+fc_status ensure_stage(fc_comm* c, int r, void** buf, int64_t* have, int64_t bytes) {
+  if (*have >= bytes) return FC_OK;
+  FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+  if (*buf) {
+    FC_CUDA_TRY(cudaDeviceSynchronize());
+    FC_CUDA_TRY(cudaFree(*buf));
+    *buf = nullptr;
+    *have = 0;
+  }
+  FC_CUDA_TRY(cudaMalloc(buf, (size_t)bytes));
+  *have = bytes;
+  return FC_OK;
+}
+
+// copy the rows of one chunk: element span [lo, hi) of every segment j of a
+// rank tensor of n elements (segment j starts at j*seg; the tail past n is padding)
+fc_status copy_rows(void* dst, const void* src, int64_t n, int64_t seg, int world, int64_t lo, int64_t hi, int e,
+                    cudaMemcpyKind kind, cudaStream_t st) {
+  int full = 0;  // rows wholly inside the tensor
+  while (full < world && (int64_t)full * seg + hi <= n) ++full;
+  const size_t pitch = (size_t)(seg * e);
+  if (full > 0)
+    FC_CUDA_TRY(cudaMemcpy2DAsync((char*)dst + lo * e, pitch, (const char*)src + lo * e, pitch, (size_t)((hi - lo) * e),
+                                  (size_t)full, kind, st));
+  if (full < world) {
+    const int64_t a = (int64_t)full * seg + lo, b = std::min(n, (int64_t)full * seg + hi);
+    if (b > a) FC_CUDA_TRY(cudaMemcpyAsync((char*)dst + a * e, (const char*)src + a * e, (size_t)((b - a) * e), kind, st));
+  }
+  return FC_OK;
+}
+
+// only_rank >= 0: IPC world, this process is that rank (its buffers at index only_rank)
+fc_status host_pipeline(fc_comm* c, const void* const* hin, void* const* hout, int64_t n, int in_dt, int out_dt,
+                        const fc_flash_cfg* cfg, int only_rank) {
+  const int N = c->world;
+  auto active = [&](int r) { return only_rank < 0 || r == only_rank; };
+  const int ein = dtype_size(in_dt), eout = dtype_size(out_dt);
+  int lead[kMaxRanks];  // the first active rank on each rank's device owns that device's streams
+  for (int r = 0; r < N; ++r) {
+    lead[r] = r;
+    for (int q = 0; q < r; ++q)
+      if (active(q) && c->devices[q] == c->devices[r]) {
+        lead[r] = q;
+        break;
+      }
+  }
+  for (int r = 0; r < N; ++r) {
+    if (!active(r)) continue;
+    FC_TRY(ensure_stage(c, r, &c->hs_in[r], &c->hs_in_bytes[r], n * ein));
+    FC_TRY(ensure_stage(c, r, &c->hs_out[r], &c->hs_out_bytes[r], n * eout));
+    if (lead[r] == r && !c->hs_h2d[r]) {
+      FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+      FC_CUDA_TRY(cudaStreamCreateWithFlags(&c->hs_h2d[r], cudaStreamNonBlocking));
+      FC_CUDA_TRY(cudaStreamCreateWithFlags(&c->hs_comp[r], cudaStreamNonBlocking));
+      FC_CUDA_TRY(cudaStreamCreateWithFlags(&c->hs_d2h[r], cudaStreamNonBlocking));
+    }
+  }
+  const void* din[kMaxRanks] = {nullptr};
+  void* dout[kMaxRanks] = {nullptr};
+  cudaStream_t st[kMaxRanks] = {nullptr};
+  for (int r = 0; r < N; ++r) {
+    if (!active(r)) continue;
+    din[r] = c->hs_in[r];
+    dout[r] = c->hs_out[r];
+    st[r] = c->hs_comp[lead[r]];
+  }
+  // chunk span: a multiple of the plan unit (group lcm, and the tile for the tiled
+  // kernels) so every chunk run quantizes the same groups as one whole call
+  const int64_t seg = (n + N - 1) / N;
+  int64_t unit = std::lcm(group_of(cfg->stage1), group_of(cfg->stage2));
+  if (fast_group(cfg->stage1) && fast_group(cfg->stage2)) unit = std::lcm(unit, (int64_t)kTileElems);
+  // 12 MiB of H2D per rank per chunk: large enough for full-rate 2-D copies, small enough that
+  // the tail after the last H2D (its all-reduce + D2H) stays short (tools/e2e_probe.py)
+  const int64_t target = c->host_chunk_bytes > 0 ? c->host_chunk_bytes : (int64_t)12 << 20;
+  int64_t span = std::max<int64_t>(1, target / ((int64_t)N * ein));
+  span = std::max(unit, span / unit * unit);
+  if (N == 1) span = seg;
+  const int64_t chunks = (seg + span - 1) / span;
+  const size_t need = (size_t)(chunks * N * 2);
+  if (c->hs_ev.size() < need) {
+    const size_t have = c->hs_ev.size();
+    c->hs_ev.resize(need, nullptr);
+    for (size_t i = have; i < need; ++i) {
+      const int r = (int)((i / 2) % N);
+      FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+      FC_CUDA_TRY(cudaEventCreateWithFlags(&c->hs_ev[i], cudaEventDisableTiming));
+    }
+  }
+  // events are created on the device of rank (i / 2) % N; the layout is fixed per comm
+  auto ev = [&](int64_t k, int r, int which) { return c->hs_ev[(size_t)((k * N + r) * 2 + which)]; };
+  fc_status status = FC_OK;
+  for (int64_t k = 0; k < chunks && status == FC_OK; ++k) {
+    const int64_t lo = k * span, hi = std::min(seg, lo + span);
+    for (int r = 0; r < N; ++r) {
+      if (!active(r)) continue;
+      FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+      FC_TRY(copy_rows(c->hs_in[r], hin[r], n, seg, N, lo, hi, ein, cudaMemcpyHostToDevice, c->hs_h2d[lead[r]]));
+      FC_CUDA_TRY(cudaEventRecord(ev(k, r, 0), c->hs_h2d[lead[r]]));
+    }
+    // every rank's chunk must have landed before any rank's run of it
+    for (int r = 0; r < N; ++r) {
+      if (lead[r] != r || !active(r)) continue;
+      FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+      for (int q = 0; q < N; ++q) {
+        if (!active(q)) continue;
+        bool last_of_dev = true;  // one wait per (device, source device): the last copy queued there
+        for (int q2 = q + 1; q2 < N; ++q2) last_of_dev &= lead[q2] != lead[q];
+        if (last_of_dev) FC_CUDA_TRY(cudaStreamWaitEvent(c->hs_comp[r], ev(k, q, 0), 0));
+      }
+    }
+    if (N == 1) {
+      status = FC_DISPATCH2(in_dt, out_dt, identity_typed, din[0], dout[0], n, c->devices[0], st[0]);
+    } else {
+      c->span_lo = lo;
+      c->span_hi = hi;
+      if (only_rank >= 0) FC_CUDA_TRY(cudaSetDevice(c->devices[only_rank]));
+      status = FC_DISPATCH_RUN(in_dt, out_dt, c, din, dout, n, cfg, st, only_rank);
+      c->span_lo = 0;
+      c->span_hi = -1;
+    }
+    if (status != FC_OK) break;
+    for (int r = 0; r < N; ++r) {
+      if (!active(r) || !hout[r]) continue;
+      FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+      FC_CUDA_TRY(cudaEventRecord(ev(k, r, 1), st[r]));
+      FC_CUDA_TRY(cudaStreamWaitEvent(c->hs_d2h[lead[r]], ev(k, r, 1), 0));
+      FC_TRY(copy_rows(hout[r], c->hs_out[r], n, seg, N, lo, hi, eout, cudaMemcpyDeviceToHost, c->hs_d2h[lead[r]]));
+    }
+  }
+  for (int r = 0; r < N; ++r) {
+    if (lead[r] != r || !active(r)) continue;
+    FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+    FC_CUDA_TRY(cudaStreamSynchronize(c->hs_h2d[r]));
+    FC_CUDA_TRY(cudaStreamSynchronize(c->hs_comp[r]));
+    FC_CUDA_TRY(cudaStreamSynchronize(c->hs_d2h[r]));
+  }
+  return status;
+}
+
+}  // namespace
+
+extern "C" {
+
+fc_status fc_flash_all_reduce_host(fc_comm* c, const void* const* host_ins, void* const* host_outs, int64_t n,
+                                   int32_t in_dtype, int32_t out_dtype, const fc_flash_cfg* cfg) {
+  FC_TRY(check_call(c, n, in_dtype, out_dtype, cfg));
+  if (c->ipc) return fail(FC_ERR_CONFIG, "fc_flash_all_reduce_host needs a local communicator");
+  if (!host_ins || !host_outs) return fail(FC_ERR_DOMAIN, "NULL buffer list");
+  for (int r = 0; r < c->world; ++r)
+    if (!host_ins[r]) return fail(FC_ERR_DOMAIN, "NULL input buffer for rank %d", r);
+  if (c->world > 1 && !dispatch_ok(in_dtype, out_dtype))
+    return fail(FC_ERR_CONFIG, "output dtype must equal the input dtype or be float32");
+  FC_TRY(host_pipeline(c, host_ins, host_outs, n, in_dtype, out_dtype, cfg, -1));
+  return fc_comm_check(c, -1);
+}
+
+fc_status fc_flash_all_reduce_host_rank(fc_comm* c, const void* host_in, void* host_out, int64_t n, int32_t in_dtype,
+                                        int32_t out_dtype, const fc_flash_cfg* cfg) {
+  FC_TRY(check_call(c, n, in_dtype, out_dtype, cfg));
+  if (!c->ipc) return fail(FC_ERR_CONFIG, "fc_flash_all_reduce_host_rank needs an IPC communicator");
+  if (!host_in) return fail(FC_ERR_DOMAIN, "NULL input buffer");
+  if (c->world > 1 && !dispatch_ok(in_dtype, out_dtype))
+    return fail(FC_ERR_CONFIG, "output dtype must equal the input dtype or be float32");
+  const int r = c->my_rank;
+  for (int p = 0; p < c->world; ++p)
+    if (!c->blk[p]) return fail(FC_ERR_PROTOCOL, "rank %d has not mapped rank %d (call fc_comm_ipc_open)", r, p);
+  const void* ins[kMaxRanks] = {nullptr};
+  void* outs[kMaxRanks] = {nullptr};
+  ins[r] = host_in;
+  outs[r] = host_out;
+  FC_TRY(host_pipeline(c, ins, outs, n, in_dtype, out_dtype, cfg, r));
+  return fc_comm_check(c, r);
 }
 
 fc_status fc_comm_slot(fc_comm* c, int32_t rank, int32_t stage, int32_t src, void* dst, fc_layout* layout) {

@@ -1,6 +1,8 @@
 // Communicator state shared by the C-ABI translation units.
 #pragma once
 
+#include <vector>
+
 #include <cuda_runtime.h>
 
 #include <string>
@@ -38,6 +40,17 @@ struct fc_comm {
   int64_t role_weights = 3 | (2 << 8) | (3 << 16);  // fused stream kernel: scatter | reduce<<8 | gather<<16  // measurement: phase mask of the one-GPU split path (0 = all)
   int64_t reduce_stages = 0, q_stages = 0, d_stages = 0, ctas_per_sm = 0;  // 0 = auto
   int64_t launches = 0, last_launches = 0;  // kernels launched by the last call
+  // segment-relative element span [span_lo, span_hi) the next run processes (-1: whole segment);
+  // set only by the host-buffer pipeline around each of its chunk runs
+  int64_t span_lo = 0, span_hi = -1;
+  // host-buffer pipeline (fc_flash_all_reduce_host): device staging per rank, copy/compute
+  // streams per device (owned by the device's first rank), events per (chunk, rank)
+  int64_t host_chunk_bytes = 0;  // H2D bytes per rank per chunk (0 = auto)
+  void* hs_in[kMaxRanks] = {nullptr};
+  void* hs_out[kMaxRanks] = {nullptr};
+  int64_t hs_in_bytes[kMaxRanks] = {0}, hs_out_bytes[kMaxRanks] = {0};
+  cudaStream_t hs_h2d[kMaxRanks] = {nullptr}, hs_comp[kMaxRanks] = {nullptr}, hs_d2h[kMaxRanks] = {nullptr};
+  std::vector<cudaEvent_t> hs_ev;  // [chunk][rank][in, out]
   // last call (debug export)
   fc_codec last_c1{}, last_c2{};
   int64_t last_R = 0, last_sub_len = 0;
