@@ -399,6 +399,276 @@ __device__ __forceinline__ void q_role(const FlashArgs& a, uint32_t sbase, int S
   }
 }
 
+// ------------------------------------------------------------------ group-per-lane quantize role
+
+// g = 128 quantize with one lane per whole group (k_qstream_gpl). The
+// 32-element lane layout above spreads a group over 4 lanes, so every lane
+// repeats the group's statistics tail, the float64 scale and the zero point
+// (SIMT: one pass computes 8 groups per warp); with one lane per group the
+// same pass serves 32 groups, and no shuffles are needed. A lane reads its
+// 256-B group as 16 vectors in XOR-swizzled order (vector k ^ (lane & 7) at
+// step k: the 8 lanes of each quarter-warp hit 8 distinct bank groups), keeps
+// the 64 input words in registers, and undoes the swizzle on the 16 (INT4) /
+// 32 (INT8) code words with three conditional-swap layers. Same numerics as
+// lane_quantize_fast (identical group_params, per-element rounding, packing).
+constexpr int kGplG = 128;
+constexpr int kGplWarps = 4;                         // consumer warps
+constexpr int kGplThreads = (kGplWarps + 1) * 32;    // + the producer warp
+constexpr int kGplWpt = kTileElems / (32 * kGplG);   // warps per tile (2)
+constexpr int kGplSlots = kGplWarps / kGplWpt;       // tiles in flight across the consumers (2)
+
+// element e (0..7) of an 8-element chunk held as 4 packed 16-bit pairs, as fp32 bits
+template <typename Tin>
+__device__ __forceinline__ uint32_t chunk_elem(const uint32_t x[4], int e) {
+  const uint32_t w = x[e >> 1];
+  if constexpr (std::is_same<Tin, __nv_bfloat16>::value) {
+    return (e & 1) ? (w & 0xFFFF0000u) : (w << 16);
+  } else {
+    const __half h = __ushort_as_half((unsigned short)((e & 1) ? (w >> 16) : (w & 0xFFFFu)));
+    return __float_as_uint(__half2float(h));
+  }
+}
+template <typename Tin>
+__device__ __forceinline__ uint64_t chunk_pair(const uint32_t x[4], int a, int b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "r"(chunk_elem<Tin>(x, a)), "r"(chunk_elem<Tin>(x, b)));
+  return r;
+}
+
+// offset-binary codes of one 8-element chunk (1 word INT4, 2 words INT8); requires g.normal
+template <class Spec, typename Tin>
+__device__ __forceinline__ void chunk_codes_packed(const uint32_t x[4], const GroupQ& g, uint32_t qmax, uint32_t* w) {
+  const uint64_t R2 = f2_splat(g.r), NS2 = f2_splat(-g.s), C2 = f2_splat(12582912.0f);
+  const uint32_t Z2 = g.z * 0x00010001u, Q2 = qmax * 0x00010001u;
+  auto code_pair = [&](int a, int b) -> uint32_t {
+    const uint64_t X = chunk_pair<Tin>(x, a, b);
+    const uint64_t T = f2_mul(X, R2);
+    const uint64_t Q = f2_fma(f2_fma(T, NS2, X), R2, T);
+    const uint64_t Y = Spec::CEIL ? f2_add_rp(Q, C2) : f2_add(Q, C2);
+    uint32_t ya, yb;
+    f2_bits(Y, ya, yb);
+    const uint32_t p = __byte_perm(ya, yb, 0x5410);
+    const uint32_t c = __viaddmax_s16x2(p, Z2, 0u);
+    return __vimin3_s16x2(c, Q2, Q2);
+  };
+  if constexpr (Spec::SB == 4) {
+    w[0] = code_pair(0, 4) + (code_pair(1, 5) << 4) + (code_pair(2, 6) << 8) + (code_pair(3, 7) << 12);
+  } else {
+    w[0] = code_pair(0, 2) + (code_pair(1, 3) << 8);
+    w[1] = code_pair(4, 6) + (code_pair(5, 7) << 8);
+  }
+}
+
+// the float-clamp path of lane_codes (fc_common.cuh) for one chunk: |x/s| may exceed 16 bits
+template <class Spec, typename Tin>
+__device__ __forceinline__ void chunk_codes_clamped(const uint32_t x[4], float s, int z, int qmax, uint32_t* w) {
+  const float r = __frcp_rn(s);
+  const float C0 = 12582912.0f;
+  const float lob = -(float)z, hib = (float)(qmax - z);
+  const int zb = z - 0x4B400000;
+  w[0] = 0;
+  if constexpr (Spec::SB == 8) w[1] = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float xv = __uint_as_float(chunk_elem<Tin>(x, e));
+    const float t = xv * r;
+    const float q1 = fmaf(fmaf(-t, s, xv), r, t);
+    const float qc = fminf(fmaxf(q1, lob), hib);
+    const float y = Spec::CEIL ? __fadd_ru(qc, C0) : __fadd_rn(qc, C0);
+    const uint32_t code = (uint32_t)(__float_as_int(y) + zb);
+    if constexpr (Spec::SB == 4)
+      w[0] |= code << (4 * e);
+    else
+      w[e >> 2] |= code << (8 * (e & 3));
+  }
+}
+
+// 16-bit packed min / max (NaN-propagating), bf16x2 or f16x2
+template <typename Tin>
+__device__ __forceinline__ uint32_t h2min(uint32_t a, uint32_t b) {
+  uint32_t r;
+  if constexpr (std::is_same<Tin, __nv_bfloat16>::value)
+    asm("min.NaN.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  else
+    asm("min.NaN.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+template <typename Tin>
+__device__ __forceinline__ uint32_t h2max(uint32_t a, uint32_t b) {
+  uint32_t r;
+  if constexpr (std::is_same<Tin, __nv_bfloat16>::value)
+    asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  else
+    asm("max.NaN.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+template <typename Tin>
+__device__ __forceinline__ float h_lo(uint32_t w) {
+  if constexpr (std::is_same<Tin, __nv_bfloat16>::value) return __uint_as_float(w << 16);
+  else return __half2float(__ushort_as_half((unsigned short)(w & 0xFFFFu)));
+}
+template <typename Tin>
+__device__ __forceinline__ float h_hi(uint32_t w) {
+  if constexpr (std::is_same<Tin, __nv_bfloat16>::value) return __uint_as_float(w & 0xFFFF0000u);
+  else return __half2float(__ushort_as_half((unsigned short)(w >> 16)));
+}
+
+// words w[k * CWPC + i] of chunk k -> chunk k ^ m (three conditional-swap layers)
+template <int NC, int CWPC>
+__device__ __forceinline__ void unswizzle_chunks(uint32_t* w, int m) {
+#pragma unroll
+  for (int b = 1; b < 8; b <<= 1) {
+    const bool sw = (m & b) != 0;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      if (k & b) continue;
+#pragma unroll
+      for (int i = 0; i < CWPC; ++i) {
+        const uint32_t u = w[k * CWPC + i], v = w[(k ^ b) * CWPC + i];
+        w[k * CWPC + i] = sw ? v : u;
+        w[(k ^ b) * CWPC + i] = sw ? u : v;
+      }
+    }
+  }
+}
+
+template <typename Tin, class S1, class Iter>
+__device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
+  static_assert(sizeof(Tin) == 2, "16-bit inputs");
+  constexpr uint32_t STAGE = kTileElems * 2;
+  constexpr int NC = kGplG / 8;      // 8-element chunks per group
+  constexpr int CWPC = S1::SB / 4;   // code words per chunk
+  const uint32_t full0 = sbase + S * STAGE, empty0 = full0 + 8 * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kGplWpt);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kGplWarps) {  // producer warp: one lane issues the bulk copies (as in q_role)
+    if (lane == 0) {
+      int st = 0, k = 0, cy = -1;
+      uint32_t ph = 0;
+      QJob<Tin> jb;
+      for (Iter it = it0; it.ok(); it.next(), ++k) {
+        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        if (it.y != cy) {
+          jb = qjob<Tin>(a, it.y);
+          cy = it.y;
+        }
+        const int64_t e0 = (int64_t)it.t * kTileElems;
+        const uint32_t bytes = (uint32_t)(tile_valid(a.sub_len, jb.limit, e0) * 2) & ~15u;
+        mbar_arrive_expect_tx(full0 + 8 * st, bytes);
+        if (bytes) bulk_g2s(sbase + st * STAGE, jb.src + e0, bytes, full0 + 8 * st);
+        ring_next(st, ph, S);
+      }
+    }
+    return;
+  }
+  const int slot = warp / kGplWpt, part = warp % kGplWpt;
+  const int m = lane & 7;
+  const int gi = part * 32 + lane;  // this lane's group within a tile
+  int st = 0, cy = -1, k = 0;
+  uint32_t ph = 0;
+  QJob<Tin> jb;
+  for (Iter it = it0; it.ok(); it.next(), ++k) {
+    if (k % kGplSlots == slot) {  // S is a multiple of the slot count: a slot always meets its own stages
+      if (it.y != cy) {
+        jb = qjob<Tin>(a, it.y);
+        cy = it.y;
+      }
+      const int64_t p0 = (int64_t)it.t * kTileElems + gi * kGplG;
+      const bool whole = p0 + kGplG <= a.sub_len && p0 + kGplG <= jb.limit;
+      mbar_wait(full0 + 8 * st, ph);
+      if (__all_sync(0xffffffffu, whole)) {
+        const uint32_t gb = sbase + st * STAGE + gi * (kGplG * 2);
+        uint32_t x[NC][4];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const uint4 u = lds128_(gb + 16 * (c ^ m));
+          x[c][0] = u.x;
+          x[c][1] = u.y;
+          x[c][2] = u.z;
+          x[c][3] = u.w;
+        }
+        // group bounds in 16-bit packed arithmetic (exact), then fp32
+        uint32_t mn, mx;
+        if constexpr (S1::SYM) {
+          mx = x[0][0] & 0x7FFF7FFFu;
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (c | i) mx = h2max<Tin>(mx, x[c][i] & 0x7FFF7FFFu);
+          mn = mx;
+        } else {
+          mn = h2min<Tin>(x[0][0], x[0][1]);
+          mx = h2max<Tin>(x[0][0], x[0][1]);
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (c > 0 || i > 1) {
+                mn = h2min<Tin>(mn, x[c][i]);
+                mx = h2max<Tin>(mx, x[c][i]);
+              }
+        }
+        float hi = fmax_nan(h_lo<Tin>(mx), h_hi<Tin>(mx));
+        float lo = S1::SYM ? -hi : fmin_nan(h_lo<Tin>(mn), h_hi<Tin>(mn));
+        const bool bad = !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
+        GroupQ g;
+        group_params<S1>(a.c1, lo, hi, g);
+        if (bad) g.z = S1::SYM ? g.z : 0u;
+        const uint32_t qmax = (1u << a.c1.bits) - 1u;
+        uint32_t w[NC * CWPC];
+        if (g.normal) {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) chunk_codes_packed<S1, Tin>(x[c], g, qmax, w + c * CWPC);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax, w + c * CWPC);
+        }
+        // every shared load has been consumed (the codes depend on all of them)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        if constexpr (S1::SYM) {
+          const uint32_t xr = rep_xor(a.c1);
+#pragma unroll
+          for (int i = 0; i < NC * CWPC; ++i) w[i] ^= xr;
+        }
+        unswizzle_chunks<NC, CWPC>(w, m);
+        uint8_t* cd = jb.dst + p0 * S1::SB / 8;
+#pragma unroll
+        for (int v = 0; v < NC * CWPC / 4; ++v)
+          *reinterpret_cast<uint4*>(cd + 16 * v) = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+        const int64_t grp = p0 >> a.c1.gshift;
+        *reinterpret_cast<unsigned short*>(jb.dst + a.c1.scales_off + 2 * grp) = g.s16;
+        if constexpr (!S1::SYM) jb.dst[a.c1.zeros_off + grp] = (uint8_t)g.z;
+        if (bad && jb.err) atomicOr(jb.err, jb.ecode);
+      } else {
+        // ragged tail: the 32-element lane codec over this warp's 4096 elements, 1024 at a time
+        bool bad = false;
+        for (int sub = 0; sub < kGplG / 32; ++sub) {
+          const int64_t q0 = (int64_t)it.t * kTileElems + part * (32 * kGplG) + sub * (32 * kLaneElems) + lane * kLaneElems;
+          const int nvalid = lane_valid(a.sub_len, q0);
+          PackedLane<Tin> L;
+          load_lane_src(jb.src, q0, jb.limit, nvalid, L);
+          LaneQuant<8> q;
+          bad |= quantize_lane<S1>(a.c1, L, nvalid, q);
+          store_codes<S1>(a.c1, jb.dst, q0, nvalid, q, lane);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        if (bad && jb.err) atomicOr(jb.err, jb.ecode);
+      }
+    }
+    ring_next(st, ph, S);
+  }
+}
+
 // ------------------------------------------------------------------ reduce role
 
 // owner j = rank_lo + y: own segment QDQ + N-1 received pieces -> fp32 sum
@@ -519,10 +789,20 @@ __device__ __forceinline__ void r_role(const FlashArgs& a, uint32_t sbase, int S
     {
       const CodeDst cd = code_dst<S2>(a.c2, p0, nvalid, lane);
       const int64_t slot_off = (int64_t)(a.world + j) * a.slot_bytes;  // gather slot [j] (gath_slot)
-      for (int p = j + 1;; ++p) {  // every peer's gather slot [j]
-        if (p == a.world) p = 0;
-        if (p == j) break;
-        store_codes_at<S2>(a.blk[p] + slot_off, cd, q2);
+      // every peer's gather slot [j]: static peer indices keep the slot bases
+      // constant-bank operands, and the peer test joins the store predicates
+      // (no per-peer branch, so the stores stay in warp-uniform code)
+      const uint4 cw = make_uint4(q2.w[0], q2.w[1], q2.w[2], q2.w[3]);
+      const int64_t oc = slot_off + cd.codes, os = slot_off + cd.scale, oz = slot_off + cd.zero;
+#pragma unroll
+      for (int p = 0; p < kMaxRanks; ++p) {
+        const bool peer = p < a.world && p != j;
+        uint8_t* b = a.blk[p];
+        st_v4_if(b + oc, cw, peer && cd.any);
+        if constexpr (S2::SB == 8)
+          st_v4_if(b + oc + 16, make_uint4(q2.w[4], q2.w[5], q2.w[6], q2.w[7]), peer && cd.any);
+        st_u16_if(b + os, __half_as_ushort(q2.s16), peer && cd.meta);
+        if constexpr (!S2::SYM) st_u8_if(b + oz, q2.z8, peer && cd.meta);
       }
     }
     LaneCodes<8> L2;
@@ -752,6 +1032,14 @@ __global__ void __launch_bounds__(kStreamThreads) k_qstream(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
   q_role<Tin, S1, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+}
+
+// g = 128 scatter / codec quantize, one lane per group (q_role_gpl)
+template <typename Tin, class S1>
+__global__ void __launch_bounds__(kGplThreads, 3) k_qstream_gpl(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
+  q_role_gpl<Tin, S1>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
 template <typename Tin, typename Tout, class S1, class S2>

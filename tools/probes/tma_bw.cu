@@ -49,6 +49,27 @@ __global__ void k_copy(const uint4* src, uint4* dst, size_t n16) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) dst[i] = __ldg(src + i);
 }
 
+// write probes: plain 16-B stores vs bulk (TMA) shared->global stores of whole tiles
+__global__ void k_stg(uint4* dst, size_t n16) {
+  const uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x) dst[i] = v;
+}
+__global__ void k_bulk_store(uint8_t* dst, size_t bytes, int tile, int depth) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  for (int i = threadIdx.x * 16; i < tile; i += blockDim.x * 16) *reinterpret_cast<uint4*>(smem + i) = make_uint4(i, 1, 2, 3);
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int items = (int)(bytes / tile);
+  int n = 0;
+  for (int i = blockIdx.x; i < items; i += gridDim.x) {
+    bulk_s2g(dst + (size_t)i * tile, smem_u32(smem), tile);
+    bulk_commit();
+    if (++n >= depth) bulk_wait_read<4>();
+  }
+  bulk_wait<0>();
+}
+
 int main() {
   const size_t bytes = 1ull << 30;
   uint8_t *src, *dst; uint32_t* sink;
@@ -73,5 +94,14 @@ int main() {
   }
   float ms = timeit([&] { k_copy<<<sms * 4, 1024>>>((const uint4*)src, (uint4*)dst, bytes / 16); });
   printf("{\"probe\":\"copy\",\"GBs\":%.0f}\n", 2.0 * bytes / ms / 1e6);
+  for (int bl : {1, 2, 4, 8}) {
+    float w = timeit([&] { k_stg<<<sms * bl, 1024>>>((uint4*)dst, bytes / 16); });
+    printf("{\"probe\":\"stg_write\",\"blocks_per_sm\":%d,\"GBs\":%.0f}\n", bl, bytes / w / 1e6);
+  }
+  cudaFuncSetAttribute(k_bulk_store, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int tile : {4096, 16384, 32768}) for (int cps : {1, 2, 4, 8}) {
+    float w = timeit([&] { k_bulk_store<<<sms * cps, 128, tile>>>(dst, bytes, tile, 8); });
+    printf("{\"probe\":\"bulk_write\",\"tile\":%d,\"ctas_per_sm\":%d,\"GBs\":%.0f}\n", tile, cps, bytes / w / 1e6);
+  }
   printf("err=%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }
