@@ -789,20 +789,10 @@ __device__ __forceinline__ void r_role(const FlashArgs& a, uint32_t sbase, int S
     {
       const CodeDst cd = code_dst<S2>(a.c2, p0, nvalid, lane);
       const int64_t slot_off = (int64_t)(a.world + j) * a.slot_bytes;  // gather slot [j] (gath_slot)
-      // every peer's gather slot [j]: static peer indices keep the slot bases
-      // constant-bank operands, and the peer test joins the store predicates
-      // (no per-peer branch, so the stores stay in warp-uniform code)
-      const uint4 cw = make_uint4(q2.w[0], q2.w[1], q2.w[2], q2.w[3]);
-      const int64_t oc = slot_off + cd.codes, os = slot_off + cd.scale, oz = slot_off + cd.zero;
-#pragma unroll
-      for (int p = 0; p < kMaxRanks; ++p) {
-        const bool peer = p < a.world && p != j;
-        uint8_t* b = a.blk[p];
-        st_v4_if(b + oc, cw, peer && cd.any);
-        if constexpr (S2::SB == 8)
-          st_v4_if(b + oc + 16, make_uint4(q2.w[4], q2.w[5], q2.w[6], q2.w[7]), peer && cd.any);
-        st_u16_if(b + os, __half_as_ushort(q2.s16), peer && cd.meta);
-        if constexpr (!S2::SYM) st_u8_if(b + oz, q2.z8, peer && cd.meta);
+      for (int p = j + 1;; ++p) {  // every peer's gather slot [j], starting after the owner
+        if (p == a.world) p = 0;
+        if (p == j) break;
+        store_codes_at<S2>(a.blk[p] + slot_off, cd, q2);
       }
     }
     LaneCodes<8> L2;

@@ -113,3 +113,57 @@ def test_known_answers():
     q = fc.quantize(torch.tensor([-2.0, 2.0], device="cuda"), fc.CodecConfig(bits=4, group_size=2))
     assert orc.unpack(q.codes.cpu().numpy(), 2, 4).tolist() == [0, 15]
     assert int(q.zeros[0]) == 8
+
+
+def _adversarial(n, dtype, seed):
+    """Groups that take every branch of the lane codecs: a large offset with a
+    tiny spread (|x/s| >= 2^14: the float-clamp path), constant groups (scale
+    floor), fp16-overflowing ranges (scale 65504), tiny values (floor bump),
+    signed zeros, next to ordinary groups inside the same warp."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(n).astype(np.float32)
+    g = 128
+    for k in range(n // g):
+        kind = k % 8
+        sl = slice(k * g, (k + 1) * g)
+        if kind == 1:
+            x[sl] = 1000.0 + rng.standard_normal(g).astype(np.float32) * 0.01
+        elif kind == 2:
+            x[sl] = -3.5
+        elif kind == 3:
+            x[sl] = rng.uniform(-60000, 60000, g).astype(np.float32) * (1e5 if dtype == torch.bfloat16 else 1.0)
+        elif kind == 4:
+            x[sl] = rng.standard_normal(g).astype(np.float32) * 1e-9
+        elif kind == 5:
+            x[sl] = np.where(rng.random(g) < 0.5, -0.0, 0.0).astype(np.float32)
+        elif kind == 6:
+            x[sl] = -77.0 - np.abs(rng.standard_normal(g).astype(np.float32)) * 1e-3
+    return torch.from_numpy(x).to(dtype)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("bits,g,sym,rnd", [(4, 128, False, "nearest-even"), (8, 128, False, "nearest-even"),
+                                            (4, 128, True, "nearest-even"), (4, 128, False, "ceil"),
+                                            (8, 128, True, "ceil"), (4, 64, False, "nearest-even")])
+def test_codec_adversarial_groups_vs_oracle(dtype, bits, g, sym, rnd):
+    n = 4 * 8192 + 3 * 128 + 40  # whole tiles plus a ragged tail tile
+    t = _adversarial(n, dtype, seed=bits + g)
+    xr = t.float().numpy()
+    cfg = fc.CodecConfig(bits=bits, group_size=g, symmetric=sym, rounding=rnd)
+    q = fc.quantize(t.cuda(), cfg)
+    oq = orc.quantize(xr, orc.Codec(bits=bits, group_size=g, symmetric=sym, rounding=rnd))
+    assert q.to_bytes() == oq.wire_bytes()
+    d = fc.dequantize(q, dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(d.view(np.uint32), orc.dequantize(oq).view(np.uint32))
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_flash_adversarial_groups_vs_oracle(bits):
+    n, m = 4, 4 * (2 * 8192 + 256)
+    ts = [_adversarial(m, torch.bfloat16, seed=10 * r + bits) * (1 + r) for r in range(n)]
+    ts = [t.to(torch.bfloat16) for t in ts]
+    xr = [t.float().numpy() for t in ts]
+    ref = orc.flash_all_reduce(xr, orc.Codec(bits=bits), orc.Codec(bits=bits)).outputs[0]
+    run = fc.flash_all_reduce([t.cuda() for t in ts], fc.FlashConfig.from_bits(bits), out_dtype=torch.float32)
+    for o in run.outputs:
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), ref.view(np.uint32))
