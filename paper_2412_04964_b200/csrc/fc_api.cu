@@ -323,7 +323,7 @@ fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
     case FC_OPT_SCATTER_STAGES: c->q_stages = std::max<int64_t>(0, std::min<int64_t>(8, value)); break;
     case FC_OPT_GATHER_STAGES: c->d_stages = std::max<int64_t>(0, std::min<int64_t>(12, value)); break;
     case FC_OPT_CTAS_PER_SM: c->ctas_per_sm = std::max<int64_t>(0, std::min<int64_t>(16, value)); break;
-    case FC_OPT_STREAM_MASK: c->stream_mask = value & 63; break;
+    case FC_OPT_STREAM_MASK: c->stream_mask = value & 255; break;
     case FC_OPT_PHASES: c->phases = value & 7; break;
     case FC_OPT_ONESHOT: c->oneshot = value != 0; break;
     case FC_OPT_ROLE_WEIGHTS: c->role_weights = value; break;

@@ -235,7 +235,7 @@ static fc_status quant_stream(const T* x, int64_t n, const DevCodec& dc, uint8_t
   FlashArgs a = codec_args(x, dst, n, dc, err);
   a.stages = 4;
   const int smem = a.stages * (kTileElems * 2 + 16);
-  if (dc.g == kGplG) {  // one lane per group
+  if (Spec::SB == 4 && dc.g == kGplG) {  // one lane per group (INT4; see launch_qstream)
     const void* k = (const void*)k_qstream_gpl<T, Spec>;
     FC_TRY(ensure_smem_attr(k, smem));
     k_qstream_gpl<T, Spec><<<stream_grid_cur(k, kGplThreads, smem, a.tiles), kGplThreads, smem, st>>>(a);
