@@ -332,9 +332,9 @@ def bench_local(args, cfg, peaks):
     phase_bytes = {"scatter": tp * (tp - 1) * seg * (e + b1),
                    "reduce": tp * seg * (2 * e + (tp - 1) * (b1 + b2)),
                    "gather": tp * (tp - 1) * seg * (b2 + e)}
-    # g = 128 scatters run the group-per-lane kernel (fc_stream.cuh q_role_gpl)
-    phase_kernel = {"scatter": "k_qstream_gpl" if cfg["group"] == 128 else "k_qstream", "reduce": "k_rstream",
-                    "gather": "k_dstream"}
+    # INT4 g = 128 scatters run the group-per-lane kernel (fc_stream.cuh q_role_gpl)
+    gpl = cfg["group"] == 128 and cfg["bits"] == 4
+    phase_kernel = {"scatter": "k_qstream_gpl" if gpl else "k_qstream", "reduce": "k_rstream", "gather": "k_dstream"}
     phases = {}
     comm.set_option(_lib.OPT_FUSED, 0)  # phase kernels are timed on the split path
     for bit, name in ((1, "scatter"), (2, "reduce"), (4, "gather")):
