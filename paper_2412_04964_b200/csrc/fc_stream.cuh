@@ -669,6 +669,328 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
   }
 }
 
+// ------------------------------------------------------------------ group-per-lane reduce role
+
+// acc (+)= (c - z) * s for NW code words (8 offset-binary INT4 codes each),
+// into pairs in the INT4 pairing (8i+a, 8i+a+4): decode_pairs over NW words
+template <int NW>
+__device__ __forceinline__ void decode_words4(const uint32_t* cw, float s, float mz, uint64_t* acc) {
+  const uint64_t S2 = f2_splat(s), NMZ2 = f2_splat(-mz);
+  const uint64_t S16 = f2_splat(s * 0.0625f), NMZ16 = f2_splat(-fmaf(mz, 16.0f, -125829120.0f));
+  auto emit = [&](int idx, uint32_t va, uint32_t vb, uint64_t nmz, uint64_t sc) {
+    uint64_t M;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(M) : "r"(va), "r"(vb));
+    acc[idx] = f2_fma(f2_add(M, nmz), sc, acc[idx]);
+  };
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    const uint32_t lo = cw[i] & 0x0F0F0F0Fu, hi = cw[i] & 0xF0F0F0F0u;
+    emit(4 * i + 0, __byte_perm(lo, 0x4B000000u, 0x7440u), __byte_perm(lo, 0x4B000000u, 0x7442u), NMZ2, S2);
+    emit(4 * i + 2, __byte_perm(lo, 0x4B000000u, 0x7441u), __byte_perm(lo, 0x4B000000u, 0x7443u), NMZ2, S2);
+    emit(4 * i + 1, __byte_perm(hi, 0x4B000000u, 0x7440u), __byte_perm(hi, 0x4B000000u, 0x7442u), NMZ16, S16);
+    emit(4 * i + 3, __byte_perm(hi, 0x4B000000u, 0x7441u), __byte_perm(hi, 0x4B000000u, 0x7443u), NMZ16, S16);
+  }
+}
+
+__device__ __forceinline__ float acc_get(const uint64_t* acc, int e) {
+  float a, b;
+  f2_unpack(acc[(e >> 3) * 4 + (e & 3)], a, b);
+  return (e & 4) ? b : a;
+}
+
+// INT4 g = 128 reduce with 64 elements per lane, 2 lanes per group
+// (k_rstream_gpl). The 32-element layout of r_role spreads a group over 4
+// lanes, so each lane repeats both quantizations' bound reductions (two
+// shuffle steps), float64 scales and zero points; here a lane pair shares a
+// group (one shuffle step, half the repeated tail), and the lane keeps its
+// 64 fp32 accumulators in registers (32 pairs in the INT4 pairing: decode,
+// accumulate and re-encode never move registers). Own-group stage-1 QDQ
+// (collectives.py:364-365), rank-ordered fp32 sum (collectives.py:182-187),
+// stage-2 quantize, peers' gather slots, own output. Whole tiles only
+// (launch_rstream falls back to r_role otherwise). The lane's own input is read
+// XOR-swizzled (conflict-free) and its output leaves through the same 128-B
+// region of the stage, then one coalesced copy per warp.
+constexpr int kRgEpl = 64;                              // elements per lane
+constexpr int kRgLpg = kGplG / kRgEpl;                  // lanes per group (2)
+constexpr int kRgWpt = kTileElems / (32 * kRgEpl);      // warps per tile (4)
+
+template <typename Tin, typename Tout, class S1, class S2, class Iter>
+__device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
+  static_assert(sizeof(Tin) == 2 && sizeof(Tout) == 2, "16-bit inputs and outputs");
+  static_assert(S1::SB == 4 && S2::SB == 4, "INT4 storage");
+  static_assert(kGplWarps == kRgWpt, "one tile per pass of the consumer warps");
+  constexpr int NC = kRgEpl / 8;  // 8-element chunks (= INT4 code words) per lane
+  const uint32_t SBY = rstage_bytes(a.c1, a.world);
+  const uint32_t PC = peer_codes_bytes(a.c1), PM = peer_meta_bytes(a.c1), SCB = peer_scale_bytes(a.c1);
+  const int NP = a.world;
+  const uint32_t full0 = sbase + S * SBY, empty0 = full0 + 8 * S * NP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S * NP; ++s) mbar_init(full0 + 8 * s, 1);
+    for (int s = 0; s < S; ++s) mbar_init(empty0 + 8 * s, kRgWpt);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kGplWarps) {  // producer: the same pieces and barriers as r_role (whole tiles)
+    if (lane == 0) {
+      int st = 0, k = 0;
+      uint32_t ph = 0;
+      for (Iter it = it0; it.ok(); it.next(), ++k) {
+        const int j = a.rank_lo + it.y;
+        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        const int64_t e0 = (int64_t)it.t * kTileElems;
+        const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
+        const int64_t grp0 = e0 >> a.c1.gshift;
+        const uint32_t st_base = sbase + st * SBY;
+        const uint32_t bar0 = full0 + 8 * (st * NP);
+        mbar_arrive_expect_tx(bar0, kTileElems * 2);
+        bulk_g2s(st_base, reinterpret_cast<const Tin*>(a.in[j]) + seg0 + e0, kTileElems * 2, bar0);
+        uint32_t dst = st_base + kTileElems * 2;
+        int piece = 1;
+        for (int s = 0; s < a.world; ++s) {
+          if (s == j) continue;
+          const uint32_t bar = bar0 + 8 * piece++;
+          const uint8_t* slot = recv_slot(a, j, s);
+          const uint32_t zb = S1::SYM ? 0u : PM - SCB;
+          mbar_arrive_expect_tx(bar, PC + SCB + zb);
+          bulk_g2s(dst, slot + e0 / 2, PC, bar);
+          bulk_g2s(dst + PC, slot + a.c1.scales_off + grp0 * 2, SCB, bar);
+          if (zb) bulk_g2s(dst + PC + SCB, slot + a.c1.zeros_off + grp0, zb, bar);
+          dst += PC + PM;
+        }
+        ring_next(st, ph, S);
+      }
+    }
+    return;
+  }
+  const int m = lane & 7;
+  const int li = warp * 32 + lane;         // lane slice of the tile: elements [li*64, li*64+64)
+  const int gt = li / kRgLpg;              // tile-local group
+  const bool lead = (li & (kRgLpg - 1)) == 0;
+  const uint32_t xr1 = rep_xor(a.c1), xr2 = rep_xor(a.c2);
+  const uint32_t qmax1 = (1u << a.c1.bits) - 1u, qmax2 = (1u << a.c2.bits) - 1u;
+  int st = 0;
+  uint32_t ph = 0;
+  for (Iter it = it0; it.ok(); it.next()) {
+    const int j = a.rank_lo + it.y;
+    const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
+    const int64_t e0 = (int64_t)it.t * kTileElems;
+    const int64_t p0 = e0 + li * kRgEpl;  // lane slice start in the round
+    const uint32_t st_base = sbase + st * SBY;
+    const uint32_t bar0 = full0 + 8 * (st * NP);
+    const uint32_t lb = st_base + li * (kRgEpl * 2);
+    // ---- own group: stage-1 QDQ
+    uint32_t own[NC];
+    float s1;
+    uint32_t z1;
+    bool bad;
+    mbar_wait(bar0, ph);
+    {
+      uint32_t x[NC][4];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const uint4 u = lds128_(lb + 16 * (c ^ m));
+        x[c][0] = u.x;
+        x[c][1] = u.y;
+        x[c][2] = u.z;
+        x[c][3] = u.w;
+      }
+      uint32_t mn, mx;
+      if constexpr (S1::SYM) {
+        mx = x[0][0] & 0x7FFF7FFFu;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (c | i) mx = h2max<Tin>(mx, x[c][i] & 0x7FFF7FFFu);
+        mn = mx;
+      } else {
+        mn = h2min<Tin>(x[0][0], x[0][1]);
+        mx = h2max<Tin>(x[0][0], x[0][1]);
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (c > 0 || i > 1) {
+              mn = h2min<Tin>(mn, x[c][i]);
+              mx = h2max<Tin>(mx, x[c][i]);
+            }
+      }
+      // the lane's bounds, then one shuffle step with the group partner
+      float hi, lo;
+      {
+        float lh = fmax_nan(h_lo<Tin>(mx), h_hi<Tin>(mx));
+        float ll = S1::SYM ? -lh : fmin_nan(h_lo<Tin>(mn), h_hi<Tin>(mn));
+        lh = fmax_nan(lh, __shfl_xor_sync(0xffffffffu, lh, 1));
+        ll = fmin_nan(ll, __shfl_xor_sync(0xffffffffu, ll, 1));
+        hi = lh;
+        lo = S1::SYM ? -hi : ll;
+      }
+      bad = !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
+      GroupQ g;
+      group_params<S1>(a.c1, lo, hi, g);
+      if (bad) g.z = S1::SYM ? g.z : 0u;
+      if (g.normal) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) chunk_codes_packed<S1, Tin>(x[c], g, qmax1, own + c);
+      } else {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax1, own + c);
+      }
+      unswizzle_chunks<NC, 1>(own, m);
+      s1 = g.s;
+      z1 = g.z;
+    }
+    // ---- fp32 sum in ascending source rank, the own group at its rank position
+    uint64_t acc[4 * NC];
+#pragma unroll
+    for (int e = 0; e < 4 * NC; ++e) acc[e] = 0ull;
+    uint32_t pbar = bar0, src = st_base + kTileElems * 2;
+    for (int s = 0; s < a.world; ++s) {
+      if (s == j) {  // uniform
+        decode_words4<NC>(own, s1, 8388608.0f + (float)z1, acc);
+      } else {
+        pbar += 8;
+        mbar_wait(pbar, ph);
+        uint32_t cw[NC];
+#pragma unroll
+        for (int v = 0; v < NC / 4; ++v) {
+          const uint4 u = lds128_(src + li * (kRgEpl / 2) + 16 * v);
+          cw[4 * v] = u.x;
+          cw[4 * v + 1] = u.y;
+          cw[4 * v + 2] = u.z;
+          cw[4 * v + 3] = u.w;
+        }
+        unsigned short sh;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(src + PC + 2 * gt));
+        float zf;
+        if constexpr (S1::SYM) {
+          zf = (float)(1 << (a.c1.bits - 1));
+#pragma unroll
+          for (int q = 0; q < NC; ++q) cw[q] ^= xr1;
+        } else {
+          uint32_t zz;
+          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(src + PC + SCB + gt));
+          zf = (float)zz;
+        }
+        decode_words4<NC>(cw, __half2float(__ushort_as_half(sh)), 8388608.0f + zf, acc);
+        src += PC + PM;
+      }
+    }
+    // ---- stage-2 quantize of the sum
+    float lo2, hi2;
+    {
+      float a0 = acc_get(acc, 0), b0 = S2::SYM ? fabsf(a0) : a0;
+#pragma unroll
+      for (int e = 1; e < kRgEpl; e += 2) {
+        const float u = acc_get(acc, e), v = e + 1 < kRgEpl ? acc_get(acc, e + 1) : u;
+        if constexpr (S2::SYM) {
+          b0 = fmax3_nan(b0, fabsf(u), fabsf(v));
+        } else {
+          a0 = fmin3_nan(a0, u, v);
+          b0 = fmax3_nan(b0, u, v);
+        }
+      }
+      b0 = fmax_nan(b0, __shfl_xor_sync(0xffffffffu, b0, 1));
+      if constexpr (!S2::SYM) a0 = fmin_nan(a0, __shfl_xor_sync(0xffffffffu, a0, 1));
+      hi2 = b0;
+      lo2 = S2::SYM ? -b0 : a0;
+    }
+    const bool bad2 = !(fabsf(lo2) <= 3.402823466e38f && fabsf(hi2) <= 3.402823466e38f);
+    bad |= bad2;
+    GroupQ g2;
+    group_params<S2>(a.c2, lo2, hi2, g2);
+    if (bad2) g2.z = S2::SYM ? g2.z : 0u;
+    uint32_t w2[NC];
+    if (g2.normal) {
+      const uint64_t R2 = f2_splat(g2.r), NS2 = f2_splat(-g2.s), C2 = f2_splat(12582912.0f);
+      const uint32_t Z2 = g2.z * 0x00010001u, Q2 = qmax2 * 0x00010001u;
+      auto code_pair = [&](uint64_t X) -> uint32_t {
+        const uint64_t T = f2_mul(X, R2);
+        const uint64_t Q = f2_fma(f2_fma(T, NS2, X), R2, T);
+        const uint64_t Y = S2::CEIL ? f2_add_rp(Q, C2) : f2_add(Q, C2);
+        uint32_t ya, yb;
+        f2_bits(Y, ya, yb);
+        const uint32_t pp = __byte_perm(ya, yb, 0x5410);
+        const uint32_t c = __viaddmax_s16x2(pp, Z2, 0u);
+        return __vimin3_s16x2(c, Q2, Q2);
+      };
+#pragma unroll
+      for (int i = 0; i < NC; ++i)
+        w2[i] = code_pair(acc[4 * i]) + (code_pair(acc[4 * i + 1]) << 4) + (code_pair(acc[4 * i + 2]) << 8) +
+                (code_pair(acc[4 * i + 3]) << 12);
+    } else {  // float clamp before rounding (the lane_codes path)
+      const float r = __frcp_rn(g2.s);
+      const float lob = -(float)g2.z, hib = (float)(qmax2 - g2.z);
+      const int zb = (int)g2.z - 0x4B400000;
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        uint32_t wv = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float xv = acc_get(acc, 8 * i + e);
+          const float t = xv * r;
+          const float q1 = fmaf(fmaf(-t, g2.s, xv), r, t);
+          const float qc = fminf(fmaxf(q1, lob), hib);
+          const float y = S2::CEIL ? __fadd_ru(qc, 12582912.0f) : __fadd_rn(qc, 12582912.0f);
+          wv |= (uint32_t)(__float_as_int(y) + zb) << (4 * e);
+        }
+        w2[i] = wv;
+      }
+    }
+    // ---- every peer's gather slot [j] (stored codes: offset binary ^ xr for sym)
+    {
+      const int64_t slot_off = (int64_t)(a.world + j) * a.slot_bytes;
+      const int64_t grp = p0 >> a.c2.gshift;
+      const uint4 c0 = make_uint4(w2[0] ^ xr2, w2[1] ^ xr2, w2[2] ^ xr2, w2[3] ^ xr2);
+      const uint4 c1 = make_uint4(w2[4] ^ xr2, w2[5] ^ xr2, w2[6] ^ xr2, w2[7] ^ xr2);
+      for (int p = j + 1;; ++p) {
+        if (p == a.world) p = 0;
+        if (p == j) break;
+        uint8_t* b = a.blk[p] + slot_off;
+        uint8_t* cd = b + p0 / 2;
+        *reinterpret_cast<uint4*>(cd) = c0;
+        *reinterpret_cast<uint4*>(cd + 16) = c1;
+        if (lead) {
+          *reinterpret_cast<unsigned short*>(b + a.c2.scales_off + 2 * grp) = g2.s16;
+          if constexpr (!S2::SYM) b[a.c2.zeros_off + grp] = (uint8_t)g2.z;
+        }
+      }
+    }
+    // ---- own output: the owner decodes its own payload (collectives.py:378), staged
+    // through its input region (swizzled), then one coalesced copy of the warp's 4 KB
+    {
+#pragma unroll
+      for (int e = 0; e < 4 * NC; ++e) acc[e] = 0ull;
+      decode_words4<NC>(w2, g2.s, 8388608.0f + (float)g2.z, acc);  // 0 + (c - z) s: exact, never -0
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        uint32_t h[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          h[q] = pack2(acc_get(acc, 8 * c + 2 * q), acc_get(acc, 8 * c + 2 * q + 1), (Tout*)nullptr);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(lb + 16 * (c ^ m)), "r"(h[0]), "r"(h[1]), "r"(h[2]),
+                     "r"(h[3])
+                     : "memory");
+      }
+      __syncwarp();
+      const uint32_t wbase = st_base + warp * (32 * kRgEpl * 2);
+      uint8_t* ob = reinterpret_cast<uint8_t*>(reinterpret_cast<Tout*>(a.out[j]) + seg0 + e0 + warp * (32 * kRgEpl));
+      // byte 512 v + 16 lane of the warp's output = chunk q = lane % 8 of slice l = 4 v + lane / 8,
+      // stored at l * 128 + 16 (q ^ (l & 7)) (conflict-free for each 8-lane phase)
+#pragma unroll
+      for (int v = 0; v < NC; ++v) {
+        const int l = 4 * v + (lane >> 3), q = lane & 7;
+        st_v4(ob + 512 * v + 16 * lane, lds128_(wbase + l * (kRgEpl * 2) + 16 * (q ^ (l & 7))));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);
+    if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
+    ring_next(st, ph, S);
+  }
+}
+
 // ------------------------------------------------------------------ reduce role
 
 // owner j = rank_lo + y: own segment QDQ + N-1 received pieces -> fp32 sum
@@ -1037,6 +1359,15 @@ __global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   r_role<Tin, Tout, S1, S2, false>(a, smem_u32(smem), a.stages,
                                    RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+}
+
+// INT4 g = 128 reduce, two lanes per group (r_role_gpl); whole tiles only
+template <typename Tin, typename Tout, class S1, class S2>
+__global__ void __launch_bounds__(kGplThreads, 2) k_rstream_gpl(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  if constexpr (sizeof(Tout) == 2 && S1::SB == 4 && S2::SB == 4)
+    r_role_gpl<Tin, Tout, S1, S2>(a, smem_u32(smem), a.stages,
+                                  RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
 template <typename Tout, class S2>

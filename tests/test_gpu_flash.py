@@ -276,3 +276,31 @@ def test_compile_time_schemes_vs_oracle(bits, g, sym, rnd, mode):
         if mode == "split":
             assert comm.slot(j, 1, s, codec).to_bytes() == res.stage1[j][s].wire_bytes(), f"stage-1 {j}<-{s}"
     comm.close()
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+@pytest.mark.parametrize("codec", [dict(bits=4), dict(bits=4, symmetric=True), dict(bits=4, rounding="ceil")])
+def test_group_lane_kernels_match_lane_kernels(tp, codec):
+    # INT4 g128 whole tiles take the group-per-lane scatter and the 2-lanes-per-group
+    # reduce; FC_OPT_STREAM_MASK bits 6/7 force the 32-element lane kernels: bit-identical
+    m = tp * 8192 * 3
+    cfg = fc.FlashConfig.uniform(fc.CodecConfig(**codec))
+    comm = _comm(tp, m // tp, cfg, "split")
+    for dt in (torch.bfloat16, torch.float16):
+        g = torch.Generator(device="cuda").manual_seed(tp)
+        ts = [(torch.randn(m, device="cuda", generator=g) * (1 + r)).to(dt) for r in range(tp)]
+        ts[0][5000:5128] = 1000.0  # a constant group (scale floor) and a large-offset one
+        ts[1][9000:9128] += 3000.0
+        outs = {}
+        for mask in (0, 64 | 128):
+            comm.set_option(_lib.OPT_STREAM_MASK, mask)
+            outs[mask] = [o.clone() for o in comm.all_reduce_local(ts, cfg, out_dtype=torch.float32)]
+        comm.set_option(_lib.OPT_STREAM_MASK, 0)
+        for a, b in zip(outs[0], outs[64 | 128]):
+            assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+        if tp == 4 and dt == torch.bfloat16:
+            xr = [t.float().cpu().numpy() for t in ts]
+            oc = orc.Codec(bits=4, symmetric=codec.get("symmetric", False), rounding=codec.get("rounding", "nearest-even"))
+            ref = orc.flash_all_reduce(xr, oc, oc).outputs[0]
+            assert np.array_equal(_bits(outs[0][2].cpu().numpy()), _bits(ref))
+    comm.close()
