@@ -332,9 +332,11 @@ def bench_local(args, cfg, peaks):
     phase_bytes = {"scatter": tp * (tp - 1) * seg * (e + b1),
                    "reduce": tp * seg * (2 * e + (tp - 1) * (b1 + b2)),
                    "gather": tp * (tp - 1) * seg * (b2 + e)}
-    # INT4 g = 128 scatters run the group-per-lane kernel (fc_stream.cuh q_role_gpl)
+    # INT4 g = 128 runs the group-per-lane scatter and the 2-lanes-per-group reduce
+    # (fc_stream.cuh q_role_gpl / r_role_gpl; the reduce needs whole tiles, true for every config here)
     gpl = cfg["group"] == 128 and cfg["bits"] == 4
-    phase_kernel = {"scatter": "k_qstream_gpl" if gpl else "k_qstream", "reduce": "k_rstream", "gather": "k_dstream"}
+    phase_kernel = {"scatter": "k_qstream_gpl" if gpl else "k_qstream",
+                    "reduce": "k_rstream_gpl" if gpl else "k_rstream", "gather": "k_dstream"}
     phases = {}
     comm.set_option(_lib.OPT_FUSED, 0)  # phase kernels are timed on the split path
     for bit, name in ((1, "scatter"), (2, "reduce"), (4, "gather")):
