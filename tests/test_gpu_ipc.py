@@ -97,7 +97,7 @@ def _run(world, mode):
     assert res == {r: "ok" for r in range(world)}, res
 
 
-@pytest.mark.parametrize("world,mode", [(2, "fused"), (4, "fused"), (2, "split"), (3, "generic")])
+@pytest.mark.parametrize("world,mode", [(2, "fused"), (4, "fused"), (2, "split"), (4, "split"), (3, "generic")])
 def test_ipc_parity(world, mode):
     _run(world, mode)
 
