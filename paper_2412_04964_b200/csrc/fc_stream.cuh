@@ -714,6 +714,12 @@ constexpr int kRgEpl = 64;                              // elements per lane
 constexpr int kRgLpg = kGplG / kRgEpl;                  // lanes per group (2)
 constexpr int kRgWpt = kTileElems / (32 * kRgEpl);      // warps per tile (4)
 
+// byte offset of the output staging after the rings and barriers, and the total bytes
+__host__ __device__ inline uint32_t rg_obuf_off(uint32_t ring_bytes) { return (ring_bytes + 127u) & ~127u; }
+__host__ __device__ inline uint32_t rg_smem_bytes(uint32_t ring_bytes) {
+  return rg_obuf_off(ring_bytes) + kGplWarps * 32 * kRgEpl * 2;
+}
+
 template <typename Tin, typename Tout, class S1, class S2, class Iter>
 __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
   static_assert(sizeof(Tin) == 2 && sizeof(Tout) == 2, "16-bit inputs and outputs");
@@ -724,6 +730,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   const uint32_t PC = peer_codes_bytes(a.c1), PM = peer_meta_bytes(a.c1), SCB = peer_scale_bytes(a.c1);
   const int NP = a.world;
   const uint32_t full0 = sbase + S * SBY, empty0 = full0 + 8 * S * NP;
+  const uint32_t obuf = rg_obuf_off(S * SBY + 8 * S * (NP + 1)) + sbase;  // output staging, 4 KB per warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S * NP; ++s) mbar_init(full0 + 8 * s, 1);
@@ -877,6 +884,10 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         src += PC + PM;
       }
     }
+    // every shared load of the stage has been consumed: hand it back to the producer now, so
+    // the next tile's copies overlap the stage-2 quantize, the stores and the output
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);
     // ---- stage-2 quantize of the sum
     float lo2, hi2;
     {
@@ -958,8 +969,10 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
       }
     }
     // ---- own output: the owner decodes its own payload (collectives.py:378), staged
-    // through its input region (swizzled), then one coalesced copy of the warp's 4 KB
+    // through the warp's own 4-KB buffer (swizzled), then one coalesced copy
     {
+      const uint32_t ob0 = obuf + warp * (32 * kRgEpl * 2);
+      const uint32_t lo_b = ob0 + lane * (kRgEpl * 2);
 #pragma unroll
       for (int e = 0; e < 4 * NC; ++e) acc[e] = 0ull;
       decode_words4<NC>(w2, g2.s, 8388608.0f + (float)g2.z, acc);  // 0 + (c - z) s: exact, never -0
@@ -969,12 +982,12 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           h[q] = pack2(acc_get(acc, 8 * c + 2 * q), acc_get(acc, 8 * c + 2 * q + 1), (Tout*)nullptr);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(lb + 16 * (c ^ m)), "r"(h[0]), "r"(h[1]), "r"(h[2]),
-                     "r"(h[3])
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(lo_b + 16 * (c ^ m)), "r"(h[0]), "r"(h[1]),
+                     "r"(h[2]), "r"(h[3])
                      : "memory");
       }
       __syncwarp();
-      const uint32_t wbase = st_base + warp * (32 * kRgEpl * 2);
+      const uint32_t wbase = ob0;
       uint8_t* ob = reinterpret_cast<uint8_t*>(reinterpret_cast<Tout*>(a.out[j]) + seg0 + e0 + warp * (32 * kRgEpl));
       // byte 512 v + 16 lane of the warp's output = chunk q = lane % 8 of slice l = 4 v + lane / 8,
       // stored at l * 128 + 16 (q ^ (l & 7)) (conflict-free for each 8-lane phase)
@@ -983,9 +996,8 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         const int l = 4 * v + (lane >> 3), q = lane & 7;
         st_v4(ob + 512 * v + 16 * lane, lds128_(wbase + l * (kRgEpl * 2) + 16 * (q ^ (l & 7))));
       }
+      __syncwarp();  // the copy's loads complete before the next tile's stores to the buffer
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * st);
     if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
     ring_next(st, ph, S);
   }
