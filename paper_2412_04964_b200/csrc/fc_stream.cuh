@@ -376,11 +376,7 @@ __device__ __forceinline__ void q_role(const FlashArgs& a, uint32_t sbase, int S
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * st);
     if (staged) unrotate_codes<S1>(q.w, rot);
-    if (a.dbg & 32) {  // timing experiment only: no code stores
-      if (q.w[0] == 0x12345678u && q.w[1] == q.w[2]) store_codes<S1>(a.c1, jb.dst, p0, nvalid, q, lane);
-    } else {
-      store_codes<S1>(a.c1, jb.dst, p0, nvalid, q, lane);
-    }
+    store_codes<S1>(a.c1, jb.dst, p0, nvalid, q, lane);
     if (bad && jb.err) atomicOr(jb.err, jb.ecode);
     if constexpr (FUSED) {
       consumers_sync();
@@ -1041,13 +1037,9 @@ __device__ __forceinline__ void r_role(const FlashArgs& a, uint32_t sbase, int S
         const int64_t v = clamp0(min((int64_t)kTileElems, a.sub_len - e0));
         const int64_t grp0 = e0 >> a.c1.gshift, ng = (v + a.c1.g - 1) >> a.c1.gshift;
         const uint32_t cb = v > 0 ? up16(v * a.c1.sb / 8) : 0u;
-        uint32_t sb = v > 0 ? up16(ng * 2) : 0u;
-        uint32_t zb = (v > 0 && !a.c1.sym) ? up16(ng) : 0u;
+        const uint32_t sb = v > 0 ? up16(ng * 2) : 0u;
+        const uint32_t zb = (v > 0 && !a.c1.sym) ? up16(ng) : 0u;
         const uint32_t st_base = sbase + st * SBY;
-        if (a.dbg & 8) {  // timing experiment only: no metadata copies (wrong results)
-          sb = 0;
-          zb = 0;
-        }
         const uint32_t bar0 = full0 + 8 * (st * NP);
         mbar_arrive_expect_tx(bar0, own);
         if (own) bulk_g2s(st_base, reinterpret_cast<const Tin*>(a.in[j]) + seg0 + e0, own, bar0);
@@ -1326,9 +1318,7 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
     // release the stage after the shared loads were consumed (see q_role)
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * st);
-    if (a.dbg & 16) {  // timing experiment only: no output stores
-      if (val[0][0] == 1.2345f) obase[0] = DT<Tout>::from_f(val[1][1] + val[2][2] + val[3][3]);
-    } else if (v >= kTileElems) {  // whole tile: no per-block checks
+    if (v >= kTileElems) {  // whole tile: no per-block checks
 #pragma unroll
       for (int b = 0; b < kBlocks; ++b) store8(obase + b * kThreads * 8, val[b]);
     } else {

@@ -114,9 +114,10 @@ def tune_sweep():
     grid += [{_lib.OPT_GATHER_STAGES: d} for d in (3, 4, 8, 12)]
     grid += [{_lib.OPT_REDUCE_STAGES: r} for r in (1, 3, 4)]
     grid += [{_lib.OPT_CTAS_PER_SM: c} for c in (1, 2, 3)]
-    grid += [{_lib.OPT_PHASES: 1}, {_lib.OPT_PHASES: 1, _lib.OPT_STREAM_MASK: 32},
-             {_lib.OPT_PHASES: 2}, {_lib.OPT_PHASES: 2, _lib.OPT_STREAM_MASK: 8},
-             {_lib.OPT_PHASES: 4}, {_lib.OPT_PHASES: 4, _lib.OPT_STREAM_MASK: 16}]
+    # per phase; stream-mask bits 6/7: the 32-element-lane INT4 g128 scatter / reduce (A/B)
+    grid += [{_lib.OPT_PHASES: 1}, {_lib.OPT_PHASES: 1, _lib.OPT_STREAM_MASK: 64},
+             {_lib.OPT_PHASES: 2}, {_lib.OPT_PHASES: 2, _lib.OPT_STREAM_MASK: 128},
+             {_lib.OPT_PHASES: 4}]
     for opts in grid:
         for o in (_lib.OPT_SCATTER_STAGES, _lib.OPT_GATHER_STAGES, _lib.OPT_REDUCE_STAGES, _lib.OPT_CTAS_PER_SM,
                   _lib.OPT_STREAM_MASK, _lib.OPT_PHASES):
