@@ -336,7 +336,7 @@ def bench_local(args, cfg, peaks):
     # (fc_stream.cuh q_role_gpl / r_role_gpl; the reduce needs whole tiles, true for every config here)
     gpl = cfg["group"] == 128 and cfg["bits"] == 4
     phase_kernel = {"scatter": "k_qstream_gpl" if gpl else "k_qstream",
-                    "reduce": "k_rstream_gpl" if gpl else "k_rstream", "gather": "k_dstream"}
+                    "reduce": "k_rstream_gpl" if cfg["group"] == 128 else "k_rstream", "gather": "k_dstream"}
     phases = {}
     comm.set_option(_lib.OPT_FUSED, 0)  # phase kernels are timed on the split path
     for bit, name in ((1, "scatter"), (2, "reduce"), (4, "gather")):

@@ -688,10 +688,40 @@ __device__ __forceinline__ void decode_words4(const uint32_t* cw, float s, float
   }
 }
 
+// the same for NW INT8 code words (4 codes each) into the INT8 pairing (4i+a, 4i+a+2)
+template <int NW>
+__device__ __forceinline__ void decode_words8(const uint32_t* cw, float s, float mz, uint64_t* acc) {
+  const uint64_t S2 = f2_splat(s), NMZ2 = f2_splat(-mz);
+  auto emit = [&](int idx, uint32_t va, uint32_t vb) {
+    uint64_t M;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(M) : "r"(va), "r"(vb));
+    acc[idx] = f2_fma(f2_add(M, NMZ2), S2, acc[idx]);
+  };
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    emit(2 * i + 0, __byte_perm(cw[i], 0x4B000000u, 0x7440u), __byte_perm(cw[i], 0x4B000000u, 0x7442u));
+    emit(2 * i + 1, __byte_perm(cw[i], 0x4B000000u, 0x7441u), __byte_perm(cw[i], 0x4B000000u, 0x7443u));
+  }
+}
+template <int SB, int NW>
+__device__ __forceinline__ void decode_words(const uint32_t* cw, float s, float mz, uint64_t* acc) {
+  if constexpr (SB == 4)
+    decode_words4<NW>(cw, s, mz, acc);
+  else
+    decode_words8<NW>(cw, s, mz, acc);
+}
+
+// element e of accumulators held in the pairing of storage width SB
+template <int SB = 4>
 __device__ __forceinline__ float acc_get(const uint64_t* acc, int e) {
   float a, b;
-  f2_unpack(acc[(e >> 3) * 4 + (e & 3)], a, b);
-  return (e & 4) ? b : a;
+  if constexpr (SB == 4) {
+    f2_unpack(acc[(e >> 3) * 4 + (e & 3)], a, b);
+    return (e & 4) ? b : a;
+  } else {
+    f2_unpack(acc[(e >> 2) * 2 + (e & 1)], a, b);
+    return (e & 2) ? b : a;
+  }
 }
 
 // INT4 g = 128 reduce with 64 elements per lane, 2 lanes per group
@@ -719,9 +749,12 @@ __host__ __device__ inline uint32_t rg_smem_bytes(uint32_t ring_bytes) {
 template <typename Tin, typename Tout, class S1, class S2, class Iter>
 __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
   static_assert(sizeof(Tin) == 2 && sizeof(Tout) == 2, "16-bit inputs and outputs");
-  static_assert(S1::SB == 4 && S2::SB == 4, "INT4 storage");
+  static_assert(S1::SB == S2::SB, "one storage width for both stages");
   static_assert(kGplWarps == kRgWpt, "one tile per pass of the consumer warps");
-  constexpr int NC = kRgEpl / 8;  // 8-element chunks (= INT4 code words) per lane
+  constexpr int SB = S1::SB;
+  constexpr int NC = kRgEpl / 8;         // 8-element chunks per lane
+  constexpr int CWPC = SB / 4;           // code words per chunk
+  constexpr int NW = NC * CWPC;          // code words per lane
   const uint32_t SBY = rstage_bytes(a.c1, a.world);
   const uint32_t PC = peer_codes_bytes(a.c1), PM = peer_meta_bytes(a.c1), SCB = peer_scale_bytes(a.c1);
   const int NP = a.world;
@@ -756,7 +789,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
           const uint8_t* slot = recv_slot(a, j, s);
           const uint32_t zb = S1::SYM ? 0u : PM - SCB;
           mbar_arrive_expect_tx(bar, PC + SCB + zb);
-          bulk_g2s(dst, slot + e0 / 2, PC, bar);
+          bulk_g2s(dst, slot + e0 * SB / 8, PC, bar);
           bulk_g2s(dst + PC, slot + a.c1.scales_off + grp0 * 2, SCB, bar);
           if (zb) bulk_g2s(dst + PC + SCB, slot + a.c1.zeros_off + grp0, zb, bar);
           dst += PC + PM;
@@ -783,7 +816,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     const uint32_t bar0 = full0 + 8 * (st * NP);
     const uint32_t lb = st_base + li * (kRgEpl * 2);
     // ---- own group: stage-1 QDQ
-    uint32_t own[NC];
+    uint32_t own[NW];
     float s1;
     uint32_t z1;
     bool bad;
@@ -835,12 +868,13 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
       if (bad) g.z = S1::SYM ? g.z : 0u;
       if (g.normal) {
 #pragma unroll
-        for (int c = 0; c < NC; ++c) chunk_codes_packed<S1, Tin>(x[c], g, qmax1, own + c);
+        for (int c = 0; c < NC; ++c) chunk_codes_packed<S1, Tin>(x[c], g, qmax1, own + c * CWPC);
       } else {
 #pragma unroll
-        for (int c = 0; c < NC; ++c) chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax1, own + c);
+        for (int c = 0; c < NC; ++c)
+          chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax1, own + c * CWPC);
       }
-      unswizzle_chunks<NC, 1>(own, m);
+      unswizzle_chunks<NC, CWPC>(own, m);
       s1 = g.s;
       z1 = g.z;
     }
@@ -851,14 +885,14 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     uint32_t pbar = bar0, src = st_base + kTileElems * 2;
     for (int s = 0; s < a.world; ++s) {
       if (s == j) {  // uniform
-        decode_words4<NC>(own, s1, 8388608.0f + (float)z1, acc);
+        decode_words<SB, NW>(own, s1, 8388608.0f + (float)z1, acc);
       } else {
         pbar += 8;
         mbar_wait(pbar, ph);
-        uint32_t cw[NC];
+        uint32_t cw[NW];
 #pragma unroll
-        for (int v = 0; v < NC / 4; ++v) {
-          const uint4 u = lds128_(src + li * (kRgEpl / 2) + 16 * v);
+        for (int v = 0; v < NW / 4; ++v) {
+          const uint4 u = lds128_(src + li * (kRgEpl * SB / 8) + 16 * v);
           cw[4 * v] = u.x;
           cw[4 * v + 1] = u.y;
           cw[4 * v + 2] = u.z;
@@ -870,13 +904,13 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         if constexpr (S1::SYM) {
           zf = (float)(1 << (a.c1.bits - 1));
 #pragma unroll
-          for (int q = 0; q < NC; ++q) cw[q] ^= xr1;
+          for (int q = 0; q < NW; ++q) cw[q] ^= xr1;
         } else {
           uint32_t zz;
           asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(src + PC + SCB + gt));
           zf = (float)zz;
         }
-        decode_words4<NC>(cw, __half2float(__ushort_as_half(sh)), 8388608.0f + zf, acc);
+        decode_words<SB, NW>(cw, __half2float(__ushort_as_half(sh)), 8388608.0f + zf, acc);
         src += PC + PM;
       }
     }
@@ -887,10 +921,10 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     // ---- stage-2 quantize of the sum
     float lo2, hi2;
     {
-      float a0 = acc_get(acc, 0), b0 = S2::SYM ? fabsf(a0) : a0;
+      float a0 = acc_get<SB>(acc, 0), b0 = S2::SYM ? fabsf(a0) : a0;
 #pragma unroll
       for (int e = 1; e < kRgEpl; e += 2) {
-        const float u = acc_get(acc, e), v = e + 1 < kRgEpl ? acc_get(acc, e + 1) : u;
+        const float u = acc_get<SB>(acc, e), v = e + 1 < kRgEpl ? acc_get<SB>(acc, e + 1) : u;
         if constexpr (S2::SYM) {
           b0 = fmax3_nan(b0, fabsf(u), fabsf(v));
         } else {
@@ -908,7 +942,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     GroupQ g2;
     group_params<S2>(a.c2, lo2, hi2, g2);
     if (bad2) g2.z = S2::SYM ? g2.z : 0u;
-    uint32_t w2[NC];
+    uint32_t w2[NW];
     if (g2.normal) {
       const uint64_t R2 = f2_splat(g2.r), NS2 = f2_splat(-g2.s), C2 = f2_splat(12582912.0f);
       const uint32_t Z2 = g2.z * 0x00010001u, Q2 = qmax2 * 0x00010001u;
@@ -922,25 +956,31 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         const uint32_t c = __viaddmax_s16x2(pp, Z2, 0u);
         return __vimin3_s16x2(c, Q2, Q2);
       };
+      if constexpr (SB == 4) {
 #pragma unroll
-      for (int i = 0; i < NC; ++i)
-        w2[i] = code_pair(acc[4 * i]) + (code_pair(acc[4 * i + 1]) << 4) + (code_pair(acc[4 * i + 2]) << 8) +
-                (code_pair(acc[4 * i + 3]) << 12);
+        for (int i = 0; i < NW; ++i)
+          w2[i] = code_pair(acc[4 * i]) + (code_pair(acc[4 * i + 1]) << 4) + (code_pair(acc[4 * i + 2]) << 8) +
+                  (code_pair(acc[4 * i + 3]) << 12);
+      } else {
+#pragma unroll
+        for (int i = 0; i < NW; ++i) w2[i] = code_pair(acc[2 * i]) + (code_pair(acc[2 * i + 1]) << 8);
+      }
     } else {  // float clamp before rounding (the lane_codes path)
       const float r = __frcp_rn(g2.s);
       const float lob = -(float)g2.z, hib = (float)(qmax2 - g2.z);
       const int zb = (int)g2.z - 0x4B400000;
+      constexpr int EPW = 32 / SB;  // elements per code word
 #pragma unroll
-      for (int i = 0; i < NC; ++i) {
+      for (int i = 0; i < NW; ++i) {
         uint32_t wv = 0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float xv = acc_get(acc, 8 * i + e);
+        for (int e = 0; e < EPW; ++e) {
+          const float xv = acc_get<SB>(acc, EPW * i + e);
           const float t = xv * r;
           const float q1 = fmaf(fmaf(-t, g2.s, xv), r, t);
           const float qc = fminf(fmaxf(q1, lob), hib);
           const float y = S2::CEIL ? __fadd_ru(qc, 12582912.0f) : __fadd_rn(qc, 12582912.0f);
-          wv |= (uint32_t)(__float_as_int(y) + zb) << (4 * e);
+          wv |= (uint32_t)(__float_as_int(y) + zb) << (SB * e);
         }
         w2[i] = wv;
       }
@@ -949,15 +989,17 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     {
       const int64_t slot_off = (int64_t)(a.world + j) * a.slot_bytes;
       const int64_t grp = p0 >> a.c2.gshift;
-      const uint4 c0 = make_uint4(w2[0] ^ xr2, w2[1] ^ xr2, w2[2] ^ xr2, w2[3] ^ xr2);
-      const uint4 c1 = make_uint4(w2[4] ^ xr2, w2[5] ^ xr2, w2[6] ^ xr2, w2[7] ^ xr2);
+      uint4 cv[NW / 4];
+#pragma unroll
+      for (int v = 0; v < NW / 4; ++v)
+        cv[v] = make_uint4(w2[4 * v] ^ xr2, w2[4 * v + 1] ^ xr2, w2[4 * v + 2] ^ xr2, w2[4 * v + 3] ^ xr2);
       for (int p = j + 1;; ++p) {
         if (p == a.world) p = 0;
         if (p == j) break;
         uint8_t* b = a.blk[p] + slot_off;
-        uint8_t* cd = b + p0 / 2;
-        *reinterpret_cast<uint4*>(cd) = c0;
-        *reinterpret_cast<uint4*>(cd + 16) = c1;
+        uint8_t* cd = b + p0 * SB / 8;
+#pragma unroll
+        for (int v = 0; v < NW / 4; ++v) *reinterpret_cast<uint4*>(cd + 16 * v) = cv[v];
         if (lead) {
           *reinterpret_cast<unsigned short*>(b + a.c2.scales_off + 2 * grp) = g2.s16;
           if constexpr (!S2::SYM) b[a.c2.zeros_off + grp] = (uint8_t)g2.z;
@@ -971,13 +1013,13 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
       const uint32_t lo_b = ob0 + lane * (kRgEpl * 2);
 #pragma unroll
       for (int e = 0; e < 4 * NC; ++e) acc[e] = 0ull;
-      decode_words4<NC>(w2, g2.s, 8388608.0f + (float)g2.z, acc);  // 0 + (c - z) s: exact, never -0
+      decode_words<SB, NW>(w2, g2.s, 8388608.0f + (float)g2.z, acc);  // 0 + (c - z) s: exact, never -0
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         uint32_t h[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          h[q] = pack2(acc_get(acc, 8 * c + 2 * q), acc_get(acc, 8 * c + 2 * q + 1), (Tout*)nullptr);
+          h[q] = pack2(acc_get<SB>(acc, 8 * c + 2 * q), acc_get<SB>(acc, 8 * c + 2 * q + 1), (Tout*)nullptr);
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(lo_b + 16 * (c ^ m)), "r"(h[0]), "r"(h[1]),
                      "r"(h[2]), "r"(h[3])
                      : "memory");
@@ -1363,11 +1405,11 @@ __global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
                                    RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
-// INT4 g = 128 reduce, two lanes per group (r_role_gpl); whole tiles only
+// g = 128 reduce, two lanes per group (r_role_gpl); one storage width, whole tiles only
 template <typename Tin, typename Tout, class S1, class S2>
 __global__ void __launch_bounds__(kGplThreads, 2) k_rstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  if constexpr (sizeof(Tout) == 2 && S1::SB == 4 && S2::SB == 4)
+  if constexpr (sizeof(Tout) == 2 && S1::SB == S2::SB)
     r_role_gpl<Tin, Tout, S1, S2>(a, smem_u32(smem), a.stages,
                                   RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }

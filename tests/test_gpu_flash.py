@@ -279,10 +279,11 @@ def test_compile_time_schemes_vs_oracle(bits, g, sym, rnd, mode):
 
 
 @pytest.mark.parametrize("tp", [2, 4, 8])
-@pytest.mark.parametrize("codec", [dict(bits=4), dict(bits=4, symmetric=True), dict(bits=4, rounding="ceil")])
+@pytest.mark.parametrize("codec", [dict(bits=4), dict(bits=4, symmetric=True), dict(bits=4, rounding="ceil"),
+                                   dict(bits=8), dict(bits=8, symmetric=True)])
 def test_group_lane_kernels_match_lane_kernels(tp, codec):
-    # INT4 g128 whole tiles take the group-per-lane scatter and the 2-lanes-per-group
-    # reduce; FC_OPT_STREAM_MASK bits 6/7 force the 32-element lane kernels: bit-identical
+    # g128 whole tiles take the 2-lanes-per-group reduce (and, for INT4, the group-per-lane
+    # scatter); FC_OPT_STREAM_MASK bits 6/7 force the 32-element lane kernels: bit-identical
     m = tp * 8192 * 3
     cfg = fc.FlashConfig.uniform(fc.CodecConfig(**codec))
     comm = _comm(tp, m // tp, cfg, "split")
@@ -300,7 +301,8 @@ def test_group_lane_kernels_match_lane_kernels(tp, codec):
             assert torch.equal(a.view(torch.int32), b.view(torch.int32))
         if tp == 4 and dt == torch.bfloat16:
             xr = [t.float().cpu().numpy() for t in ts]
-            oc = orc.Codec(bits=4, symmetric=codec.get("symmetric", False), rounding=codec.get("rounding", "nearest-even"))
+            oc = orc.Codec(bits=codec["bits"], symmetric=codec.get("symmetric", False),
+                           rounding=codec.get("rounding", "nearest-even"))
             ref = orc.flash_all_reduce(xr, oc, oc).outputs[0]
             assert np.array_equal(_bits(outs[0][2].cpu().numpy()), _bits(ref))
     comm.close()

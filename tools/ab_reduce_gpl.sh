@@ -10,7 +10,9 @@ from paper_2412_04964_b200 import _lib
 from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for
 from bench import _events_time
 st = torch.cuda.current_stream()
-for tp, m, dt, cfg in ((8, 8 * 1024 * 8192, torch.bfloat16, fc.FlashConfig.from_bits(4)),
+for tp, m, dt, cfg in ((4, 1024 * 8192, torch.float16, fc.FlashConfig.from_bits(8)),
+                       (8, 8 * 1024 * 8192, torch.bfloat16, fc.FlashConfig.from_bits(8)),
+                       (8, 8 * 1024 * 8192, torch.bfloat16, fc.FlashConfig.from_bits(4)),
                        (4, 8 * 1024 * 8192, torch.float16, fc.FlashConfig.from_bits(4)),
                        (8, 8 * 1024 * 8192, torch.bfloat16,
                         fc.FlashConfig.uniform(fc.CodecConfig(bits=4, symmetric=True))), (8, 8 * 1024 * 8192, torch.bfloat16, fc.FlashConfig.uniform(fc.CodecConfig(bits=4, rounding="ceil")))):
@@ -28,6 +30,6 @@ for tp, m, dt, cfg in ((8, 8 * 1024 * 8192, torch.bfloat16, fc.FlashConfig.from_
         comm.set_option(_lib.OPT_PHASES, 2)
         for _ in range(3): step()
         ms, _ = _events_time(step, 20, st)
-        print(f"tp{tp} {dt} sym={cfg.stage1_codec.symmetric} mask {mask}: reduce {ms*1e3:.1f} us bitexact {ok}", flush=True)
+        print(f"tp{tp} {dt} int{cfg.stage1_codec.bits} sym={cfg.stage1_codec.symmetric} mask {mask}: reduce {ms*1e3:.1f} us bitexact {ok}", flush=True)
     comm.close()
 PY
