@@ -150,7 +150,7 @@ typedef enum {
   FC_OPT_SCATTER_STAGES = 7,/* ring depth of the streaming scatter / quantize kernel (0 = auto) */
   FC_OPT_GATHER_STAGES = 8, /* ring depth of the streaming gather / dequantize kernel (0 = auto) */
   FC_OPT_CTAS_PER_SM = 9,   /* cap on resident CTAs per SM of the streaming kernels (0 = occupancy) */
-  FC_OPT_STREAM_MASK = 10,  /* testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels; bits 6/7: INT4 g=128 scatter/reduce on the 32-element lane layout */
+  FC_OPT_STREAM_MASK = 10,  /* A/B testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels; bit 4: INT8 g=128 scatter on the group-per-lane kernel; bit 5: its code stores direct (not staged); bits 6/7: g=128 scatter/reduce on the 32-element lane layout */
   FC_OPT_PHASES = 11,       /* measurement only: run just these phases (bit 0/1/2) of a one-GPU split call */
   FC_OPT_ROLE_WEIGHTS = 12, /* fused stream kernel CTA roles: scatter | reduce << 8 | gather << 16 (sum <= 16) */
   FC_OPT_ONESHOT = 13,      /* one GPU: small calls as one cooperative launch with grid barriers (default 1) */

@@ -46,7 +46,7 @@ struct FlashArgs {
   uint32_t role_pat;        // 2 bits per slot: 0 scatter, 1 reduce, 2 gather
   int q_stages_f, r_stages_f, d_stages_f;  // fused stream kernel ring depths per role
   int sys_scope;            // flags cross GPUs: system-scope fences; else gpu scope (one GPU)
-  int dbg;                  // FC_OPT_STREAM_MASK: bits 6/7 select the 32-element-lane INT4 g128 scatter/reduce (A/B)
+  int dbg;                  // FC_OPT_STREAM_MASK A/B bits (include/flashcomm.h)
   DevCodec c1, c2;
   int mode;                 // 0: flash all-reduce; 1: single-GPU codec job (in[0] -> out[0], c1)
   uint32_t* cerr;           // mode 1: error word

@@ -627,19 +627,43 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
 #pragma unroll
           for (int c = 0; c < NC; ++c) chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax, w + c * CWPC);
         }
-        // every shared load has been consumed (the codes depend on all of them)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * st);
         if constexpr (S1::SYM) {
           const uint32_t xr = rep_xor(a.c1);
 #pragma unroll
           for (int i = 0; i < NC * CWPC; ++i) w[i] ^= xr;
         }
         unswizzle_chunks<NC, CWPC>(w, m);
-        uint8_t* cd = jb.dst + p0 * S1::SB / 8;
+        constexpr int NV = NC * CWPC / 4;      // 16-B code vectors per lane
+        constexpr int CB = 16 * NV;            // code bytes per lane (group)
+        if (!(a.dbg & 32)) {
+          // coalesced code stores: the warp's 32 groups of codes are contiguous in the slot;
+          // stage them in the lanes' own (consumed) input regions, vector v at slot v ^ m,
+          // then copy the warp's 32 * CB bytes out 512 B per instruction
+          __syncwarp();  // every lane's shared loads of its group are consumed
 #pragma unroll
-        for (int v = 0; v < NC * CWPC / 4; ++v)
-          *reinterpret_cast<uint4*>(cd + 16 * v) = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+          for (int v = 0; v < NV; ++v)
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(gb + 16 * (v ^ m)), "r"(w[4 * v]),
+                         "r"(w[4 * v + 1]), "r"(w[4 * v + 2]), "r"(w[4 * v + 3])
+                         : "memory");
+          __syncwarp();
+          const uint32_t wb = sbase + st * STAGE + part * 32 * (kGplG * 2);
+          uint8_t* cw0 = jb.dst + ((int64_t)it.t * kTileElems + part * 32 * kGplG) * S1::SB / 8;
+#pragma unroll
+          for (int r = 0; r < NV; ++r) {
+            const int x = 512 * r + 16 * lane, l = x / CB, v = (x % CB) / 16;
+            st_v4(cw0 + x, lds128_(wb + l * (kGplG * 2) + 16 * (v ^ (l & 7))));
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        } else {
+          // every shared load has been consumed (the codes depend on all of them)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty0 + 8 * st);
+          uint8_t* cd = jb.dst + p0 * S1::SB / 8;
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            *reinterpret_cast<uint4*>(cd + 16 * v) = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+        }
         const int64_t grp = p0 >> a.c1.gshift;
         *reinterpret_cast<unsigned short*>(jb.dst + a.c1.scales_off + 2 * grp) = g.s16;
         if constexpr (!S1::SYM) jb.dst[a.c1.zeros_off + grp] = (uint8_t)g.z;
