@@ -250,11 +250,12 @@ static fc_status quant_stream(const T* x, int64_t n, const DevCodec& dc, uint8_t
 template <typename T, class Spec>
 static fc_status dequant_stream(const uint8_t* src, int64_t n, const DevCodec& dc, T* out, cudaStream_t st) {
   FlashArgs a = codec_args(src, out, n, dc, nullptr);
-  a.stages = 6;
+  a.stages = dstream_stages<Spec>();
   const int smem = a.stages * ((int)dstage_bytes(dc) + 16);
   const void* k = (const void*)k_dstream<T, Spec>;
   FC_TRY(ensure_smem_attr(k, smem));
-  k_dstream<T, Spec><<<stream_grid_cur(k, kStreamThreads, smem, a.tiles), kStreamThreads, smem, st>>>(a);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.tiles, (int64_t)kDCtasPerSm * cur_sms()));
+  k_dstream<T, Spec><<<grid, kStreamThreads, smem, st>>>(a);
   return FC_OK;
 }
 
