@@ -513,7 +513,8 @@ fc_status host_pipeline(fc_comm* c, const void* const* hin, void* const* hout, i
   const int ein = dtype_size(in_dt), eout = dtype_size(out_dt);
   int lead[kMaxRanks];  // the first active rank on each rank's device owns that device's streams
   for (int r = 0; r < N; ++r) {
-    lead[r] = r;
+    lead[r] = active(r) ? r : -1;
+    if (!active(r)) continue;
     for (int q = 0; q < r; ++q)
       if (active(q) && c->devices[q] == c->devices[r]) {
         lead[r] = q;
@@ -580,7 +581,7 @@ fc_status host_pipeline(fc_comm* c, const void* const* hin, void* const* hout, i
       for (int q = 0; q < N; ++q) {
         if (!active(q)) continue;
         bool last_of_dev = true;  // one wait per (device, source device): the last copy queued there
-        for (int q2 = q + 1; q2 < N; ++q2) last_of_dev &= lead[q2] != lead[q];
+        for (int q2 = q + 1; q2 < N; ++q2) last_of_dev &= !(active(q2) && lead[q2] == lead[q]);
         if (last_of_dev) FC_CUDA_TRY(cudaStreamWaitEvent(c->hs_comp[r], ev(k, q, 0), 0));
       }
     }

@@ -143,8 +143,12 @@ def _ipc_host_worker(rank, world, port, q):
                                                                                cfg.stage2_codec))
         comm.set_timeout(30.0)
         comm.set_option(_lib.OPT_HOST_CHUNK_BYTES, 48 << 10)  # many chunks, same on every rank
-        hs = _case(n, m, torch.bfloat16, seed=11)
-        ref = orc.flash_all_reduce([h.float().numpy() for h in hs], orc.Codec(bits=4), orc.Codec(bits=4)).outputs[0]
+        for variant in range(3):  # fresh inputs every call: a chunk run that read stale staging would show
+            hs = _case(n, m, torch.bfloat16, seed=11 + variant)
+            ref = orc.flash_all_reduce([h.float().numpy() for h in hs], orc.Codec(bits=4), orc.Codec(bits=4)).outputs[0]
+            got = comm.all_reduce_host_rank(hs[rank], cfg, out_dtype=torch.float32)
+            bad = (got != torch.from_numpy(ref)).nonzero().ravel()
+            assert bad.numel() == 0, (variant, bad.numel(), bad[:4].tolist(), m)
         for odt in (torch.bfloat16, torch.float32):
             want = torch.from_numpy(ref).to(odt)
             for order in range(3):  # host, device, host: no state leaks between the two forms
