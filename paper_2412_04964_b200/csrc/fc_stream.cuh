@@ -841,6 +841,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     const uint32_t lb = st_base + li * (kRgEpl * 2);
     // ---- own group: stage-1 QDQ
     uint32_t own[NW];
+    const uint32_t own_park = obuf + warp * (32 * kRgEpl * 2) + lane * (kRgEpl * 2);
     float s1;
     uint32_t z1;
     bool bad;
@@ -899,6 +900,13 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
           chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax1, own + c * CWPC);
       }
       unswizzle_chunks<NC, CWPC>(own, m);
+      // park the own codes in the lane's (still unused) output staging slot until their rank
+      // position comes up in the sum: 8-16 registers fewer across the source loop
+#pragma unroll
+      for (int v = 0; v < NW / 4; ++v)
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(own_park + 16 * v), "r"(own[4 * v]),
+                     "r"(own[4 * v + 1]), "r"(own[4 * v + 2]), "r"(own[4 * v + 3])
+                     : "memory");
       s1 = g.s;
       z1 = g.z;
     }
@@ -909,7 +917,16 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     uint32_t pbar = bar0, src = st_base + kTileElems * 2;
     for (int s = 0; s < a.world; ++s) {
       if (s == j) {  // uniform
-        decode_words<SB, NW>(own, s1, 8388608.0f + (float)z1, acc);
+        uint32_t ow[NW];
+#pragma unroll
+        for (int v = 0; v < NW / 4; ++v) {
+          const uint4 u = lds128_(own_park + 16 * v);
+          ow[4 * v] = u.x;
+          ow[4 * v + 1] = u.y;
+          ow[4 * v + 2] = u.z;
+          ow[4 * v + 3] = u.w;
+        }
+        decode_words<SB, NW>(ow, s1, 8388608.0f + (float)z1, acc);
       } else {
         pbar += 8;
         mbar_wait(pbar, ph);
@@ -1438,7 +1455,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
 
 // g = 128 reduce, two lanes per group (r_role_gpl); one storage width, whole tiles only
 template <typename Tin, typename Tout, class S1, class S2>
-__global__ void __launch_bounds__(kGplThreads, 2) k_rstream_gpl(FlashArgs a) {
+__global__ void __launch_bounds__(kGplThreads, 3) k_rstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   if constexpr (sizeof(Tout) == 2 && S1::SB == S2::SB)
     r_role_gpl<Tin, Tout, S1, S2>(a, smem_u32(smem), a.stages,
