@@ -76,6 +76,64 @@ def load_peaks() -> dict:
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
 
+class NvmlClockSampler:
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every
+    ~1 ms from a background thread DURING the timed region (a 20-step C2 run is
+    ~12 ms, shorter than nvidia-smi's sampling period). Falls back to the
+    nvidia-smi sampler when NVML is unavailable."""
+
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+             ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.stop_flag = threading.Event()
+        self.thread = None
+        self.fallback = None
+
+    def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            masks = [(nm, getattr(pynvml, attr, 0)) for nm, attr in self.NAMES]
+
+            def run():
+                while not self.stop_flag.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+                        rs = get_reasons(self.h)
+                        self.samples.append((sm, [nm for nm, m in masks if m and (rs & m)]))
+                    except Exception:
+                        pass
+                    time.sleep(0.001)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.fallback = ClockSampler(self.index)
+            self.fallback.start()
+
+    def stop(self) -> dict:
+        if self.fallback is not None:
+            return self.fallback.stop()
+        self.stop_flag.set()
+        self.thread.join(timeout=2)
+        sms = [sm for sm, _ in self.samples]
+        reasons = sorted({r for _, rs in self.samples for r in rs})
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": self.max_sm,
+                "reasons": reasons, "samples": len(sms), "source": "nvml, ~1 ms period"}
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
 
@@ -319,7 +377,7 @@ def bench_local(args, cfg, peaks):
         step()
     comm.check()
     launches_per_step = comm.get_option(_lib.OPT_LAST_LAUNCHES)
-    clocks = ClockSampler(0)
+    clocks = NvmlClockSampler(0)
     clocks.start()
     ms, per = _events_time(step, args.steps, stream)
     clk = clocks.stop()
@@ -508,7 +566,7 @@ def bench_dist(args, cfg, peaks):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t)
 
-    clocks = ClockSampler(local)
+    clocks = NvmlClockSampler(local)
     clocks.start()
     ms = timed(lambda: comm.all_reduce(x, fcfg, out=out))
     clk = clocks.stop()
