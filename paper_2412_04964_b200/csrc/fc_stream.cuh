@@ -1271,10 +1271,10 @@ __device__ __forceinline__ void decode8(uint2 cw, float s, float mz, float v[8])
 
 // The write-dominated gather runs fastest with ~26-42 KB of code reads in flight per SM
 // from a single CTA: more CTAs / deeper rings put more concurrent read streams against
-// its output writes (C2: 201 µs at 1 CTA x 6 stages vs 222 µs at 3 x 6; tools/gather_sweep.sh)
+// its output writes (C2: 198-201 µs at 1 CTA x 6-7 stages vs 222 µs at 3 x 6; tools/gather_sweep.sh)
 constexpr int kDCtasPerSm = 1;
 template <class S2>
-constexpr int dstream_stages() { return S2::SB == 4 ? 6 : 5; }
+constexpr int dstream_stages() { return S2::SB == 4 ? 7 : 5; }
 
 // dequantize job y: quantized source, output span
 template <typename Tout>

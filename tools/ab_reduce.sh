@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B of the reduce kernel's ring depth (FC_OPT_REDUCE_STAGES) at C2; bit-exactness checked.
 cd ${GRAFT_REPO_ROOT:-.}
-python - <<'PY'
+C1=${C1:-} python - <<'PY'
 import sys, torch
 sys.path.insert(0, ".")
 import paper_2412_04964_b200 as fc
@@ -9,8 +9,9 @@ from paper_2412_04964_b200 import _lib
 from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for
 from bench import _events_time
 st = torch.cuda.current_stream()
-tp, m = 8, 8 * 1024 * 8192
-cfg = fc.FlashConfig.from_bits(4)
+import os
+tp, m, bits = (4, 1024 * 8192, 8) if os.environ.get("C1") else (8, 8 * 1024 * 8192, 4)
+cfg = fc.FlashConfig.from_bits(bits)
 comm = FlashComm.local([0] * tp, slot_bytes_for(m // tp, cfg.stage1_codec, cfg.stage2_codec))
 ins = [torch.randn(m, device="cuda").to(torch.bfloat16) for _ in range(tp)]
 outs = [torch.empty_like(t) for t in ins]

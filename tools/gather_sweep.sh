@@ -9,7 +9,7 @@ from paper_2412_04964_b200 import _lib
 from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for
 from bench import _events_time
 st = torch.cuda.current_stream()
-for tp, m, bits in ((8, 8 * 1024 * 8192, 4), (8, 8 * 1024 * 8192, 8)):
+for tp, m, bits in ((8, 8 * 1024 * 8192, 4),):
     cfg = fc.FlashConfig.from_bits(bits)
     comm = FlashComm.local([0] * tp, slot_bytes_for(m // tp, cfg.stage1_codec, cfg.stage2_codec))
     ins = [torch.randn(m, device="cuda").to(torch.bfloat16) for _ in range(tp)]
@@ -17,8 +17,8 @@ for tp, m, bits in ((8, 8 * 1024 * 8192, 4), (8, 8 * 1024 * 8192, 8)):
     step = lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False)
     comm.set_option(_lib.OPT_FUSED, 0)
     comm.set_option(_lib.OPT_PHASES, 4)
-    for cap in (1, 0):
-        for ds in (2, 3, 4, 5, 6):
+    for cap in (1,):
+        for ds in (5, 6, 7, 8):
             comm.set_option(_lib.OPT_CTAS_PER_SM, cap)
             comm.set_option(_lib.OPT_GATHER_STAGES, ds)
             for _ in range(2): step()
