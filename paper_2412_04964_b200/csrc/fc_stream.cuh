@@ -757,17 +757,21 @@ __device__ __forceinline__ float acc_get(const uint64_t* acc, int e) {
 // accumulate and re-encode never move registers). Own-group stage-1 QDQ
 // (collectives.py:364-365), rank-ordered fp32 sum (collectives.py:182-187),
 // stage-2 quantize, peers' gather slots, own output. Whole tiles only
-// (launch_rstream falls back to r_role otherwise). The lane's own input is read
-// XOR-swizzled (conflict-free) and its output leaves through the same 128-B
-// region of the stage, then one coalesced copy per warp.
+// (launch_rstream falls back to r_role otherwise). Two rings: two own-input
+// slots (the next tile's own input lands while this one runs; the lane's
+// 128-B region of its slot parks its own codes during the sum and stages its
+// output, XOR-swizzled, before one coalesced copy per warp) and one slot for
+// the N-1 peer pieces, handed back right after the source loop.
 constexpr int kRgEpl = 64;                              // elements per lane
 constexpr int kRgLpg = kGplG / kRgEpl;                  // lanes per group (2)
 constexpr int kRgWpt = kTileElems / (32 * kRgEpl);      // warps per tile (4)
 
-// byte offset of the output staging after the rings and barriers, and the total bytes
-__host__ __device__ inline uint32_t rg_obuf_off(uint32_t ring_bytes) { return (ring_bytes + 127u) & ~127u; }
-__host__ __device__ inline uint32_t rg_smem_bytes(uint32_t ring_bytes) {
-  return rg_obuf_off(ring_bytes) + kGplWarps * 32 * kRgEpl * 2;
+// peer slot bytes and total shared memory of the group-lane reduce (2 own slots + 1 peer slot)
+__host__ __device__ inline uint32_t rg_peer_bytes(const DevCodec& c1, int world) {
+  return (uint32_t)(world - 1) * (peer_codes_bytes(c1) + peer_meta_bytes(c1));
+}
+__host__ __device__ inline uint32_t rg2_smem_bytes(const DevCodec& c1, int world) {
+  return 2 * kTileElems * 2 + rg_peer_bytes(c1, world) + 8 * (4 + world);
 }
 
 template <typename Tin, typename Tout, class S1, class S2, class Iter>
@@ -779,37 +783,45 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   constexpr int NC = kRgEpl / 8;         // 8-element chunks per lane
   constexpr int CWPC = SB / 4;           // code words per chunk
   constexpr int NW = NC * CWPC;          // code words per lane
-  const uint32_t SBY = rstage_bytes(a.c1, a.world);
   const uint32_t PC = peer_codes_bytes(a.c1), PM = peer_meta_bytes(a.c1), SCB = peer_scale_bytes(a.c1);
   const int NP = a.world;
-  const uint32_t full0 = sbase + S * SBY, empty0 = full0 + 8 * S * NP;
-  const uint32_t obuf = rg_obuf_off(S * SBY + 8 * S * (NP + 1)) + sbase;  // output staging, 4 KB per warp
+  // two rings: own-input slots (2 x 16 KB: the next tile's own input lands while this one
+  // runs; a slot also stages the lane's parked own codes and its output) and one slot for
+  // the N-1 peer pieces (handed back right after the source loop)
+  const uint32_t peer0 = sbase + 2 * kTileElems * 2;
+  const uint32_t bars = peer0 + rg_peer_bytes(a.c1, a.world);
+  const uint32_t own_full = bars, own_empty = bars + 16, peer_full = bars + 32, peer_empty = peer_full + 8 * (NP - 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S * NP; ++s) mbar_init(full0 + 8 * s, 1);
-    for (int s = 0; s < S; ++s) mbar_init(empty0 + 8 * s, kRgWpt);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(own_full + 8 * s, 1);
+      mbar_init(own_empty + 8 * s, kRgWpt);
+    }
+    for (int s = 0; s < NP - 1; ++s) mbar_init(peer_full + 8 * s, 1);
+    mbar_init(peer_empty, kRgWpt);
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == kGplWarps) {  // producer: the same pieces and barriers as r_role (whole tiles)
+  (void)S;
+  if (warp == kGplWarps) {  // producer
     if (lane == 0) {
-      int st = 0, k = 0;
-      uint32_t ph = 0;
+      int k = 0;
       for (Iter it = it0; it.ok(); it.next(), ++k) {
         const int j = a.rank_lo + it.y;
-        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
         const int64_t e0 = (int64_t)it.t * kTileElems;
         const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
         const int64_t grp0 = e0 >> a.c1.gshift;
-        const uint32_t st_base = sbase + st * SBY;
-        const uint32_t bar0 = full0 + 8 * (st * NP);
-        mbar_arrive_expect_tx(bar0, kTileElems * 2);
-        bulk_g2s(st_base, reinterpret_cast<const Tin*>(a.in[j]) + seg0 + e0, kTileElems * 2, bar0);
-        uint32_t dst = st_base + kTileElems * 2;
-        int piece = 1;
+        const int os = k & 1;
+        if (k >= 2) mbar_wait(own_empty + 8 * os, ((k >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(own_full + 8 * os, kTileElems * 2);
+        bulk_g2s(sbase + os * (kTileElems * 2), reinterpret_cast<const Tin*>(a.in[j]) + seg0 + e0, kTileElems * 2,
+                 own_full + 8 * os);
+        if (k >= 1) mbar_wait(peer_empty, (k & 1) ^ 1);
+        uint32_t dst = peer0;
+        int piece = 0;
         for (int s = 0; s < a.world; ++s) {
           if (s == j) continue;
-          const uint32_t bar = bar0 + 8 * piece++;
+          const uint32_t bar = peer_full + 8 * piece++;
           const uint8_t* slot = recv_slot(a, j, s);
           const uint32_t zb = S1::SYM ? 0u : PM - SCB;
           mbar_arrive_expect_tx(bar, PC + SCB + zb);
@@ -818,7 +830,6 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
           if (zb) bulk_g2s(dst + PC + SCB, slot + a.c1.zeros_off + grp0, zb, bar);
           dst += PC + PM;
         }
-        ring_next(st, ph, S);
       }
     }
     return;
@@ -829,23 +840,23 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   const bool lead = (li & (kRgLpg - 1)) == 0;
   const uint32_t xr1 = rep_xor(a.c1), xr2 = rep_xor(a.c2);
   const uint32_t qmax1 = (1u << a.c1.bits) - 1u, qmax2 = (1u << a.c2.bits) - 1u;
-  int st = 0;
-  uint32_t ph = 0;
-  for (Iter it = it0; it.ok(); it.next()) {
+  int k = 0;
+  for (Iter it = it0; it.ok(); it.next(), ++k) {
     const int j = a.rank_lo + it.y;
     const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
     const int64_t e0 = (int64_t)it.t * kTileElems;
     const int64_t p0 = e0 + li * kRgEpl;  // lane slice start in the round
-    const uint32_t st_base = sbase + st * SBY;
-    const uint32_t bar0 = full0 + 8 * (st * NP);
-    const uint32_t lb = st_base + li * (kRgEpl * 2);
+    const int os = k & 1;
+    const uint32_t own_base = sbase + os * (kTileElems * 2);
+    const uint32_t lb = own_base + li * (kRgEpl * 2);  // the lane's 128-B region of the own slot
+    const uint32_t ph = k & 1;                          // peer-slot phase
     // ---- own group: stage-1 QDQ
     uint32_t own[NW];
-    const uint32_t own_park = obuf + warp * (32 * kRgEpl * 2) + lane * (kRgEpl * 2);
+    const uint32_t own_park = lb;  // consumed input region; rewritten by the output later
     float s1;
     uint32_t z1;
     bool bad;
-    mbar_wait(bar0, ph);
+    mbar_wait(own_full + 8 * os, (k >> 1) & 1);
     {
       uint32_t x[NC][4];
 #pragma unroll
@@ -914,7 +925,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     uint64_t acc[4 * NC];
 #pragma unroll
     for (int e = 0; e < 4 * NC; ++e) acc[e] = 0ull;
-    uint32_t pbar = bar0, src = st_base + kTileElems * 2;
+    uint32_t pbar = peer_full - 8, src = peer0;
     for (int s = 0; s < a.world; ++s) {
       if (s == j) {  // uniform
         uint32_t ow[NW];
@@ -955,10 +966,10 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         src += PC + PM;
       }
     }
-    // every shared load of the stage has been consumed: hand it back to the producer now, so
-    // the next tile's copies overlap the stage-2 quantize, the stores and the output
+    // every shared load of the peer slot has been consumed: hand it back to the producer now,
+    // so the next tile's pieces land during the stage-2 quantize, the stores and the output
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * st);
+    if (lane == 0) mbar_arrive(peer_empty);
     // ---- stage-2 quantize of the sum
     float lo2, hi2;
     {
@@ -1050,8 +1061,8 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     // ---- own output: the owner decodes its own payload (collectives.py:378), staged
     // through the warp's own 4-KB buffer (swizzled), then one coalesced copy
     {
-      const uint32_t ob0 = obuf + warp * (32 * kRgEpl * 2);
-      const uint32_t lo_b = ob0 + lane * (kRgEpl * 2);
+      const uint32_t ob0 = own_base + warp * (32 * kRgEpl * 2);
+      const uint32_t lo_b = lb;
 #pragma unroll
       for (int e = 0; e < 4 * NC; ++e) acc[e] = 0ull;
       decode_words<SB, NW>(w2, g2.s, 8388608.0f + (float)g2.z, acc);  // 0 + (c - z) s: exact, never -0
@@ -1075,10 +1086,10 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         const int l = 4 * v + (lane >> 3), q = lane & 7;
         st_v4(ob + 512 * v + 16 * lane, lds128_(wbase + l * (kRgEpl * 2) + 16 * (q ^ (l & 7))));
       }
-      __syncwarp();  // the copy's loads complete before the next tile's stores to the buffer
+      __syncwarp();  // the copy's loads are complete: the own slot can be refilled
+      if (lane == 0) mbar_arrive(own_empty + 8 * os);
     }
     if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
-    ring_next(st, ph, S);
   }
 }
 
