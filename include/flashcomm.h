@@ -138,10 +138,13 @@ FC_API fc_status fc_comm_ipc_open(fc_comm* comm, const void* handles /* world * 
 FC_API fc_status fc_comm_destroy(fc_comm* comm);
 
 typedef enum {
-  FC_OPT_FUSED = 0,        /* 1: one persistent kernel with per-tile flags (the streaming fused kernel when
-                              the scheme has a compile-time codec, else the staged one); 0 / -1 (default):
-                              phase-split streaming kernels (flag barriers between phases across GPUs) */
-  FC_OPT_CTAS = 1,         /* CTAs per rank for the fused kernel (0 = auto) */
+  FC_OPT_FUSED = 0,        /* -1 (default): the fused kernel (one cooperative launch per rank, per-tile
+                              flags, k_fstream) whenever ranks live on different GPUs or processes and the
+                              round is eligible (g = 128, one storage width, 16-bit in/out, whole tiles),
+                              else the phase-split streaming kernels (flag barriers between phases
+                              across GPUs); 1: the fused kernel wherever eligible (also all ranks on one
+                              GPU); 0: phase-split */
+  FC_OPT_CTAS = 1,         /* CTA cap per rank of the fused kernels (0 = auto) */
   FC_OPT_TIMEOUT_MS = 2,   /* flag-wait timeout -> ProtocolError (fabric.py:158-178); default 5000 */
   FC_OPT_LAG = 3,          /* fused schedule: tiles between a tile's scatter and its reduce (0 = auto) */
   FC_OPT_FAST = 4,         /* 0: force the generic (any group size) kernels; for testing */
@@ -152,7 +155,8 @@ typedef enum {
   FC_OPT_CTAS_PER_SM = 9,   /* cap on resident CTAs per SM of the streaming kernels (0 = occupancy) */
   FC_OPT_STREAM_MASK = 10,  /* A/B testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels; bit 4: INT8 g=128 scatter on the group-per-lane kernel; bit 5: its code stores direct (not staged); bits 6/7: g=128 scatter/reduce on the 32-element lane layout */
   FC_OPT_PHASES = 11,       /* measurement only: run just these phases (bit 0/1/2) of a one-GPU split call */
-  FC_OPT_ROLE_WEIGHTS = 12, /* fused stream kernel CTA roles: scatter | reduce << 8 | gather << 16 (sum <= 16) */
+  FC_OPT_FUSED_CHUNK = 12,  /* fused kernel schedule: tiles per chunk (step s scatters chunk s, reduces s-1,
+                               gathers s-2); 0 = auto: the whole round on one GPU, a quarter across GPUs */
   FC_OPT_ONESHOT = 13,      /* one GPU: small calls as one cooperative launch with grid barriers (default 1) */
   FC_OPT_HOST_CHUNK_BYTES = 14 /* fc_flash_all_reduce_host: H2D bytes per rank per pipeline chunk (0 = auto) */
 } fc_option;

@@ -13,6 +13,8 @@ from .codec import (
     QuantizedTensor,
     codec_from_name,
     dequantize,
+    group_params_asym,
+    group_params_sym,
     int6_flash_pair,
     mse,
     quantize,
@@ -25,6 +27,7 @@ from .collectives import (
     run_collective,
     sequential_sum,
 )
+from .bitpack import magic_dequant_identity, pack, packed_byte_len, unpack
 from .comm import FabricTopology, FlashComm, TrafficLedger, flash_ledger
 from .errors import ConfigError, CudaError, DomainError, IntegrityError, ProtocolError, QCollectivesError
 from .rotation import HadamardBlock, hadamard_apply, hadamard_inverse
@@ -53,6 +56,12 @@ __all__ = [
     "dequantize",
     "flash_all_reduce",
     "flash_ledger",
+    "group_params_asym",
+    "group_params_sym",
+    "magic_dequant_identity",
+    "pack",
+    "packed_byte_len",
+    "unpack",
     "hadamard_apply",
     "hadamard_inverse",
     "int6_flash_pair",

@@ -254,23 +254,37 @@ class QuantizedTensor:
         return cls(torch.from_numpy(host).to(dev), element_count, config)
 
     def validate(self) -> None:
-        """The reference's decode-time integrity checks (codec.py:360-382)."""
+        """The reference's decode-time integrity checks (codec.py:360-382):
+        scales finite and positive; for integer codecs narrower than their
+        storage, every code (the padding nibble of an odd count excluded,
+        bitpack.py:64-75) below 2^bits; zero points at most 2^bits - 1. One
+        device round trip."""
         cfg = self.config
         if cfg.is_passthrough:
             return
         s = self.scales.float()
-        if not bool(torch.isfinite(s).all()) or bool((s <= 0).any()):
+        dev = self.codes.device
+        bad_scale = (~torch.isfinite(s)).any() | (s <= 0).any()
+        bad_code = torch.zeros((), dtype=torch.bool, device=dev)
+        bad_zero = torch.zeros((), dtype=torch.bool, device=dev)
+        if cfg.is_int and cfg.bits < cfg.storage_bits and self.element_count:
+            lim = 1 << cfg.bits
+            if cfg.storage_bits == 4:
+                lo = self.codes & 0x0F
+                hi = self.codes >> 4
+                if self.element_count % 2:
+                    hi = hi[:-1]
+                bad_code = (lo >= lim).any() | (hi >= lim).any()
+            else:
+                bad_code = (self.codes >= lim).any()
+        if cfg.is_int and self.zeros is not None and self.zeros.numel():
+            bad_zero = (self.zeros.to(torch.int32) > (1 << cfg.bits) - 1).any()
+        flags = torch.stack([bad_scale, bad_code, bad_zero]).cpu().tolist()
+        if flags[0]:
             raise IntegrityError("scales must be finite and positive")
-        if not cfg.is_int:
-            return
-        if cfg.storage_bits == 4 and cfg.bits < 4 and self.element_count:
-            lo = self.codes & 0x0F
-            hi = self.codes >> 4
-            if int(torch.maximum(lo, hi).max()) >= (1 << cfg.bits):
-                raise IntegrityError(f"code exceeds {cfg.bits}-bit range")
-        if cfg.storage_bits == 8 and cfg.bits < 8 and int(self.codes.max()) >= (1 << cfg.bits):
+        if flags[1]:
             raise IntegrityError(f"code exceeds {cfg.bits}-bit range")
-        if self.zeros is not None and int(self.zeros.max()) > (1 << cfg.bits) - 1:
+        if flags[2]:
             raise IntegrityError(f"zero point exceeds {cfg.bits}-bit range")
 
 
@@ -297,9 +311,14 @@ def quantize(x, config: CodecConfig, *, check: bool = True) -> QuantizedTensor:
     return QuantizedTensor(buf, n, config)
 
 
-def dequantize(q: QuantizedTensor, dtype: torch.dtype = torch.float32, *, validate: bool = False) -> torch.Tensor:
+def dequantize(q: QuantizedTensor, dtype: torch.dtype = torch.float32, *, validate: bool = True) -> torch.Tensor:
     """Decode to a flat tensor (codec.py:354-384). float32 output equals the
-    reference bit for bit; bf16/fp16 outputs are its RNE rounding."""
+    reference bit for bit; bf16/fp16 outputs are its RNE rounding.
+
+    Like the reference, the integrity checks run by default and raise
+    IntegrityError for corrupt payloads (codec.py:360-382; one device round
+    trip). validate=False skips them and keeps the call asynchronous (for
+    callers that produced the payload themselves)."""
     if validate:
         q.validate()
     c = q.config.to_fc()
@@ -308,6 +327,40 @@ def dequantize(q: QuantizedTensor, dtype: torch.dtype = torch.float32, *, valida
         _lib.check(_lib.lib().fc_dequantize(q._buf.data_ptr(), q.element_count, C.byref(c), out.data_ptr(),
                                             fc_dtype(dtype), _stream_of(out)))
     return out
+
+
+def group_params_asym(group, bits: int, scale_floor: float = 1e-8) -> tuple[float, int]:
+    """Raw (unsnapped) affine parameters of one group (codec.py:251-262):
+    scale = max((max - min) / (2^bits - 1), floor), zero = clip(ceil(-min /
+    scale), 0, 2^bits - 1), in float64. A tests-only scalar API in the
+    reference; the kernels compute the fp16-snapped form (_wire_scale)."""
+    if not 2 <= int(bits) <= 8:
+        raise DomainError(f"bits must be in 2..8, got {bits}")
+    g = _flat_f64(group)
+    lo, hi = float(g.min()), float(g.max())
+    scale = max((hi - lo) / (2 ** int(bits) - 1), scale_floor)
+    zero = int(min(max(np.ceil(np.float64(-lo) / np.float64(scale)), 0), 2 ** int(bits) - 1))
+    return float(scale), zero
+
+
+def group_params_sym(group, bits: int, scale_floor: float = 1e-8) -> float:
+    """Raw symmetric scale of one group: max(absmax / (2^(bits-1) - 1), floor)
+    (codec.py:265-270)."""
+    if not 2 <= int(bits) <= 8:
+        raise DomainError(f"bits must be in 2..8, got {bits}")
+    g = _flat_f64(group)
+    return float(max(float(g.abs().max()) / (2 ** (int(bits) - 1) - 1), scale_floor))
+
+
+def _flat_f64(x) -> torch.Tensor:
+    """float64 flat view, DomainError for empty / non-finite input (codec.py:226-232)."""
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, np.float64))
+    t = t.reshape(-1).to(torch.float64)
+    if t.numel() == 0:
+        raise DomainError("input tensor is empty")
+    if not bool(torch.isfinite(t).all()):
+        raise DomainError("input contains NaN or infinity")
+    return t
 
 
 def mse(a, b) -> float:

@@ -133,6 +133,21 @@ def exchange_handles(my_handle: bytes, group=None) -> bytes:
     return b"".join(bytes(h) for h in got)
 
 
+def _check_out(o: torch.Tensor, n: int, dtype: torch.dtype, device: int, what: str) -> None:
+    """Caller-supplied output buffers: the kernels write n elements of `dtype`
+    through a raw pointer, so size, dtype, layout and device are checked here."""
+    if not isinstance(o, torch.Tensor):
+        raise DomainError(f"{what} must be a tensor")
+    if o.numel() != n:
+        raise DomainError(f"{what} holds {o.numel()} elements, expected {n}")
+    if o.dtype != dtype:
+        raise DomainError(f"{what} dtype {o.dtype} != {dtype}")
+    if not o.is_contiguous():
+        raise DomainError(f"{what} must be contiguous")
+    if o.get_device() != device:
+        raise DomainError(f"{what} must live on cuda:{device}")
+
+
 def _device_index(d) -> int:
     if isinstance(d, torch.device):
         return d.index if d.index is not None else torch.cuda.current_device()
@@ -246,8 +261,14 @@ class FlashComm:
             if not t.is_contiguous():
                 raise DomainError(f"rank {r} tensor must be contiguous")
         odt = out_dtype or dt
+        fc_dtype(odt)
         if outs is None:
             outs = [torch.empty(n, dtype=odt, device=t.device) for t in ins]
+        else:
+            if len(outs) != self.world_size:
+                raise ProtocolError(f"expected {self.world_size} output tensors, got {len(outs)}")
+            for r, o in enumerate(outs):
+                _check_out(o, n, odt, self.devices[r], f"rank {r} output")
         N = self.world_size
         arr = _ptr_array(N)
         pin = arr(*[t.data_ptr() for t in ins])
@@ -336,11 +357,16 @@ class FlashComm:
         out may be `tensor` (in place). Asynchronous unless check=True."""
         if self.rank is None:
             raise ConfigError("all_reduce needs an IPC communicator (from_process_group)")
+        if tensor.get_device() != self.devices[self.rank]:
+            raise DomainError(f"tensor must live on cuda:{self.devices[self.rank]}")
         if not tensor.is_contiguous():
             raise DomainError("tensor must be contiguous")
         odt = out_dtype or tensor.dtype
+        fc_dtype(odt)
         if out is None:
             out = torch.empty_like(tensor, dtype=odt)
+        else:
+            _check_out(out, tensor.numel(), odt, self.devices[self.rank], "out")
         c = self._cfg(cfg)
         st = torch.cuda.current_stream(tensor.device).cuda_stream
         _lib.check(_lib.lib().fc_flash_all_reduce(self._h, tensor.data_ptr(), out.data_ptr(), tensor.numel(),

@@ -326,7 +326,7 @@ fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
     case FC_OPT_STREAM_MASK: c->stream_mask = value & 255; break;
     case FC_OPT_PHASES: c->phases = value & 7; break;
     case FC_OPT_ONESHOT: c->oneshot = value != 0; break;
-    case FC_OPT_ROLE_WEIGHTS: c->role_weights = value; break;
+    case FC_OPT_FUSED_CHUNK: c->fused_chunk = std::max<int64_t>(0, value); break;
     case FC_OPT_HOST_CHUNK_BYTES: c->host_chunk_bytes = std::max<int64_t>(0, value); break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
@@ -349,7 +349,7 @@ fc_status fc_comm_get_option(fc_comm* c, int32_t option, int64_t* value) {
     case FC_OPT_STREAM_MASK: *value = c->stream_mask; break;
     case FC_OPT_PHASES: *value = c->phases; break;
     case FC_OPT_ONESHOT: *value = c->oneshot; break;
-    case FC_OPT_ROLE_WEIGHTS: *value = c->role_weights; break;
+    case FC_OPT_FUSED_CHUNK: *value = c->fused_chunk; break;
     case FC_OPT_HOST_CHUNK_BYTES: *value = c->host_chunk_bytes; break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }

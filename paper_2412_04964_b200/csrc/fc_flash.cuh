@@ -42,9 +42,9 @@ struct FlashArgs {
   int stage_hint;           // host-side override of the reduce ring depth (0 = auto)
   int q_hint, d_hint;       // ring depths of the streaming scatter / gather kernels (0 = auto)
   int cta_cap;              // resident CTAs per SM cap for the streaming kernels (0 = occupancy)
-  int role_period;          // fused stream kernel: CTA role pattern length (<= 16)
-  uint32_t role_pat;        // 2 bits per slot: 0 scatter, 1 reduce, 2 gather
-  int q_stages_f, r_stages_f, d_stages_f;  // fused stream kernel ring depths per role
+  int fp_chunk;             // fused stream kernel: tiles per schedule chunk
+  int fp_bars;              // fused stream kernel: byte offset of the barrier region in shared memory
+  int q_stages_f, d_stages_f;  // fused stream kernel ring depths of the scatter / gather roles
   int sys_scope;            // flags cross GPUs: system-scope fences; else gpu scope (one GPU)
   int dbg;                  // FC_OPT_STREAM_MASK A/B bits (include/flashcomm.h)
   DevCodec c1, c2;

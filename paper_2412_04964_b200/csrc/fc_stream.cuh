@@ -242,9 +242,9 @@ struct RangeIter {
 // producers run ahead of its consumers.
 struct RoundIter {
   int i, items, y, t, P, dy, dt, step;
-  __device__ __forceinline__ RoundIter(int items_, int P_, int first, int step_)
+  __device__ __forceinline__ RoundIter(int items_, int P_, int first, int step_, int t0 = 0)
       : i(first), items(items_), P(P_), step(step_) {
-    t = first / P;
+    t = t0 + first / P;
     y = first - t * P;
     dt = step / P;
     dy = step - dt * P;
@@ -296,7 +296,24 @@ __device__ __forceinline__ bool warp_wait_flags(const FlashArgs& a, int rank, co
 
 // consumer warps only (named barrier 1): every consumer thread's stores of this
 // item happen before thread 0's system-scope fence and flag stores
-__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
+template <int NT = kThreads>
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+
+// publish one per-tile flag after a named-barrier sync of the threads whose
+// stores it covers: system scope (fence.sc.sys, then a relaxed sys store) when
+// the flag crosses GPUs, else a gpu-scope release store
+__device__ __forceinline__ void publish_flag(const FlashArgs& a, uint32_t* f, uint32_t ep) {
+  if (a.sys_scope) {
+    __threadfence_system();
+    st_relaxed_sys(f, ep);
+  } else {
+    st_release_gpu(f, ep);
+  }
+}
+
+__device__ __forceinline__ void mbar_inval(uint32_t bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
 
 // ------------------------------------------------------------------ ring setup
 
@@ -528,13 +545,13 @@ __device__ __forceinline__ void unswizzle_chunks(uint32_t* w, int m) {
   }
 }
 
-template <typename Tin, class S1, class Iter>
-__device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
+template <typename Tin, class S1, bool FUSED, class Iter>
+__device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0, uint32_t bars = 0) {
   static_assert(sizeof(Tin) == 2, "16-bit inputs");
   constexpr uint32_t STAGE = kTileElems * 2;
   constexpr int NC = kGplG / 8;      // 8-element chunks per group
   constexpr int CWPC = S1::SB / 4;   // code words per chunk
-  const uint32_t full0 = sbase + S * STAGE, empty0 = full0 + 8 * S;
+  const uint32_t full0 = bars ? bars : sbase + S * STAGE, empty0 = full0 + 8 * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -647,6 +664,7 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
                          : "memory");
           __syncwarp();
           const uint32_t wb = sbase + st * STAGE + part * 32 * (kGplG * 2);
+          fence_proxy_async_smem();  // generic st.shared before the stage's next bulk (async-proxy) fill
           uint8_t* cw0 = jb.dst + ((int64_t)it.t * kTileElems + part * 32 * kGplG) * S1::SB / 8;
 #pragma unroll
           for (int r = 0; r < NV; ++r) {
@@ -668,6 +686,15 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
         *reinterpret_cast<unsigned short*>(jb.dst + a.c1.scales_off + 2 * grp) = g.s16;
         if constexpr (!S1::SYM) jb.dst[a.c1.zeros_off + grp] = (uint8_t)g.z;
         if (bad && jb.err) atomicOr(jb.err, jb.ecode);
+        if constexpr (FUSED) {
+          // both warps of this slot stored their 32 groups of the tile: publish rflag[j][r][t]
+          asm volatile("bar.sync %0, %1;" ::"r"(2 + slot), "n"(32 * kGplWpt) : "memory");
+          if (part == 0 && lane == 0) {
+            int r, j;
+            pair_of(a, it.y, r, j);
+            publish_flag(a, rflag(a, j, r) + it.t, flag_epoch(a));
+          }
+        }
       } else {
         // ragged tail: the 32-element lane codec over this warp's 4096 elements, 1024 at a time
         bool bad = false;
@@ -683,6 +710,14 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * st);
         if (bad && jb.err) atomicOr(jb.err, jb.ecode);
+        if constexpr (FUSED) {
+          asm volatile("bar.sync %0, %1;" ::"r"(2 + slot), "n"(32 * kGplWpt) : "memory");
+          if (part == 0 && lane == 0) {
+            int r, j;
+            pair_of(a, it.y, r, j);
+            publish_flag(a, rflag(a, j, r) + it.t, flag_epoch(a));
+          }
+        }
       }
     }
     ring_next(st, ph, S);
@@ -774,8 +809,8 @@ __host__ __device__ inline uint32_t rg2_smem_bytes(const DevCodec& c1, int world
   return 2 * kTileElems * 2 + rg_peer_bytes(c1, world) + 8 * (4 + world);
 }
 
-template <typename Tin, typename Tout, class S1, class S2, class Iter>
-__device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
+template <typename Tin, typename Tout, class S1, class S2, bool FUSED, class Iter>
+__device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0, uint32_t bars_in = 0) {
   static_assert(sizeof(Tin) == 2 && sizeof(Tout) == 2, "16-bit inputs and outputs");
   static_assert(S1::SB == S2::SB, "one storage width for both stages");
   static_assert(kGplWarps == kRgWpt, "one tile per pass of the consumer warps");
@@ -789,7 +824,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   // runs; a slot also stages the lane's parked own codes and its output) and one slot for
   // the N-1 peer pieces (handed back right after the source loop)
   const uint32_t peer0 = sbase + 2 * kTileElems * 2;
-  const uint32_t bars = peer0 + rg_peer_bytes(a.c1, a.world);
+  const uint32_t bars = bars_in ? bars_in : peer0 + rg_peer_bytes(a.c1, a.world);
   const uint32_t own_full = bars, own_empty = bars + 16, peer_full = bars + 32, peer_empty = peer_full + 8 * (NP - 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -803,19 +838,23 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   }
   __syncthreads();
   (void)S;
-  if (warp == kGplWarps) {  // producer
-    if (lane == 0) {
-      int k = 0;
-      for (Iter it = it0; it.ok(); it.next(), ++k) {
-        const int j = a.rank_lo + it.y;
-        const int64_t e0 = (int64_t)it.t * kTileElems;
-        const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
-        const int64_t grp0 = e0 >> a.c1.gshift;
-        const int os = k & 1;
+  if (warp == kGplWarps) {  // producer (lane 0 issues; FUSED: the warp waits for the peers' tile flags)
+    int k = 0;
+    for (Iter it = it0; it.ok(); it.next(), ++k) {
+      const int j = a.rank_lo + it.y;
+      const int64_t e0 = (int64_t)it.t * kTileElems;
+      const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
+      const int64_t grp0 = e0 >> a.c1.gshift;
+      const int os = k & 1;
+      if (lane == 0) {
         if (k >= 2) mbar_wait(own_empty + 8 * os, ((k >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(own_full + 8 * os, kTileElems * 2);
         bulk_g2s(sbase + os * (kTileElems * 2), reinterpret_cast<const Tin*>(a.in[j]) + seg0 + e0, kTileElems * 2,
                  own_full + 8 * os);
+      }
+      if constexpr (FUSED)  // lanes s != j wait for rank s's stage-1 piece of tile t (rflag[j][s][t])
+        warp_wait_flags(a, j, rflag(a, j, lane) + it.t, lane, lane < a.world && lane != j, kPhReduce);
+      if (lane == 0) {
         if (k >= 1) mbar_wait(peer_empty, (k & 1) ^ 1);
         uint32_t dst = peer0;
         int piece = 0;
@@ -831,6 +870,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
           dst += PC + PM;
         }
       }
+      __syncwarp();
     }
     return;
   }
@@ -1057,6 +1097,18 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
           if constexpr (!S2::SYM) b[a.c2.zeros_off + grp] = (uint8_t)g2.z;
         }
       }
+      if constexpr (FUSED) {
+        // the 4 consumer warps stored the whole tile into every peer's gather slot [j]:
+        // publish gflag[p][j][t] for every peer p
+        consumers_sync<kGplWarps * 32>();
+        if (threadIdx.x == 0) {
+          const uint32_t ep = flag_epoch(a);
+          if (a.sys_scope) __threadfence_system();
+          else __threadfence();
+          for (int p = 0; p < a.world; ++p)
+            if (p != j) st_relaxed_sys(gflag(a, p, j) + it.t, ep);
+        }
+      }
     }
     // ---- own output: the owner decodes its own payload (collectives.py:378), staged
     // through the warp's own 4-KB buffer (swizzled), then one coalesced copy
@@ -1077,6 +1129,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
                      : "memory");
       }
       __syncwarp();
+      fence_proxy_async_smem();  // the staging st.shared before the slot's next bulk fill
       const uint32_t wbase = ob0;
       uint8_t* ob = reinterpret_cast<uint8_t*>(reinterpret_cast<Tout*>(a.out[j]) + seg0 + e0 + warp * (32 * kRgEpl));
       // byte 512 v + 16 lane of the warp's output = chunk q = lane % 8 of slice l = 4 v + lane / 8,
@@ -1324,16 +1377,25 @@ __host__ __device__ inline uint32_t dstage_bytes(const DevCodec& c) {
 // consumer thread t decodes 8-element blocks t + 256*b (b = 0..3) of the
 // tile: conflict-free shared loads and coalesced 16-B output stores.
 // FUSED: wait gflag[r][j][t] before the copies.
-template <typename Tout, class S2, bool FUSED, class Iter>
-__device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S, Iter it0) {
-  constexpr int kBlocks = kTileElems / 8 / kThreads;  // 4
+template <typename Tout, class S2, bool FUSED, class Iter, int NCW = kConsumerWarps>
+__device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S, Iter it0, uint32_t bars = 0) {
+  constexpr int NT = NCW * 32;                    // consumer threads
+  constexpr int kBlocks = kTileElems / 8 / NT;    // 8-element blocks per thread and tile (4 or 8)
+  constexpr int kHalf = kBlocks < 4 ? kBlocks : 4;  // blocks decoded per pass (register budget)
   const DevCodec& c = a.c2;
   const uint32_t SBY = dstage_bytes(c), PC = peer_codes_bytes(c), SCB = peer_scale_bytes(c);
-  const uint32_t full0 = sbase + S * SBY, empty0 = full0 + 8 * S;
+  const uint32_t full0 = bars ? bars : sbase + S * SBY, empty0 = full0 + 8 * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gs = c.gshift;
-  ring_init(full0, empty0, S);
-  if (warp == kConsumerWarps) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == NCW) {
     int st = 0, k = 0, cy = -1;
     uint32_t ph = 0;
     DJob<Tout> d;
@@ -1369,7 +1431,7 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
   const float zsym = S2::SYM ? 8388608.0f + (float)(1 << (c.bits - 1)) : 0.0f;
   const uint32_t code_off = threadIdx.x * S2::SB;                // bytes of 8 codes of SB bits
   const uint32_t grp_off = (uint32_t)(threadIdx.x * 8) >> gs;    // tile-local group of block 0
-  const uint32_t grp_step = (uint32_t)(kThreads * 8) >> gs;      // groups per block step
+  const uint32_t grp_step = (uint32_t)(NT * 8) >> gs;            // groups per block step
   int st = 0, cy = -1;
   uint32_t ph = 0;
   DJob<Tout> d;
@@ -1382,57 +1444,62 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
     const int64_t v = min(a.sub_len - e0, d.limit - e0);  // valid elements from e0
     const uint32_t tile = sbase + st * SBY;
     Tout* obase = d.out + e0 + threadIdx.x * 8;
-    uint2 cw[kBlocks];
-    float sc[kBlocks], mz[kBlocks];
     mbar_wait(full0 + 8 * st, ph);
 #pragma unroll
-    for (int b = 0; b < kBlocks; ++b) {
-      const uint32_t ca = tile + code_off + b * kThreads * S2::SB;
-      if constexpr (S2::SB == 4) {
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw[b].x) : "r"(ca));
-        cw[b].y = 0;
-      } else {
-        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(cw[b].x), "=r"(cw[b].y) : "r"(ca));
-      }
-      const uint32_t g = grp_off + b * grp_step;
-      unsigned short sh;
-      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(tile + PC + 2 * g));
-      sc[b] = __half2float(__ushort_as_half(sh));
-      if constexpr (S2::SYM) {
-        mz[b] = zsym;
-      } else {
-        uint32_t zz;
-        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(tile + PC + SCB + g));
-        mz[b] = __uint_as_float(0x4B000000u | zz);
-      }
-    }
-    float val[kBlocks][8];
+    for (int h = 0; h < kBlocks; h += kHalf) {
+      uint2 cw[kHalf];
+      float sc[kHalf], mz[kHalf];
 #pragma unroll
-    for (int b = 0; b < kBlocks; ++b) {
-      uint2 w = cw[b];
-      if constexpr (S2::SYM) {
-        w.x ^= xr;
-        w.y ^= xr;
-      }
-      decode8<S2>(w, sc[b], mz[b], val[b]);
-    }
-    // release the stage after the shared loads were consumed (see q_role)
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * st);
-    if (v >= kTileElems) {  // whole tile: no per-block checks
-#pragma unroll
-      for (int b = 0; b < kBlocks; ++b) store8(obase + b * kThreads * 8, val[b]);
-    } else {
-#pragma unroll
-      for (int b = 0; b < kBlocks; ++b) {
-        const int64_t e = (int64_t)(threadIdx.x + b * kThreads) * 8;
-        Tout* o = obase + b * kThreads * 8;
-        if (e + 8 <= v) {
-          store8(o, val[b]);
+      for (int b = 0; b < kHalf; ++b) {
+        const uint32_t ca = tile + code_off + (h + b) * NT * S2::SB;
+        if constexpr (S2::SB == 4) {
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw[b].x) : "r"(ca));
+          cw[b].y = 0;
         } else {
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(cw[b].x), "=r"(cw[b].y) : "r"(ca));
+        }
+        const uint32_t g = grp_off + (h + b) * grp_step;
+        unsigned short sh;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(tile + PC + 2 * g));
+        sc[b] = __half2float(__ushort_as_half(sh));
+        if constexpr (S2::SYM) {
+          mz[b] = zsym;
+        } else {
+          uint32_t zz;
+          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(tile + PC + SCB + g));
+          mz[b] = __uint_as_float(0x4B000000u | zz);
+        }
+      }
+      float val[kHalf][8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (e + q < v) o[q] = DT<Tout>::from_f(val[b][q]);
+      for (int b = 0; b < kHalf; ++b) {
+        uint2 w = cw[b];
+        if constexpr (S2::SYM) {
+          w.x ^= xr;
+          w.y ^= xr;
+        }
+        decode8<S2>(w, sc[b], mz[b], val[b]);
+      }
+      if (h + kHalf >= kBlocks) {
+        // release the stage after the shared loads were consumed (see q_role)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+      }
+      if (v >= kTileElems) {  // whole tile: no per-block checks
+#pragma unroll
+        for (int b = 0; b < kHalf; ++b) store8(obase + (h + b) * NT * 8, val[b]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < kHalf; ++b) {
+          const int64_t e = (int64_t)(threadIdx.x + (h + b) * NT) * 8;
+          Tout* o = obase + (h + b) * NT * 8;
+          if (e + 8 <= v) {
+            store8(o, val[b]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (e + q < v) o[q] = DT<Tout>::from_f(val[b][q]);
+          }
         }
       }
     }
@@ -1454,7 +1521,7 @@ template <typename Tin, class S1>
 __global__ void __launch_bounds__(kGplThreads, 3) k_qstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
-  q_role_gpl<Tin, S1>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+  q_role_gpl<Tin, S1, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
 template <typename Tin, typename Tout, class S1, class S2>
@@ -1469,7 +1536,7 @@ template <typename Tin, typename Tout, class S1, class S2>
 __global__ void __launch_bounds__(kGplThreads, 3) k_rstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   if constexpr (sizeof(Tout) == 2 && S1::SB == S2::SB)
-    r_role_gpl<Tin, Tout, S1, S2>(a, smem_u32(smem), a.stages,
+    r_role_gpl<Tin, Tout, S1, S2, false>(a, smem_u32(smem), a.stages,
                                   RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
@@ -1482,40 +1549,92 @@ __global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
 
 // ------------------------------------------------------------------ fused kernel
 
-// One cooperative launch: CTA roles interleaved by blockIdx with the pattern
-// a.role_pat (2 bits per slot, a.role_period slots: 0 scatter, 1 reduce, 2
-// gather). Each role walks its items tile-major and round-robin over the role's
-// CTAs, synchronised with the other roles (and, across GPUs, other ranks) only
-// through the per-tile epoch flags; all CTAs are resident, waits only target
-// producers that never wait on their consumers, so the schedule cannot deadlock.
+// smem layout of the fused kernel: one data region (the largest role's rings)
+// and one barrier region behind it, so a role's barriers never overlay
+// another role's data
+struct FusedSmem {
+  int q_stages, d_stages, data_bytes, bars_off, max_bars, total;
+};
+__host__ __device__ inline FusedSmem fused_smem(const DevCodec& c1, const DevCodec& c2, int world, int qs, int ds) {
+  FusedSmem f;
+  f.q_stages = qs;
+  f.d_stages = ds;
+  const int q = qs * kTileElems * 2;
+  const int r = 2 * kTileElems * 2 + (int)rg_peer_bytes(c1, world);
+  const int d = ds * (int)dstage_bytes(c2);
+  f.data_bytes = q > r ? (q > d ? q : d) : (r > d ? r : d);
+  f.bars_off = (f.data_bytes + 127) & ~127;
+  const int nq = 2 * qs, nr = 4 + world, nd = 2 * ds;
+  f.max_bars = nq > nr ? (nq > nd ? nq : nd) : (nr > nd ? nr : nd);
+  f.total = f.bars_off + 8 * f.max_bars;
+  return f;
+}
+
+// hand the CTA's shared memory from one role to the next: every thread's
+// generic shared stores are ordered before later bulk (async-proxy) fills, all
+// of the previous role's waits are over, its barriers are invalidated
+__device__ __forceinline__ void fused_role_switch(uint32_t bars, int nb) {
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < nb; ++i) mbar_inval(bars + 8 * i);
+}
+
+// One cooperative launch per rank (or one for all logical ranks of a GPU):
+// the paper's fused kernel. Every CTA runs the three roles
+// of the group-lane codec — scatter (q_role_gpl: stage-1 quantize, codes
+// stored straight into the owners' receive slots, peer memory over NVLink),
+// reduce (r_role_gpl: N-1 received pieces + own QDQ -> fp32 rank-ordered sum ->
+// stage-2 quantize -> every peer's gather slot) and gather (d_role: decode the
+// owners' stage-2 pieces) — synchronised only by per-tile epoch flags (rflag /
+// gflag: release after a tile's stores, acquire before its bulk copies).
+// The segment's tiles are cut into chunks of a.fp_chunk tiles; at step s a CTA
+// scatters chunk s, reduces chunk s-1 and gathers chunk s-2, so NVLink-bound
+// scatter/reduce traffic of one chunk overlaps the HBM-bound gather of an
+// earlier one. Items of a (role, chunk) are dealt round-robin over the grid
+// (rotated per chunk). Every wait targets an item of an earlier step (on any
+// rank), and all CTAs are co-resident (cooperative launch), so the schedule
+// cannot deadlock.
 template <typename Tin, typename Tout, class S1, class S2>
-__global__ void __launch_bounds__(kStreamThreads, 2) k_fstream(FlashArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int per = a.role_period;
-  const int slot = (int)blockIdx.x % per, rep = (int)blockIdx.x / per;
-  int cnt[3] = {0, 0, 0}, idx = 0, role = 0;
-  for (int k = 0; k < per; ++k) {
-    const int rk = (a.role_pat >> (2 * k)) & 3;
-    if (k == slot) {
-      role = rk;
-      idx = cnt[rk];
+__global__ void __launch_bounds__(kGplThreads, 3) k_fstream(const __grid_constant__ FlashArgs a) {
+  if constexpr (sizeof(Tin) == 2 && sizeof(Tout) == 2 && S1::SB == S2::SB) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sb = smem_u32(smem);
+    const uint32_t bars = sb + (uint32_t)a.fp_bars;
+    const int G = (int)gridDim.x, cta = (int)blockIdx.x;
+    const int nr = a.rank_hi - a.rank_lo;
+    const int P = nr * (a.world - 1);
+    const int B = a.fp_chunk;
+    const int nch = (a.tiles + B - 1) / B;
+    int nb = 0;
+#pragma unroll 1
+    for (int s = 0; s < nch + 2; ++s) {
+#pragma unroll 1
+      for (int role = 0; role < 3; ++role) {
+        const int c = s - role;
+        if (c < 0 || c >= nch) continue;
+        const int t0 = c * B, bt = min(B, a.tiles - t0);
+        const int per = role == 1 ? nr : P;
+        const int items = per * bt;
+        // item i of this (role, chunk) runs on CTA (base + i) mod G
+        const int base = (int)(((int64_t)c * per * B + (int64_t)role * (G / 3)) % G);
+        const int first = cta >= base ? cta - base : cta - base + G;
+        if (first >= items) continue;
+        fused_role_switch(bars, nb);
+        const RoundIter it(items, per, first, G, t0);
+        if (role == 0) {
+          q_role_gpl<Tin, S1, true>(a, sb, a.q_stages_f, it, bars);
+          nb = 2 * a.q_stages_f;
+        } else if (role == 1) {
+          r_role_gpl<Tin, Tout, S1, S2, true>(a, sb, 1, it, bars);
+          nb = 4 + a.world;
+        } else {
+          d_role<Tout, S2, true, RoundIter, kGplWarps>(a, sb, a.d_stages_f, it, bars);
+          nb = 2 * a.d_stages_f;
+        }
+      }
     }
-    ++cnt[rk];
   }
-  const int reps = ((int)gridDim.x + per - 1) / per;
-  // CTAs of this role: cnt[role] per full period (the last partial period contributes its share)
-  int nrole = 0;
-  for (int k = 0; k < per; ++k)
-    if (((a.role_pat >> (2 * k)) & 3) == role) nrole += (reps - 1) + (k < (int)gridDim.x - (reps - 1) * per ? 1 : 0);
-  const int first = rep * cnt[role] + idx;
-  const int npairs = (a.rank_hi - a.rank_lo) * (a.world - 1), nown = a.rank_hi - a.rank_lo;
-  const uint32_t sb = smem_u32(smem);
-  if (role == 0)
-    q_role<Tin, S1, true>(a, sb, a.q_stages_f, RoundIter(npairs * a.tiles, npairs, first, nrole));
-  else if (role == 1)
-    r_role<Tin, Tout, S1, S2, true>(a, sb, a.r_stages_f, RoundIter(nown * a.tiles, nown, first, nrole));
-  else
-    d_role<Tout, S2, true>(a, sb, a.d_stages_f, RoundIter(npairs * a.tiles, npairs, first, nrole));
 }
 
 }  // namespace fc

@@ -295,8 +295,84 @@ def make_reports(out_path: str) -> None:
     print(f"reports -> {out_path}")
 
 
+# ---------------------------------------------------------------------------
+# full-size digests: the unmodified reference at the BASELINE configs
+
+DIGEST_CASES = [
+    # (name, n_ranks, tokens, hidden, bits preset, input dtype)
+    ("c1_tp4_int8_fp16", 4, 1024, 8192, 8, "fp16"),
+    ("tp8_int8_bf16", 8, 1024, 8192, 8, "bf16"),
+    ("tp8_int6_bf16", 8, 1024, 8192, 6, "bf16"),
+    ("c2_tp8_int4_bf16", 8, 8192, 8192, 4, "bf16"),
+]
+
+
+def _sha(b) -> str:
+    import hashlib
+
+    return hashlib.sha256(bytes(memoryview(np.ascontiguousarray(b)).cast("B")) if not isinstance(b, bytes) else b).hexdigest()
+
+
+def split_wire(msgs, plen, codec):
+    """codes / scales / zeros parts of a list of per-piece wire messages, each concatenated."""
+    from qcollectives.bitpack import packed_byte_len
+
+    packed = packed_byte_len(plen, codec.storage_bits)
+    groups = codec.group_count(plen)
+    codes, scales, zeros = [], [], []
+    for m in msgs:
+        codes.append(m[:packed])
+        scales.append(m[packed:packed + 2 * groups])
+        zeros.append(m[packed + 2 * groups:])
+    return b"".join(codes), b"".join(scales), b"".join(zeros)
+
+
+def make_digests(out_path: str, only=None) -> None:
+    import time
+
+    res = {}
+    if os.path.exists(out_path):
+        with open(out_path) as fh:
+            res = json.load(fh)
+    for name, n, tokens, hidden, bits, dt in DIGEST_CASES:
+        if only and name not in only:
+            continue
+        t0 = time.time()
+        prof = qc.ActivationProfile(hidden_dim=hidden, tokens=tokens, seed=0)
+        xs = qc.gen_rank_activations(prof, n)
+        rnd = round_to_bf16 if dt == "bf16" else round_to_fp16
+        xs = [rnd(x) for x in xs]
+        cfg = qc.FlashConfig.from_bits(bits)
+        with Capture() as cap:
+            run = qc.flash_all_reduce(xs, cfg)
+        for o in run.outputs[1:]:
+            assert np.array_equal(o, run.outputs[0])
+        m = xs[0].size
+        seg = m // n
+        plen = cfg.resolve_chunk_size(n) // n
+        s1, s2 = cfg.stage1_codec, cfg.stage2_codec
+        d = {"n": n, "m": m, "tokens": tokens, "hidden": hidden, "bits": bits, "dtype": dt, "seed": 0,
+             "piece": plen, "inputs": [_sha(x.astype(np.float32)) for x in xs],
+             "out_f32": _sha(run.outputs[0].astype(np.float32)), "stage1": {}, "stage2": {},
+             "wire_bytes_per_rank": run.wire_bytes_per_rank}
+        for (src, dst), lst in sorted(cap.msgs.items()):
+            # per (src, dst) and piece: one stage-1 message, then one stage-2 message (collectives.py:359-381)
+            assert len(lst) == 2 * (seg // plen)
+            c, sc, z = split_wire(lst[0::2], plen, s1)
+            d["stage1"][f"{src}->{dst}"] = [_sha(c), _sha(sc), _sha(z)]
+            c, sc, z = split_wire(lst[1::2], plen, s2)
+            key = str(src)
+            dig = [_sha(c), _sha(sc), _sha(z)]
+            assert d["stage2"].setdefault(key, dig) == dig  # the owner sends one payload to every peer
+        res[name] = d
+        print(f"digest {name}: {time.time() - t0:.1f} s", flush=True)
+        del run, xs, cap
+        with open(out_path, "w") as fh:
+            json.dump(res, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["codec", "flash", "reports", "extras"]
+    which = sys.argv[1:] or ["codec", "flash", "reports", "extras", "digests"]
     if "codec" in which:
         make_codec(os.path.join(HERE, "codec.npz"))
     if "flash" in which:
@@ -305,3 +381,5 @@ if __name__ == "__main__":
         make_reports(os.path.join(HERE, "reports.json"))
     if "extras" in which:
         make_extras(os.path.join(HERE, "extras.npz"))
+    if "digests" in which:
+        make_digests(os.path.join(HERE, "digests.json"), [w for w in which if w != "digests"])

@@ -101,8 +101,28 @@ def test_wire_roundtrip_and_integrity():
     cfg = fc.CodecConfig(bits=2, group_size=8)
     blob = bytearray(fc.quantize(torch.linspace(-1, 1, 8, device="cuda"), cfg).to_bytes())
     blob[0] = 0xFF
+    with pytest.raises(fc.IntegrityError):  # validated by default, like codec.py:354-384
+        fc.dequantize(fc.QuantizedTensor.from_bytes(bytes(blob), 8, cfg))
+    fc.dequantize(fc.QuantizedTensor.from_bytes(bytes(blob), 8, cfg), validate=False)  # opt-out: no check
+    # test_codec.py:157-163: non-positive / non-finite scales
+    cfg = fc.CodecConfig(bits=4, group_size=8)
+    q = fc.quantize(torch.linspace(-1, 1, 16, device="cuda"), cfg)
+    for bad in (0.0, -1.0, float("inf"), float("nan")):
+        blob = bytearray(q.to_bytes())
+        blob[8:10] = np.array([bad], np.float16).tobytes()
+        with pytest.raises(fc.IntegrityError):
+            fc.dequantize(fc.QuantizedTensor.from_bytes(bytes(blob), 16, cfg))
+    # zero point past the 2^bits - 1 range (3-bit codec, zero byte 9)
+    cfg = fc.CodecConfig(bits=3, group_size=8)
+    blob = bytearray(fc.quantize(torch.linspace(-1, 1, 8, device="cuda"), cfg).to_bytes())
+    blob[-1] = 9
     with pytest.raises(fc.IntegrityError):
-        fc.dequantize(fc.QuantizedTensor.from_bytes(bytes(blob), 8, cfg), validate=True)
+        fc.dequantize(fc.QuantizedTensor.from_bytes(bytes(blob), 8, cfg))
+    # the padding nibble of an odd count is not a code (bitpack.py:64-75)
+    cfg = fc.CodecConfig(bits=2, group_size=8)
+    blob = bytearray(fc.quantize(torch.linspace(-1, 1, 7, device="cuda"), cfg).to_bytes())
+    blob[3] |= 0xF0
+    fc.dequantize(fc.QuantizedTensor.from_bytes(bytes(blob), 7, cfg))
 
 
 def test_known_answers():

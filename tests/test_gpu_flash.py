@@ -282,11 +282,19 @@ def test_compile_time_schemes_vs_oracle(bits, g, sym, rnd, mode):
 @pytest.mark.parametrize("codec", [dict(bits=4), dict(bits=4, symmetric=True), dict(bits=4, rounding="ceil"),
                                    dict(bits=8), dict(bits=8, symmetric=True)])
 def test_group_lane_kernels_match_lane_kernels(tp, codec):
-    # g128 whole tiles take the 2-lanes-per-group reduce (and, for INT4, the group-per-lane
-    # scatter); FC_OPT_STREAM_MASK bits 6/7 force the 32-element lane kernels: bit-identical
-    m = tp * 8192 * 3
+    """g128 whole tiles take the 2-lanes-per-group reduce (and, for INT4, the
+    group-per-lane scatter) — compiled for 16-bit outputs only, so the outputs
+    here are bf16/fp16 (compared as int16). FC_OPT_STREAM_MASK bits 6/7 force
+    the 32-element lane kernels: bit-identical. ~1800 tiles per call give every
+    CTA of the persistent grids several tiles (ring slot / phase wrap-around at
+    k >= 1, 2, 3), and the first 16 tiles of segment 0 (CTA 0's k = 0..3) are
+    checked bit-exactly against the oracle."""
+    tiles = -(-1800 // tp)
+    m = tp * 8192 * tiles
     cfg = fc.FlashConfig.uniform(fc.CodecConfig(**codec))
     comm = _comm(tp, m // tp, cfg, "split")
+    oc = orc.Codec(bits=codec["bits"], symmetric=codec.get("symmetric", False),
+                   rounding=codec.get("rounding", "nearest-even"))
     for dt in (torch.bfloat16, torch.float16):
         g = torch.Generator(device="cuda").manual_seed(tp)
         ts = [(torch.randn(m, device="cuda", generator=g) * (1 + r)).to(dt) for r in range(tp)]
@@ -295,14 +303,57 @@ def test_group_lane_kernels_match_lane_kernels(tp, codec):
         outs = {}
         for mask in (0, 64 | 128):
             comm.set_option(_lib.OPT_STREAM_MASK, mask)
-            outs[mask] = [o.clone() for o in comm.all_reduce_local(ts, cfg, out_dtype=torch.float32)]
+            outs[mask] = [o.clone() for o in comm.all_reduce_local(ts, cfg)]
         comm.set_option(_lib.OPT_STREAM_MASK, 0)
         for a, b in zip(outs[0], outs[64 | 128]):
-            assert torch.equal(a.view(torch.int32), b.view(torch.int32))
-        if tp == 4 and dt == torch.bfloat16:
-            xr = [t.float().cpu().numpy() for t in ts]
-            oc = orc.Codec(bits=codec["bits"], symmetric=codec.get("symmetric", False),
-                           rounding=codec.get("rounding", "nearest-even"))
-            ref = orc.flash_all_reduce(xr, oc, oc).outputs[0]
-            assert np.array_equal(_bits(outs[0][2].cpu().numpy()), _bits(ref))
+            assert a.dtype == dt and torch.equal(a.view(torch.int16), b.view(torch.int16))
+        seg, L = m // tp, 16 * 8192
+        xr = [t[:L].float().cpu().numpy() for t in ts]  # segment 0's first 16 tiles of every rank
+        red = orc.sequential_sum([orc.dequantize(orc.quantize(x, oc)) for x in xr])
+        ref = torch.from_numpy(orc.dequantize(orc.quantize(red, oc))).to(dt)
+        for r in (0, tp - 1):
+            assert torch.equal(outs[0][r][:L].cpu().view(torch.int16), ref.view(torch.int16)), (dt, r)
     comm.close()
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+@pytest.mark.parametrize("codec", [dict(bits=4), dict(bits=4, symmetric=True), dict(bits=4, rounding="ceil"),
+                                   dict(bits=8), dict(bits=8, symmetric=True)])
+def test_fused_kernel_vs_split_and_oracle(tp, codec):
+    """The fused single-launch kernel (k_fstream: group-lane scatter / reduce /
+    gather roles, per-tile flags) for every schedule chunking — the whole
+    segment, 1 tile, 3 tiles, an uneven split — is bit-identical to the
+    phase-split kernels, and its stage-1 / stage-2 slots and outputs equal the
+    oracle (bf16 and fp16, 16-bit outputs)."""
+    tiles = 40
+    m = tp * 8192 * tiles
+    cfg = fc.FlashConfig.uniform(fc.CodecConfig(**codec))
+    comm = _comm(tp, m // tp, cfg, "split")
+    oc = orc.Codec(bits=codec["bits"], symmetric=codec.get("symmetric", False),
+                   rounding=codec.get("rounding", "nearest-even"))
+    try:
+        for dt in (torch.bfloat16, torch.float16):
+            g = torch.Generator(device="cuda").manual_seed(17 * tp + codec["bits"])
+            ts = [(torch.randn(m, device="cuda", generator=g) * (1 + r)).to(dt) for r in range(tp)]
+            ts[0][5000:5128] = 1000.0
+            comm.set_option(_lib.OPT_FUSED, 0)
+            ref = [o.clone() for o in comm.all_reduce_local(ts, cfg)]
+            comm.set_option(_lib.OPT_FUSED, 1)
+            for chunk in (0, 1, 3, 17):
+                comm.set_option(_lib.OPT_FUSED_CHUNK, chunk)
+                for _ in range(2):  # back-to-back calls (epoch flags, no reset)
+                    outs = comm.all_reduce_local(ts, cfg)
+                    for r in range(tp):
+                        assert torch.equal(outs[r].view(torch.int16), ref[r].view(torch.int16)), (dt, chunk, r)
+            comm.set_option(_lib.OPT_FUSED_CHUNK, 0)
+            xr = [t.float().cpu().numpy() for t in ts]
+            res = orc.flash_all_reduce(xr, oc, oc)
+            want = torch.from_numpy(res.outputs[0]).to(dt).view(torch.int16)
+            assert torch.equal(outs[tp - 1].cpu().view(torch.int16), want)
+            if dt == torch.bfloat16:
+                for j in range(tp):
+                    s = (j + 1) % tp
+                    assert comm.slot(j, 1, s, cfg.stage1_codec).to_bytes() == res.stage1[j][s].wire_bytes()
+                    assert comm.slot(s, 2, j, cfg.stage2_codec).to_bytes() == res.stage2[j].wire_bytes()
+    finally:
+        comm.close()

@@ -1,6 +1,7 @@
 """One process per rank over CUDA IPC (the torchrun path), exercised on a
-single GPU: 2-4 processes share cuda:0, map each other's blocks with
-cudaIpcOpenMemHandle and run the fused flag-synchronised kernel. Parity vs the
+single GPU: 2-8 processes share cuda:0, map each other's blocks with
+cudaIpcOpenMemHandle and run the fused flag-synchronised kernel (OPT_FUSED 1)
+or the phase-split kernels with IPC barriers (OPT_FUSED 0). Parity vs the
 oracle, plus the fault path: a rank that never arrives -> ProtocolError
 naming the stuck peer (fabric.py:158-178)."""
 
@@ -42,6 +43,8 @@ def _worker(rank, world, port, q, mode):
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
         comm = FlashComm.from_process_group(device=0, slot_bytes=1 << 20)
         comm.set_timeout(20.0)
+        if mode == "fused":
+            comm.set_option(_lib.OPT_FUSED, 1)
         if mode == "split":
             comm.set_option(_lib.OPT_FUSED, 0)
         if mode == "generic":
@@ -97,7 +100,8 @@ def _run(world, mode):
     assert res == {r: "ok" for r in range(world)}, res
 
 
-@pytest.mark.parametrize("world,mode", [(2, "fused"), (4, "fused"), (2, "split"), (4, "split"), (3, "generic")])
+@pytest.mark.parametrize("world,mode", [(2, "fused"), (4, "fused"), (8, "fused"), (2, "split"), (4, "split"),
+                                        (8, "split"), (3, "generic")])
 def test_ipc_parity(world, mode):
     _run(world, mode)
 

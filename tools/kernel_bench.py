@@ -132,24 +132,31 @@ def tune_sweep():
 
 
 def fused_tune():
-    """Role weights (scatter:reduce:gather CTAs) of the fused streaming kernel at C2."""
+    """Schedule chunk / ring depths / CTA cap of the fused streaming kernel at C2
+    (all 8 ranks in one launch), against the phase-split path."""
     M, tp, e = 8 * 1024 * 8192, 8, 2
     cfg = fc.FlashConfig.from_bits(4)
     seg = M // tp
     comm = FlashComm.local([0] * tp, slot_bytes_for(seg, cfg.stage1_codec, cfg.stage2_codec))
-    comm.set_option(_lib.OPT_FUSED, 1)
     ins = [torch.randn(M, device="cuda").to(torch.bfloat16) for _ in range(tp)]
     outs = [torch.empty_like(t) for t in ins]
     w = cfg.stage1_codec.wire_byte_len(seg)
     alg = tp * (2 * e * M + 2 * (tp - 1) * 2 * w)
-    for q, r, d in ((3, 2, 3), (4, 3, 4), (5, 3, 5), (6, 4, 6), (5, 4, 5), (4, 2, 4), (6, 3, 5), (5, 3, 6), (3, 3, 3), (7, 4, 5)):
-        comm.set_option(_lib.OPT_ROLE_WEIGHTS, q | (r << 8) | (d << 16))
-        for cap in (0, 1):
+    comm.set_option(_lib.OPT_FUSED, 0)
+    t = timeit(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), iters=10, warm=3)
+    print(json.dumps({"kernel": "flash_split", "ms": t, "frac": alg / t / 1e6 / PEAK}), flush=True)
+    comm.set_option(_lib.OPT_FUSED, 1)
+    tiles = seg // 8192
+    for chunk in (0, tiles // 2, tiles // 4, tiles // 8):
+        for qs, ds, cap in ((0, 0, 0), (4, 4, 0), (4, 8, 0), (6, 0, 0), (4, 0, 2)):
+            comm.set_option(_lib.OPT_FUSED_CHUNK, chunk)
+            comm.set_option(_lib.OPT_SCATTER_STAGES, qs)
+            comm.set_option(_lib.OPT_GATHER_STAGES, ds)
             comm.set_option(_lib.OPT_CTAS_PER_SM, cap)
-            t = timeit(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), iters=5, warm=2)
+            t = timeit(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), iters=10, warm=3)
             comm.check()
-            print(json.dumps({"kernel": "flash_fused_tune", "w": [q, r, d], "cta_cap": cap, "ms": t,
-                              "frac": alg / t / 1e6 / PEAK}), flush=True)
+            print(json.dumps({"kernel": "flash_fused_tune", "chunk": chunk, "q_stages": qs, "d_stages": ds,
+                              "cta_cap": cap, "ms": t, "frac": alg / t / 1e6 / PEAK}), flush=True)
     comm.close()
 
 

@@ -26,5 +26,5 @@ else:
     x = torch.randn(M, device="cuda").to(torch.bfloat16)
     for _ in range(3):
         q = fc.quantize(x, fc.CodecConfig(bits=4))
-        fc.dequantize(q, dtype=torch.bfloat16)
+        fc.dequantize(q, dtype=torch.bfloat16, validate=False)
 torch.cuda.synchronize()
