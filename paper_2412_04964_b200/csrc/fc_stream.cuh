@@ -244,8 +244,9 @@ struct RoundIter {
   int i, items, y, t, P, dy, dt, step;
   __device__ __forceinline__ RoundIter(int items_, int P_, int first, int step_, int t0 = 0)
       : i(first), items(items_), P(P_), step(step_) {
-    t = t0 + first / P;
+    t = first / P;
     y = first - t * P;
+    t += t0;
     dt = step / P;
     dy = step - dt * P;
   }
