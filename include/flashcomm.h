@@ -153,12 +153,14 @@ typedef enum {
   FC_OPT_SCATTER_STAGES = 7,/* ring depth of the streaming scatter / quantize kernel (0 = auto) */
   FC_OPT_GATHER_STAGES = 8, /* ring depth of the streaming gather / dequantize kernel (0 = auto) */
   FC_OPT_CTAS_PER_SM = 9,   /* cap on resident CTAs per SM of the streaming kernels (0 = occupancy) */
-  FC_OPT_STREAM_MASK = 10,  /* A/B testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels; bit 4: INT8 g=128 scatter on the group-per-lane kernel; bit 5: its code stores direct (not staged); bits 6/7: g=128 scatter/reduce on the 32-element lane layout */
+  FC_OPT_STREAM_MASK = 10,  /* A/B testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels; bit 4: INT8 g=128 scatter on the group-per-lane kernel; bit 5: its code stores direct (not staged); bits 6/7: g=128 scatter/reduce on the 32-element lane layout; measurement only (results invalid): bit 8 skips the fused kernel's flag waits, bit 9 its flag publications */
   FC_OPT_PHASES = 11,       /* measurement only: run just these phases (bit 0/1/2) of a one-GPU split call */
   FC_OPT_FUSED_CHUNK = 12,  /* fused kernel schedule: tiles per chunk (step s scatters chunk s, reduces s-1,
                                gathers s-2); 0 = auto: the whole round on one GPU, a quarter across GPUs */
   FC_OPT_ONESHOT = 13,      /* one GPU: small calls as one cooperative launch with grid barriers (default 1) */
-  FC_OPT_HOST_CHUNK_BYTES = 14 /* fc_flash_all_reduce_host: H2D bytes per rank per pipeline chunk (0 = auto) */
+  FC_OPT_HOST_CHUNK_BYTES = 14, /* fc_flash_all_reduce_host: H2D bytes per rank per pipeline chunk (0 = auto) */
+  FC_OPT_FUSED_GATHER_CTAS = 15, /* fused kernel: gather-role CTAs per SM (0 = auto) */
+  FC_OPT_ROLE_PROFILE = 16  /* measurement: record the fused kernel's per-CTA role timeline (fc_comm_role_profile) */
 } fc_option;
 FC_API fc_status fc_comm_set_option(fc_comm* comm, int32_t option, int64_t value);
 FC_API fc_status fc_comm_get_option(fc_comm* comm, int32_t option, int64_t* value);
@@ -207,6 +209,14 @@ FC_API fc_status fc_comm_slot(fc_comm* comm, int32_t rank, int32_t stage, int32_
 /* Topology discovery: peer-access matrix (world*world ints) and NVLink
  * multicast support of rank's device. */
 FC_API fc_status fc_comm_topology(fc_comm* comm, int32_t* can_access, int32_t* multicast);
+/* Measurement: per-CTA role timeline of rank's last fused-kernel launch
+ * (FC_OPT_ROLE_PROFILE = 1 first): FC_ROLE_PROFILE_U64 %globaltimer values
+ * per CTA — first start / last end / busy ns of the scatter, reduce and
+ * gather roles, kernel start, kernel end. Copies up to max_ctas CTAs into
+ * host memory and stores the launch's CTA count (synchronous). */
+#define FC_ROLE_PROFILE_U64 16
+FC_API fc_status fc_comm_role_profile(fc_comm* comm, int32_t rank, uint64_t* host_dst, int32_t max_ctas,
+                                      int32_t* ctas);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,7 @@ MINIFLOAT_FORMAT_IDS = {"e4m3": 0, "e5m2": 1, "e2m1": 2}
 ROUND_NEAREST_EVEN, ROUND_CEIL = 0, 1
 OPT_FUSED, OPT_CTAS, OPT_TIMEOUT_MS, OPT_LAG, OPT_FAST, OPT_LAST_LAUNCHES, OPT_REDUCE_STAGES = 0, 1, 2, 3, 4, 5, 6
 OPT_SCATTER_STAGES, OPT_GATHER_STAGES, OPT_CTAS_PER_SM, OPT_STREAM_MASK, OPT_PHASES = 7, 8, 9, 10, 11
-OPT_FUSED_CHUNK, OPT_ONESHOT, OPT_HOST_CHUNK_BYTES = 12, 13, 14
+OPT_FUSED_CHUNK, OPT_ONESHOT, OPT_HOST_CHUNK_BYTES, OPT_FUSED_GATHER_CTAS, OPT_ROLE_PROFILE = 12, 13, 14, 15, 16
 
 
 class fc_codec(C.Structure):
@@ -83,6 +83,7 @@ _SIGS = {
     "fc_comm_check": (C.c_int, [_P, _I32]),
     "fc_comm_slot": (C.c_int, [_P, _I32, _I32, _I32, _P, C.POINTER(fc_layout)]),
     "fc_comm_topology": (C.c_int, [_P, C.POINTER(_I32), C.POINTER(_I32)]),
+    "fc_comm_role_profile": (C.c_int, [_P, _I32, C.POINTER(C.c_uint64), _I32, C.POINTER(_I32)]),
     "fc_hadamard": (C.c_int, [_P, _I32, _I64, _I64, _I32, _I32, _P, _I32, _P, _I32, _I64, _P]),
 }
 

@@ -293,6 +293,7 @@ fc_status fc_comm_destroy(fc_comm* c) {
     }
     if (c->opened[r] && c->blk[r]) cudaIpcCloseMemHandle(c->blk[r]);
     if (c->scratch[r]) cudaFree(c->scratch[r]);
+    if (c->tprof[r]) cudaFree(c->tprof[r]);
     if (c->ev[r]) cudaEventDestroy(c->ev[r]);
     if (c->hs_in[r] || c->hs_out[r] || c->hs_h2d[r]) cudaSetDevice(c->devices[r]);
     if (c->hs_in[r]) cudaFree(c->hs_in[r]);
@@ -323,11 +324,13 @@ fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
     case FC_OPT_SCATTER_STAGES: c->q_stages = std::max<int64_t>(0, std::min<int64_t>(8, value)); break;
     case FC_OPT_GATHER_STAGES: c->d_stages = std::max<int64_t>(0, std::min<int64_t>(12, value)); break;
     case FC_OPT_CTAS_PER_SM: c->ctas_per_sm = std::max<int64_t>(0, std::min<int64_t>(16, value)); break;
-    case FC_OPT_STREAM_MASK: c->stream_mask = value & 255; break;
+    case FC_OPT_STREAM_MASK: c->stream_mask = value & 65535; break;
     case FC_OPT_PHASES: c->phases = value & 7; break;
     case FC_OPT_ONESHOT: c->oneshot = value != 0; break;
     case FC_OPT_FUSED_CHUNK: c->fused_chunk = std::max<int64_t>(0, value); break;
     case FC_OPT_HOST_CHUNK_BYTES: c->host_chunk_bytes = std::max<int64_t>(0, value); break;
+    case FC_OPT_FUSED_GATHER_CTAS: c->fused_gather_ctas = std::max<int64_t>(0, std::min<int64_t>(16, value)); break;
+    case FC_OPT_ROLE_PROFILE: c->role_profile = value != 0; break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
   return FC_OK;
@@ -351,6 +354,8 @@ fc_status fc_comm_get_option(fc_comm* c, int32_t option, int64_t* value) {
     case FC_OPT_ONESHOT: *value = c->oneshot; break;
     case FC_OPT_FUSED_CHUNK: *value = c->fused_chunk; break;
     case FC_OPT_HOST_CHUNK_BYTES: *value = c->host_chunk_bytes; break;
+    case FC_OPT_FUSED_GATHER_CTAS: *value = c->fused_gather_ctas; break;
+    case FC_OPT_ROLE_PROFILE: *value = c->role_profile; break;
     default: return fail(FC_ERR_CONFIG, "unknown option %d", option);
   }
   return FC_OK;
@@ -669,6 +674,19 @@ fc_status fc_comm_slot(fc_comm* c, int32_t rank, int32_t stage, int32_t src, voi
     FC_CUDA_TRY(cudaDeviceSynchronize());
     FC_CUDA_TRY(cudaMemcpy(dst, p, (size_t)L.total_bytes, cudaMemcpyDefault));
   }
+  return FC_OK;
+}
+
+fc_status fc_comm_role_profile(fc_comm* c, int32_t rank, uint64_t* host_dst, int32_t max_ctas, int32_t* ctas) {
+  if (!c || !host_dst) return fail(FC_ERR_CONFIG, "NULL argument");
+  if (rank < 0 || rank >= c->world) return fail(FC_ERR_DOMAIN, "rank out of range");
+  if (!c->tprof[rank] || c->tprof_ctas[rank] <= 0)
+    return fail(FC_ERR_PROTOCOL, "no profiled fused launch on rank %d (set FC_OPT_ROLE_PROFILE)", rank);
+  const int n = std::min(max_ctas, c->tprof_ctas[rank]);
+  FC_CUDA_TRY(cudaSetDevice(c->devices[rank]));
+  FC_CUDA_TRY(cudaDeviceSynchronize());
+  FC_CUDA_TRY(cudaMemcpy(host_dst, c->tprof[rank], (size_t)n * FC_ROLE_PROFILE_U64 * 8, cudaMemcpyDeviceToHost));
+  if (ctas) *ctas = c->tprof_ctas[rank];
   return FC_OK;
 }
 

@@ -1,6 +1,7 @@
 // Single-GPU group codec kernels: quantize (codec.py:292-329) and dequantize
 // (codec.py:354-384), plus the generic (any group size) kernels that the
 // flash path reuses for group sizes outside {32, 64, 128, 256}.
+#include <cstring>
 #include <algorithm>
 #include <map>
 #include <mutex>
@@ -230,12 +231,47 @@ static unsigned stream_grid_cur(const void* kern, int threads, int smem, int64_t
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(items, (int64_t)occ * cur_sms()));
 }
 
+// A/B selection of the codec quantize kernel (measurement only): FC_CODEC_QKERNEL=lane|gpl|gq
+static int codec_qkernel() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FC_CODEC_QKERNEL");
+    v = !e ? 0 : (!strcmp(e, "lane") ? 1 : !strcmp(e, "gpl") ? 2 : !strcmp(e, "gq") ? 3 : 0);
+  }
+  return v;
+}
+
+template <typename T, class Spec, int G>
+static fc_status quant_gq(FlashArgs a, cudaStream_t st) {
+  const void* k = (const void*)k_qstream_gq<T, Spec, G>;
+  const int smem = a.stages * (kTileElems * 2 + 16);
+  FC_TRY(ensure_smem_attr(k, smem));
+  k_qstream_gq<T, Spec, G><<<stream_grid_cur(k, kGplThreads, smem, a.tiles), kGplThreads, smem, st>>>(a);
+  return FC_OK;
+}
+
 template <typename T, class Spec>
 static fc_status quant_stream(const T* x, int64_t n, const DevCodec& dc, uint8_t* dst, uint32_t* err, cudaStream_t st) {
   FlashArgs a = codec_args(x, dst, n, dc, err);
   a.stages = 4;
   const int smem = a.stages * (kTileElems * 2 + 16);
-  if (Spec::SB == 4 && dc.g == kGplG) {  // one lane per group (INT4; see launch_qstream)
+  const int sel = codec_qkernel();
+  // group-lane slices (k_qstream_gq) for g in {64, 128, 256} (INT8) / {64, 256} (INT4); INT4
+  // g = 128 keeps the register-resident-group kernel (k_qstream_gpl), g = 32 the 32-element
+  // lanes (k_qstream: four float64 group tails per slice cost more than the shuffles;
+  // profiles/r02_codec_ab.txt)
+  const bool gq_ok = dc.g == 32 || dc.g == 64 || dc.g == 128 || dc.g == 256;
+  const bool gq_auto = dc.g != 32 && !(Spec::SB == 4 && dc.g == kGplG);
+  if (gq_ok && (sel == 3 || (sel == 0 && gq_auto))) {
+    a.stages = 3;
+    switch (dc.g) {
+      case 32: return quant_gq<T, Spec, 32>(a, st);
+      case 64: return quant_gq<T, Spec, 64>(a, st);
+      case 128: return quant_gq<T, Spec, 128>(a, st);
+      default: return quant_gq<T, Spec, 256>(a, st);
+    }
+  }
+  if (sel != 1 && Spec::SB == 4 && dc.g == kGplG) {  // one lane per group (INT4; see launch_qstream)
     const void* k = (const void*)k_qstream_gpl<T, Spec>;
     FC_TRY(ensure_smem_attr(k, smem));
     k_qstream_gpl<T, Spec><<<stream_grid_cur(k, kGplThreads, smem, a.tiles), kGplThreads, smem, st>>>(a);

@@ -37,6 +37,10 @@ struct fc_comm {
   int64_t stream_mask = 0;
   int64_t phases = 0;
   int64_t oneshot = 1;  // one-GPU small messages: single cooperative launch (k_oneshot)
+  int64_t role_profile = 0;  // record the fused kernel's per-CTA role timeline
+  uint64_t* tprof[kMaxRanks] = {nullptr};
+  int32_t tprof_ctas[kMaxRanks] = {0};
+  int64_t fused_gather_ctas = 0;  // fused stream kernel: gather-role CTAs per SM (0 = auto)
   int64_t fused_chunk = 0;  // fused stream kernel: tiles per schedule chunk (0 = auto)  // measurement: phase mask of the one-GPU split path (0 = all)
   int64_t reduce_stages = 0, q_stages = 0, d_stages = 0, ctas_per_sm = 0;  // 0 = auto
   int64_t launches = 0, last_launches = 0;  // kernels launched by the last call

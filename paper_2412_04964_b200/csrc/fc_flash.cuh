@@ -43,7 +43,10 @@ struct FlashArgs {
   int q_hint, d_hint;       // ring depths of the streaming scatter / gather kernels (0 = auto)
   int cta_cap;              // resident CTAs per SM cap for the streaming kernels (0 = occupancy)
   int fp_chunk;             // fused stream kernel: tiles per schedule chunk
+  int fp_dctas;             // fused stream kernel: CTAs [0, fp_dctas) run the gather role
+  uint64_t* tprof;          // fused stream kernel: per-CTA role timeline (measurement; null = off)
   int fp_bars;              // fused stream kernel: byte offset of the barrier region in shared memory
+  int fp_meta;              // fused stream kernel: byte offset of the DynIter id ring in shared memory
   int q_stages_f, d_stages_f;  // fused stream kernel ring depths of the scatter / gather roles
   int sys_scope;            // flags cross GPUs: system-scope fences; else gpu scope (one GPU)
   int dbg;                  // FC_OPT_STREAM_MASK A/B bits (include/flashcomm.h)
@@ -60,7 +63,10 @@ __host__ __device__ inline int64_t blk_flags_off(int world, int64_t slot_bytes) 
 __host__ __device__ inline int64_t blk_misc_off(int world, int64_t slot_bytes, int64_t flags_cap) {
   return blk_flags_off(world, slot_bytes) + 2 * (int64_t)world * flags_cap * 4;
 }
-constexpr int64_t kMiscBytes = 512;  // err word @0, barrier flags @64: [2][kMaxRanks] u32
+// err word @0, barrier flags @64: [2][kMaxRanks] u32; fused-kernel work counters @512:
+// [3 roles][kFusedMaxChunks] u32 + one launch-done counter
+constexpr int kFusedMaxChunks = 1024;
+constexpr int64_t kMiscBytes = 512 + (3 * kFusedMaxChunks + 32) * 4;
 
 __device__ __forceinline__ uint8_t* recv_slot(const FlashArgs& a, int owner, int src) {
   return a.blk[owner] + (int64_t)src * a.slot_bytes;
@@ -78,6 +84,7 @@ __device__ __forceinline__ uint32_t* gflag(const FlashArgs& a, int owner, int sr
 __device__ __forceinline__ uint32_t* errw(const FlashArgs& a, int owner) {
   return reinterpret_cast<uint32_t*>(a.blk[owner] + blk_misc_off(a.world, a.slot_bytes, a.flags_cap));
 }
+__device__ __forceinline__ uint32_t* fctr(const FlashArgs& a, int owner) { return errw(a, owner) + 128; }
 __device__ __forceinline__ uint32_t* barflag(const FlashArgs& a, int owner, int phase, int src) {
   return errw(a, owner) + 16 + phase * kMaxRanks + src;
 }

@@ -220,18 +220,19 @@ __device__ __forceinline__ void read_peer(const DevCodec& c1, uint32_t src, uint
 // are consecutive tiles of one job.
 struct RangeIter {
   int i, end, y, t, tiles;
-  __device__ __forceinline__ RangeIter(int items, int tiles_, int cta, int nctas) : tiles(tiles_) {
+  int t0;
+  __device__ __forceinline__ RangeIter(int items, int tiles_, int cta, int nctas, int t0_ = 0) : tiles(tiles_), t0(t0_) {
     const int per = (items + nctas - 1) / nctas;
     i = min(items, cta * per);
     end = min(items, i + per);
     y = i / tiles;
-    t = i - y * tiles;
+    t = i - y * tiles + t0;
   }
   __device__ __forceinline__ bool ok() const { return i < end; }
   __device__ __forceinline__ void next() {
     ++i;
-    if (++t == tiles) {
-      t = 0;
+    if (++t == tiles + t0) {
+      t = t0;
       ++y;
     }
   }
@@ -271,7 +272,7 @@ struct RoundIter {
 __device__ __forceinline__ bool warp_wait_flags(const FlashArgs& a, int rank, const uint32_t* flag, int peer,
                                                 bool active, uint32_t phase) {
   bool ok = true;
-  if (active) {
+  if (active && !(a.dbg & 256)) {  // dbg 256: measurement only, no waits (results are garbage)
     const uint64_t t0 = globaltimer();
     volatile uint32_t* ew = errw(a, rank);
     uint32_t spins = 0;
@@ -310,6 +311,29 @@ __device__ __forceinline__ void publish_flag(const FlashArgs& a, uint32_t* f, ui
   } else {
     st_release_gpu(f, ep);
   }
+}
+
+// fused kernels publish a tile's flags from the PRODUCER warp once the tile's
+// consumers have handed its ring stage back: the consumers issue all of the
+// tile's global stores before they arrive on the stage's empty barrier
+// (mbarrier.arrive: release.cta; the producer's try_wait: acquire.cta), so the
+// producer's gpu/system-scope release covers them by cumulativity -- the same
+// argument as a bar.sync before a publishing thread, but the fence stalls
+// only the producer (which has S stages of bulk copies queued), not a
+// consumer warp in the middle of its tiles.
+__device__ __forceinline__ void publish_scatter(const FlashArgs& a, int y, int t, uint32_t ep) {
+  if (a.dbg & 512) return;  // measurement only
+  int r, j;
+  pair_of(a, y, r, j);
+  publish_flag(a, rflag(a, j, r) + t, ep);
+}
+__device__ __forceinline__ void publish_reduce(const FlashArgs& a, int y, int t, uint32_t ep) {
+  if (a.dbg & 512) return;
+  const int j = a.rank_lo + y;
+  if (a.sys_scope) __threadfence_system();
+  else __threadfence();
+  for (int p = 0; p < a.world; ++p)
+    if (p != j) st_relaxed_sys(gflag(a, p, j) + t, ep);
 }
 
 __device__ __forceinline__ void mbar_inval(uint32_t bar) {
@@ -411,6 +435,36 @@ __device__ __forceinline__ void q_role(const FlashArgs& a, uint32_t sbase, int S
     }
     ring_next(st, ph, S);
   }
+}
+
+// ------------------------------------------------------------------ fused kernel: dynamic item dealing
+
+// One (role, chunk) of the fused kernel: its items are dealt dynamically. The
+// producer warp of a CTA grabs item ids from a global counter (tile-major:
+// t = t0 + id / per, y = id % per) and writes each id beside its ring stage in
+// shared memory; the consumer warps read it after the stage's full barrier; a
+// negative id ends the role. Faster CTAs take more items, so the CTAs leave a
+// role together (a static round-robin deal left 50-100 us of per-role tails
+// at C2 on one GPU). The counters are zeroed by the last CTA of the launch.
+struct DynIter {
+  uint32_t* ctr;  // this (role, chunk)'s counter
+  int items, per, t0;
+  uint32_t meta;  // shared-memory id ring, one int per stage
+  uint32_t ep;    // the round's flag epoch
+  __device__ __forceinline__ int grab() const { return (int)atomicAdd(ctr, 1u); }
+  __device__ __forceinline__ void decode(int id, int& y, int& t) const {
+    t = id / per;
+    y = id - t * per;
+    t += t0;
+  }
+};
+__device__ __forceinline__ void sts32(uint32_t addr, int v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int lds_id(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
 }
 
 // ------------------------------------------------------------------ group-per-lane quantize role
@@ -567,17 +621,60 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
       int st = 0, k = 0, cy = -1;
       uint32_t ph = 0;
       QJob<Tin> jb;
-      for (Iter it = it0; it.ok(); it.next(), ++k) {
-        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
-        if (it.y != cy) {
-          jb = qjob<Tin>(a, it.y);
-          cy = it.y;
+      auto issue = [&](int y, int t) {
+        if (y != cy) {
+          jb = qjob<Tin>(a, y);
+          cy = y;
         }
-        const int64_t e0 = (int64_t)it.t * kTileElems;
+        const int64_t e0 = (int64_t)t * kTileElems;
         const uint32_t bytes = (uint32_t)(tile_valid(a.sub_len, jb.limit, e0) * 2) & ~15u;
         mbar_arrive_expect_tx(full0 + 8 * st, bytes);
         if (bytes) bulk_g2s(sbase + st * STAGE, jb.src + e0, bytes, full0 + 8 * st);
-        ring_next(st, ph, S);
+      };
+      if constexpr (!FUSED) {
+        for (Iter it = it0; it.ok(); it.next(), ++k) {
+          if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+          issue(it.y, it.t);
+          ring_next(st, ph, S);
+        }
+      } else {
+        // dynamic dealing (DynIter): grab ids until the (role, chunk) is exhausted; a recycled
+        // stage's previous item has its stores issued: publish its flag (publish_scatter)
+        const DynIter& D = it0;
+        auto publish_id = [&](int old) {
+          int y, t;
+          D.decode(old, y, t);
+          publish_scatter(a, y, t, D.ep);
+        };
+        auto recycle = [&]() {
+          mbar_wait(empty0 + 8 * st, ph ^ 1);
+          publish_id(lds_id(D.meta + 4 * st));
+        };
+        int id = D.grab();
+        for (;; ++k) {
+          const int nid = id < D.items ? D.grab() : id;  // the next id is in flight during this item
+          if (k >= S) recycle();
+          if (id >= D.items) break;
+          sts32(D.meta + 4 * st, id);
+          int y, t;
+          D.decode(id, y, t);
+          issue(y, t);
+          ring_next(st, ph, S);
+          id = nid;
+        }
+        // one end sentinel per consumer slot (the first one takes the stage recycled above)
+        const int K = k;
+        for (int n = 0; n < kGplSlots; ++n, ++k) {
+          if (n > 0 && k >= S) recycle();
+          sts32(D.meta + 4 * st, -1);
+          mbar_arrive(full0 + 8 * st);
+          ring_next(st, ph, S);
+        }
+        // the real items whose stages were not recycled: wait for their hand-back, publish
+        for (int kp = k > S ? k - S : 0; kp < K; ++kp) {
+          mbar_wait(empty0 + 8 * (kp % S), (uint32_t)(kp / S) & 1u);
+          publish_id(lds_id(D.meta + 4 * (kp % S)));
+        }
       }
     }
     return;
@@ -585,16 +682,14 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
   const int slot = warp / kGplWpt, part = warp % kGplWpt;
   const int m = lane & 7;
   const int gi = part * 32 + lane;  // this lane's group within a tile
-  int st = 0, cy = -1, k = 0;
-  uint32_t ph = 0;
+  int cy = -1;
   QJob<Tin> jb;
-  for (Iter it = it0; it.ok(); it.next(), ++k) {
-    if (k % kGplSlots == slot) {  // S is a multiple of the slot count: a slot always meets its own stages
-      if (it.y != cy) {
-        jb = qjob<Tin>(a, it.y);
-        cy = it.y;
+  auto item = [&](int y, int t, int st, uint32_t ph) {
+      if (y != cy) {
+        jb = qjob<Tin>(a, y);
+        cy = y;
       }
-      const int64_t p0 = (int64_t)it.t * kTileElems + gi * kGplG;
+      const int64_t p0 = (int64_t)t * kTileElems + gi * kGplG;
       const bool whole = p0 + kGplG <= a.sub_len && p0 + kGplG <= jb.limit;
       mbar_wait(full0 + 8 * st, ph);
       if (__all_sync(0xffffffffu, whole)) {
@@ -666,18 +761,13 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
           __syncwarp();
           const uint32_t wb = sbase + st * STAGE + part * 32 * (kGplG * 2);
           fence_proxy_async_smem();  // generic st.shared before the stage's next bulk (async-proxy) fill
-          uint8_t* cw0 = jb.dst + ((int64_t)it.t * kTileElems + part * 32 * kGplG) * S1::SB / 8;
+          uint8_t* cw0 = jb.dst + ((int64_t)t * kTileElems + part * 32 * kGplG) * S1::SB / 8;
 #pragma unroll
           for (int r = 0; r < NV; ++r) {
             const int x = 512 * r + 16 * lane, l = x / CB, v = (x % CB) / 16;
             st_v4(cw0 + x, lds128_(wb + l * (kGplG * 2) + 16 * (v ^ (l & 7))));
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(empty0 + 8 * st);
         } else {
-          // every shared load has been consumed (the codes depend on all of them)
-          __syncwarp();
-          if (lane == 0) mbar_arrive(empty0 + 8 * st);
           uint8_t* cd = jb.dst + p0 * S1::SB / 8;
 #pragma unroll
           for (int v = 0; v < NV; ++v)
@@ -686,21 +776,15 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
         const int64_t grp = p0 >> a.c1.gshift;
         *reinterpret_cast<unsigned short*>(jb.dst + a.c1.scales_off + 2 * grp) = g.s16;
         if constexpr (!S1::SYM) jb.dst[a.c1.zeros_off + grp] = (uint8_t)g.z;
+        // the tile's stores are issued: hand the stage back (FUSED: the producer then publishes rflag)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * st);
         if (bad && jb.err) atomicOr(jb.err, jb.ecode);
-        if constexpr (FUSED) {
-          // both warps of this slot stored their 32 groups of the tile: publish rflag[j][r][t]
-          asm volatile("bar.sync %0, %1;" ::"r"(2 + slot), "n"(32 * kGplWpt) : "memory");
-          if (part == 0 && lane == 0) {
-            int r, j;
-            pair_of(a, it.y, r, j);
-            publish_flag(a, rflag(a, j, r) + it.t, flag_epoch(a));
-          }
-        }
       } else {
         // ragged tail: the 32-element lane codec over this warp's 4096 elements, 1024 at a time
         bool bad = false;
         for (int sub = 0; sub < kGplG / 32; ++sub) {
-          const int64_t q0 = (int64_t)it.t * kTileElems + part * (32 * kGplG) + sub * (32 * kLaneElems) + lane * kLaneElems;
+          const int64_t q0 = (int64_t)t * kTileElems + part * (32 * kGplG) + sub * (32 * kLaneElems) + lane * kLaneElems;
           const int nvalid = lane_valid(a.sub_len, q0);
           PackedLane<Tin> L;
           load_lane_src(jb.src, q0, jb.limit, nvalid, L);
@@ -711,14 +795,218 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
         __syncwarp();
         if (lane == 0) mbar_arrive(empty0 + 8 * st);
         if (bad && jb.err) atomicOr(jb.err, jb.ecode);
-        if constexpr (FUSED) {
-          asm volatile("bar.sync %0, %1;" ::"r"(2 + slot), "n"(32 * kGplWpt) : "memory");
-          if (part == 0 && lane == 0) {
-            int r, j;
-            pair_of(a, it.y, r, j);
-            publish_flag(a, rflag(a, j, r) + it.t, flag_epoch(a));
+      }
+  };
+  if constexpr (!FUSED) {
+    int st = 0, k = 0;
+    uint32_t ph = 0;
+    for (Iter it = it0; it.ok(); it.next(), ++k) {
+      if (k % kGplSlots == slot) item(it.y, it.t, st, ph);  // S is a multiple of the slot count
+      ring_next(st, ph, S);
+    }
+  } else {
+    const DynIter& D = it0;
+    for (int k = slot;; k += kGplSlots) {
+      const int st = k % S;
+      const uint32_t ph = (uint32_t)(k / S) & 1u;
+      mbar_wait(full0 + 8 * st, ph);
+      const int id = lds_id(D.meta + 4 * st);
+      if (id < 0) break;
+      int y, t;
+      D.decode(id, y, t);
+      item(y, t, st, ph);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ group-lane quantize, any g in {32..256}
+
+// Quantize with a lane per 128-element slice for group sizes 32, 64, 128 and
+// 256 and both storage widths (k_qstream_gq: the single-GPU codec and the
+// INT8 scatter). Same CTA shape, producer ring and coalesced staged code
+// stores as q_role_gpl, but two passes over the staged slice: pass 1 reads the
+// 16 XOR-swizzled vectors for the group bounds only, pass 2 reads them again
+// and encodes chunk by chunk, so the 64 input words never sit in registers
+// (INT8: no spills, 4 CTAs per SM). A slice holds 128 / g groups (g <= 128) or
+// half a group (g = 256: the partner lane's bounds come over one shuffle). At
+// step c a lane reads physical chunk c ^ m, whose group is (c / CPG) ^ (m /
+// CPG): bounds and parameters are kept per step-order ("virtual") group and
+// the metadata goes to the physical group's address.
+template <typename Tin, class S1, int G, bool FUSED, class Iter>
+__device__ __forceinline__ void q_role_gq(const FlashArgs& a, uint32_t sbase, int S, Iter it0, uint32_t bars = 0) {
+  static_assert(sizeof(Tin) == 2, "16-bit inputs");
+  static_assert(G == 32 || G == 64 || G == 128 || G == 256, "group size");
+  static_assert(!FUSED, "the fused kernel uses q_role_gpl");
+  constexpr uint32_t STAGE = kTileElems * 2;
+  constexpr int SL = 128;                      // elements per lane slice
+  constexpr int NC = SL / 8;                   // 8-element chunks per slice
+  constexpr int NGL = G >= SL ? 1 : SL / G;    // groups per slice
+  constexpr int CPG = NC / NGL;                // chunks per (virtual) group
+  constexpr int CWPC = S1::SB / 4;             // code words per chunk
+  constexpr int MSH = CPG >= 8 ? 0 : (CPG == 4 ? 2 : 1);  // m >> MSH: the swizzle's group-index bits
+  const uint32_t full0 = bars ? bars : sbase + S * STAGE, empty0 = full0 + 8 * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kGplWpt);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kGplWarps) {
+    if (lane == 0) {
+      int st = 0, k = 0, cy = -1;
+      uint32_t ph = 0;
+      QJob<Tin> jb;
+      for (Iter it = it0; it.ok(); it.next(), ++k) {
+        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        if (it.y != cy) {
+          jb = qjob<Tin>(a, it.y);
+          cy = it.y;
+        }
+        const int64_t e0 = (int64_t)it.t * kTileElems;
+        const uint32_t bytes = (uint32_t)(tile_valid(a.sub_len, jb.limit, e0) * 2) & ~15u;
+        mbar_arrive_expect_tx(full0 + 8 * st, bytes);
+        if (bytes) bulk_g2s(sbase + st * STAGE, jb.src + e0, bytes, full0 + 8 * st);
+        ring_next(st, ph, S);
+      }
+    }
+    return;
+  }
+  const int slot = warp / kGplWpt, part = warp % kGplWpt;
+  const int m = lane & 7;
+  const int mg = CPG >= 8 ? 0 : (m >> MSH);  // physical group = virtual ^ mg
+  const int li = part * 32 + lane;           // this lane's slice within a tile
+  const uint32_t qmax = (1u << a.c1.bits) - 1u;
+  int st = 0, cy = -1, k = 0;
+  uint32_t ph = 0;
+  QJob<Tin> jb;
+  for (Iter it = it0; it.ok(); it.next(), ++k) {
+    if (k % kGplSlots == slot) {
+      if (it.y != cy) {
+        jb = qjob<Tin>(a, it.y);
+        cy = it.y;
+      }
+      const int64_t p0 = (int64_t)it.t * kTileElems + li * SL;
+      const bool whole = p0 + SL <= a.sub_len && p0 + SL <= jb.limit;
+      mbar_wait(full0 + 8 * st, ph);
+      if (__all_sync(0xffffffffu, whole)) {
+        const uint32_t gb = sbase + st * STAGE + li * (SL * 2);
+        // ---- pass 1: bounds per virtual group (16-bit packed, exact)
+        uint32_t mn[NGL], mx[NGL];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const uint4 u = lds128_(gb + 16 * (c ^ m));
+          const int v = c / CPG;
+          const uint32_t xs[4] = {u.x, u.y, u.z, u.w};
+          if constexpr (S1::SYM) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t ab = xs[i] & 0x7FFF7FFFu;
+              mx[v] = (c % CPG == 0 && i == 0) ? ab : h2max<Tin>(mx[v], ab);
+            }
+          } else {
+            if (c % CPG == 0) {
+              mn[v] = h2min<Tin>(xs[0], xs[1]);
+              mx[v] = h2max<Tin>(xs[0], xs[1]);
+            } else {
+              mn[v] = h2min<Tin>(mn[v], xs[0]);
+              mx[v] = h2max<Tin>(mx[v], xs[0]);
+              mn[v] = h2min<Tin>(mn[v], xs[1]);
+              mx[v] = h2max<Tin>(mx[v], xs[1]);
+            }
+            mn[v] = h2min<Tin>(mn[v], xs[2]);
+            mx[v] = h2max<Tin>(mx[v], xs[2]);
+            mn[v] = h2min<Tin>(mn[v], xs[3]);
+            mx[v] = h2max<Tin>(mx[v], xs[3]);
           }
         }
+        GroupQ gq[NGL];
+        bool bad = false;
+#pragma unroll
+        for (int v = 0; v < NGL; ++v) {
+          float hi = fmax_nan(h_lo<Tin>(mx[v]), h_hi<Tin>(mx[v]));
+          float lo = S1::SYM ? -hi : fmin_nan(h_lo<Tin>(mn[v]), h_hi<Tin>(mn[v]));
+          if constexpr (G > SL) {  // the partner lane holds the other half of the group
+            hi = fmax_nan(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+            lo = S1::SYM ? -hi : fmin_nan(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+          }
+          const bool b = !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
+          group_params<S1>(a.c1, lo, hi, gq[v]);
+          if (b) gq[v].z = S1::SYM ? gq[v].z : 0u;
+          bad |= b;
+        }
+        // ---- pass 2: re-read each chunk and encode it with its group's parameters
+        uint32_t w[NC * CWPC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const uint4 u = lds128_(gb + 16 * (c ^ m));
+          const uint32_t xs[4] = {u.x, u.y, u.z, u.w};
+          const GroupQ& g = gq[c / CPG];
+          if (g.normal)
+            chunk_codes_packed<S1, Tin>(xs, g, qmax, w + c * CWPC);
+          else
+            chunk_codes_clamped<S1, Tin>(xs, g.s, (int)g.z, (int)qmax, w + c * CWPC);
+        }
+        if constexpr (S1::SYM) {
+          const uint32_t xr = rep_xor(a.c1);
+#pragma unroll
+          for (int i = 0; i < NC * CWPC; ++i) w[i] ^= xr;
+        }
+        unswizzle_chunks<NC, CWPC>(w, m);
+        constexpr int NV = NC * CWPC / 4;  // 16-B code vectors per lane
+        constexpr int CB = 16 * NV;        // code bytes per lane
+        __syncwarp();  // every lane's shared loads of its slice are consumed
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(gb + 16 * (v ^ m)), "r"(w[4 * v]),
+                       "r"(w[4 * v + 1]), "r"(w[4 * v + 2]), "r"(w[4 * v + 3])
+                       : "memory");
+        __syncwarp();
+        const uint32_t wb = sbase + st * STAGE + part * 32 * (SL * 2);
+        fence_proxy_async_smem();
+        uint8_t* cw0 = jb.dst + ((int64_t)it.t * kTileElems + part * 32 * SL) * S1::SB / 8;
+#pragma unroll
+        for (int r = 0; r < NV; ++r) {
+          const int x = 512 * r + 16 * lane, l = x / CB, v = (x % CB) / 16;
+          st_v4(cw0 + x, lds128_(wb + l * (SL * 2) + 16 * (v ^ (l & 7))));
+        }
+        // ---- metadata of the slice's groups (physical group v ^ mg)
+        if constexpr (G > SL) {
+          if ((lane & 1) == 0) {
+            const int64_t grp = p0 / G;
+            *reinterpret_cast<unsigned short*>(jb.dst + a.c1.scales_off + 2 * grp) = gq[0].s16;
+            if constexpr (!S1::SYM) jb.dst[a.c1.zeros_off + grp] = (uint8_t)gq[0].z;
+          }
+        } else {
+          const int64_t grp0 = p0 / G;
+#pragma unroll
+          for (int v = 0; v < NGL; ++v) {
+            const int64_t grp = grp0 + (v ^ mg);
+            *reinterpret_cast<unsigned short*>(jb.dst + a.c1.scales_off + 2 * grp) = gq[v].s16;
+            if constexpr (!S1::SYM) jb.dst[a.c1.zeros_off + grp] = (uint8_t)gq[v].z;
+          }
+        }
+        // every store of the slice is issued: hand the stage back (FUSED: the producer publishes)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        if (bad && jb.err) atomicOr(jb.err, jb.ecode);
+      } else {
+        // ragged tail: the 32-element lane codec over this warp's 4096 elements, 1024 at a time
+        bool bad = false;
+        for (int sub = 0; sub < SL / 32; ++sub) {
+          const int64_t q0 = (int64_t)it.t * kTileElems + part * (32 * SL) + sub * (32 * kLaneElems) + lane * kLaneElems;
+          const int nvalid = lane_valid(a.sub_len, q0);
+          PackedLane<Tin> L;
+          load_lane_src(jb.src, q0, jb.limit, nvalid, L);
+          LaneQuant<8> q;
+          bad |= quantize_lane<S1>(a.c1, L, nvalid, q);
+          store_codes<S1>(a.c1, jb.dst, q0, nvalid, q, lane);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        if (bad && jb.err) atomicOr(jb.err, jb.ecode);
       }
     }
     ring_next(st, ph, S);
@@ -841,20 +1129,20 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   (void)S;
   if (warp == kGplWarps) {  // producer (lane 0 issues; FUSED: the warp waits for the peers' tile flags)
     int k = 0;
-    for (Iter it = it0; it.ok(); it.next(), ++k) {
-      const int j = a.rank_lo + it.y;
-      const int64_t e0 = (int64_t)it.t * kTileElems;
+    // item (y, t) as the k-th of this CTA: own input into own slot k & 1, peer pieces into the peer slot
+    auto issue = [&](int y, int t) {
+      const int j = a.rank_lo + y;
+      const int64_t e0 = (int64_t)t * kTileElems;
       const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
       const int64_t grp0 = e0 >> a.c1.gshift;
       const int os = k & 1;
       if (lane == 0) {
-        if (k >= 2) mbar_wait(own_empty + 8 * os, ((k >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(own_full + 8 * os, kTileElems * 2);
         bulk_g2s(sbase + os * (kTileElems * 2), reinterpret_cast<const Tin*>(a.in[j]) + seg0 + e0, kTileElems * 2,
                  own_full + 8 * os);
       }
       if constexpr (FUSED)  // lanes s != j wait for rank s's stage-1 piece of tile t (rflag[j][s][t])
-        warp_wait_flags(a, j, rflag(a, j, lane) + it.t, lane, lane < a.world && lane != j, kPhReduce);
+        warp_wait_flags(a, j, rflag(a, j, lane) + t, lane, lane < a.world && lane != j, kPhReduce);
       if (lane == 0) {
         if (k >= 1) mbar_wait(peer_empty, (k & 1) ^ 1);
         uint32_t dst = peer0;
@@ -872,6 +1160,61 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         }
       }
       __syncwarp();
+    };
+    if constexpr (!FUSED) {
+      for (Iter it = it0; it.ok(); it.next(), ++k) {
+        if (lane == 0 && k >= 2) mbar_wait(own_empty + 8 * (k & 1), ((k >> 1) & 1) ^ 1);
+        issue(it.y, it.t);
+      }
+    } else {
+      // dynamic dealing (DynIter); when own slot k & 1 comes back, item k-2 has stored its stage-2
+      // codes into every peer's gather slot: publish its gflags (publish_reduce)
+      const DynIter& D = it0;
+      int id = 0;
+      if (lane == 0) id = D.grab();
+      id = __shfl_sync(0xffffffffu, id, 0);
+      for (;; ++k) {
+        int nid = 0, old = -1;
+        if (lane == 0) {
+          if (id < D.items) nid = D.grab();  // the next id is in flight during this item
+          if (k >= 2) {
+            mbar_wait(own_empty + 8 * (k & 1), ((k >> 1) & 1) ^ 1);
+            old = lds_id(D.meta + 4 * (k & 1));
+          }
+          if (id < D.items) sts32(D.meta + 4 * (k & 1), id);
+        }
+        if (id >= D.items) {
+          if (lane == 0 && old >= 0) {
+            int y, t;
+            D.decode(old, y, t);
+            publish_reduce(a, y, t, D.ep);
+          }
+          break;
+        }
+        int y, t;
+        D.decode(id, y, t);
+        issue(y, t);
+        if (lane == 0 && old >= 0) {  // item k-2 stored its stage-2 codes into every peer's gather slot
+          int yo, to;
+          D.decode(old, yo, to);
+          publish_reduce(a, yo, to, D.ep);
+        }
+        id = __shfl_sync(0xffffffffu, nid, 0);
+      }
+      if (lane == 0) {
+        // end sentinel (every consumer warp reads it) in the slot recycled above, then the last
+        // real item's flags once its slot is back
+        sts32(D.meta + 4 * (k & 1), -1);
+        mbar_arrive(own_full + 8 * (k & 1));
+        if (k >= 1) {
+          const int kp = k - 1;
+          mbar_wait(own_empty + 8 * (kp & 1), (uint32_t)(kp >> 1) & 1u);
+          int y, t;
+          D.decode(lds_id(D.meta + 4 * (kp & 1)), y, t);
+          publish_reduce(a, y, t, D.ep);
+        }
+      }
+      __syncwarp();
     }
     return;
   }
@@ -881,11 +1224,10 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   const bool lead = (li & (kRgLpg - 1)) == 0;
   const uint32_t xr1 = rep_xor(a.c1), xr2 = rep_xor(a.c2);
   const uint32_t qmax1 = (1u << a.c1.bits) - 1u, qmax2 = (1u << a.c2.bits) - 1u;
-  int k = 0;
-  for (Iter it = it0; it.ok(); it.next(), ++k) {
-    const int j = a.rank_lo + it.y;
+  auto item = [&](int k, int y, int t) {
+    const int j = a.rank_lo + y;
     const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
-    const int64_t e0 = (int64_t)it.t * kTileElems;
+    const int64_t e0 = (int64_t)t * kTileElems;
     const int64_t p0 = e0 + li * kRgEpl;  // lane slice start in the round
     const int os = k & 1;
     const uint32_t own_base = sbase + os * (kTileElems * 2);
@@ -1098,18 +1440,6 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
           if constexpr (!S2::SYM) b[a.c2.zeros_off + grp] = (uint8_t)g2.z;
         }
       }
-      if constexpr (FUSED) {
-        // the 4 consumer warps stored the whole tile into every peer's gather slot [j]:
-        // publish gflag[p][j][t] for every peer p
-        consumers_sync<kGplWarps * 32>();
-        if (threadIdx.x == 0) {
-          const uint32_t ep = flag_epoch(a);
-          if (a.sys_scope) __threadfence_system();
-          else __threadfence();
-          for (int p = 0; p < a.world; ++p)
-            if (p != j) st_relaxed_sys(gflag(a, p, j) + it.t, ep);
-        }
-      }
     }
     // ---- own output: the owner decodes its own payload (collectives.py:378), staged
     // through the warp's own 4-KB buffer (swizzled), then one coalesced copy
@@ -1144,6 +1474,20 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
       if (lane == 0) mbar_arrive(own_empty + 8 * os);
     }
     if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
+  };
+  if constexpr (!FUSED) {
+    int k = 0;
+    for (Iter it = it0; it.ok(); it.next(), ++k) item(k, it.y, it.t);
+  } else {
+    const DynIter& D = it0;
+    for (int k = 0;; ++k) {
+      mbar_wait(own_full + 8 * (k & 1), (k >> 1) & 1);
+      const int id = lds_id(D.meta + 4 * (k & 1));
+      if (id < 0) break;
+      int y, t;
+      D.decode(id, y, t);
+      item(k, y, t);
+    }
   }
 }
 
@@ -1400,31 +1744,57 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
     int st = 0, k = 0, cy = -1;
     uint32_t ph = 0;
     DJob<Tout> d;
-    for (Iter it = it0; it.ok(); it.next(), ++k) {
-      if constexpr (FUSED) {
-        int r, j;
-        pair_of(a, it.y, r, j);
-        warp_wait_flags(a, r, gflag(a, r, j) + it.t, j, lane == 0, kPhGather);
+    auto issue = [&](int y, int t, bool wait_empty) {  // lane 0
+      if (wait_empty) mbar_wait(empty0 + 8 * st, ph ^ 1);
+      if (y != cy) {
+        d = djob<Tout>(a, y);
+        cy = y;
       }
-      if (lane == 0) {
-        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
-        if (it.y != cy) {
-          d = djob<Tout>(a, it.y);
-          cy = it.y;
+      const int64_t e0 = (int64_t)t * kTileElems;
+      const int64_t v = clamp0(min((int64_t)kTileElems, min(a.sub_len - e0, d.limit - e0)));
+      const int64_t grp0 = e0 >> gs, ng = (v + c.g - 1) >> gs;
+      const uint32_t cb = v > 0 ? up16(v * S2::SB / 8) : 0u, sb = v > 0 ? up16(ng * 2) : 0u;
+      const uint32_t zb = (v > 0 && !S2::SYM) ? up16(ng) : 0u;
+      const uint32_t dst = sbase + st * SBY, bar = full0 + 8 * st;
+      mbar_arrive_expect_tx(bar, cb + sb + zb);
+      if (cb) bulk_g2s(dst, d.src + e0 * S2::SB / 8, cb, bar);
+      if (sb) bulk_g2s(dst + PC, d.src + c.scales_off + grp0 * 2, sb, bar);
+      if (zb) bulk_g2s(dst + PC + SCB, d.src + c.zeros_off + grp0, zb, bar);
+    };
+    if constexpr (!FUSED) {
+      for (Iter it = it0; it.ok(); it.next(), ++k) {
+        if (lane == 0) issue(it.y, it.t, k >= S);
+        __syncwarp();
+        ring_next(st, ph, S);
+      }
+    } else {
+      const DynIter& D = it0;  // dynamic dealing; the owner's gflag is awaited before the copies
+      int id = 0;
+      if (lane == 0) id = D.grab();
+      id = __shfl_sync(0xffffffffu, id, 0);
+      for (;; ++k) {
+        if (id >= D.items) break;
+        int nid = 0;
+        if (lane == 0) nid = D.grab();  // the next id is in flight during this item
+        int y, t, r, j;
+        D.decode(id, y, t);
+        pair_of(a, y, r, j);
+        warp_wait_flags(a, r, gflag(a, r, j) + t, j, lane == 0, kPhGather);
+        if (lane == 0) {
+          if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+          sts32(D.meta + 4 * st, id);
+          issue(y, t, false);
         }
-        const int64_t e0 = (int64_t)it.t * kTileElems;
-        const int64_t v = clamp0(min((int64_t)kTileElems, min(a.sub_len - e0, d.limit - e0)));
-        const int64_t grp0 = e0 >> gs, ng = (v + c.g - 1) >> gs;
-        const uint32_t cb = v > 0 ? up16(v * S2::SB / 8) : 0u, sb = v > 0 ? up16(ng * 2) : 0u;
-        const uint32_t zb = (v > 0 && !S2::SYM) ? up16(ng) : 0u;
-        const uint32_t dst = sbase + st * SBY, bar = full0 + 8 * st;
-        mbar_arrive_expect_tx(bar, cb + sb + zb);
-        if (cb) bulk_g2s(dst, d.src + e0 * S2::SB / 8, cb, bar);
-        if (sb) bulk_g2s(dst + PC, d.src + c.scales_off + grp0 * 2, sb, bar);
-        if (zb) bulk_g2s(dst + PC + SCB, d.src + c.zeros_off + grp0, zb, bar);
+        __syncwarp();
+        ring_next(st, ph, S);
+        id = __shfl_sync(0xffffffffu, nid, 0);
+      }
+      if (lane == 0) {  // end sentinel
+        if (k >= S) mbar_wait(empty0 + 8 * st, ph ^ 1);
+        sts32(D.meta + 4 * st, -1);
+        mbar_arrive(full0 + 8 * st);
       }
       __syncwarp();
-      ring_next(st, ph, S);
     }
     return;
   }
@@ -1433,15 +1803,14 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
   const uint32_t code_off = threadIdx.x * S2::SB;                // bytes of 8 codes of SB bits
   const uint32_t grp_off = (uint32_t)(threadIdx.x * 8) >> gs;    // tile-local group of block 0
   const uint32_t grp_step = (uint32_t)(NT * 8) >> gs;            // groups per block step
-  int st = 0, cy = -1;
-  uint32_t ph = 0;
+  int cy = -1;
   DJob<Tout> d;
-  for (Iter it = it0; it.ok(); it.next()) {
-    if (it.y != cy) {
-      d = djob<Tout>(a, it.y);
-      cy = it.y;
+  auto item = [&](int y, int t, int st, uint32_t ph) {
+    if (y != cy) {
+      d = djob<Tout>(a, y);
+      cy = y;
     }
-    const int64_t e0 = (int64_t)it.t * kTileElems;
+    const int64_t e0 = (int64_t)t * kTileElems;
     const int64_t v = min(a.sub_len - e0, d.limit - e0);  // valid elements from e0
     const uint32_t tile = sbase + st * SBY;
     Tout* obase = d.out + e0 + threadIdx.x * 8;
@@ -1504,7 +1873,25 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
         }
       }
     }
-    ring_next(st, ph, S);
+  };
+  int st = 0;
+  uint32_t ph = 0;
+  if constexpr (!FUSED) {
+    for (Iter it = it0; it.ok(); it.next()) {
+      item(it.y, it.t, st, ph);
+      ring_next(st, ph, S);
+    }
+  } else {
+    const DynIter& D = it0;
+    for (;;) {
+      mbar_wait(full0 + 8 * st, ph);
+      const int id = lds_id(D.meta + 4 * st);
+      if (id < 0) break;
+      int y, t;
+      D.decode(id, y, t);
+      item(y, t, st, ph);
+      ring_next(st, ph, S);
+    }
   }
 }
 
@@ -1523,6 +1910,14 @@ __global__ void __launch_bounds__(kGplThreads, 3) k_qstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
   q_role_gpl<Tin, S1, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+}
+
+// any g in {32, 64, 128, 256}, INT4 or INT8, one lane per 128-element slice (q_role_gq)
+template <typename Tin, class S1, int G>
+__global__ void __launch_bounds__(kGplThreads, 4) k_qstream_gq(FlashArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
+  q_role_gq<Tin, S1, G, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
 template <typename Tin, typename Tout, class S1, class S2>
@@ -1554,7 +1949,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
 // and one barrier region behind it, so a role's barriers never overlay
 // another role's data
 struct FusedSmem {
-  int q_stages, d_stages, data_bytes, bars_off, max_bars, total;
+  int q_stages, d_stages, data_bytes, bars_off, max_bars, meta_off, total;
 };
 __host__ __device__ inline FusedSmem fused_smem(const DevCodec& c1, const DevCodec& c2, int world, int qs, int ds) {
   FusedSmem f;
@@ -1567,7 +1962,8 @@ __host__ __device__ inline FusedSmem fused_smem(const DevCodec& c1, const DevCod
   f.bars_off = (f.data_bytes + 127) & ~127;
   const int nq = 2 * qs, nr = 4 + world, nd = 2 * ds;
   f.max_bars = nq > nr ? (nq > nd ? nq : nd) : (nr > nd ? nr : nd);
-  f.total = f.bars_off + 8 * f.max_bars;
+  f.meta_off = f.bars_off + 8 * f.max_bars;  // DynIter id ring: one int per stage (<= 16)
+  f.total = f.meta_off + 64;
   return f;
 }
 
@@ -1588,18 +1984,22 @@ __device__ __forceinline__ void fused_role_switch(uint32_t bars, int nb) {
 // reduce (r_role_gpl: N-1 received pieces + own QDQ -> fp32 rank-ordered sum ->
 // stage-2 quantize -> every peer's gather slot) and gather (d_role: decode the
 // owners' stage-2 pieces) — synchronised only by per-tile epoch flags (rflag /
-// gflag: release after a tile's stores, acquire before its bulk copies).
+// gflag: published by a role's producer warp once the tile's stores are
+// issued, acquired before the tile's bulk copies).
 // The segment's tiles are cut into chunks of a.fp_chunk tiles; at step s a CTA
 // scatters chunk s, reduces chunk s-1 and gathers chunk s-2, so NVLink-bound
 // scatter/reduce traffic of one chunk overlaps the HBM-bound gather of an
-// earlier one. Items of a (role, chunk) are dealt round-robin over the grid
-// (rotated per chunk). Every wait targets an item of an earlier step (on any
-// rank), and all CTAs are co-resident (cooperative launch), so the schedule
-// cannot deadlock.
+// earlier one. Items of a (role, chunk) are dealt dynamically (DynIter: a
+// global counter per (role, chunk), tile-major ids). A CTA enters a role only
+// after every item of the previous (role, chunk) was taken, every wait
+// targets an item of an earlier step (on any rank), and all CTAs are
+// co-resident (cooperative launch), so the schedule cannot deadlock. The
+// launch's last CTA zeroes the counters for the next launch.
 template <typename Tin, typename Tout, class S1, class S2>
 __global__ void __launch_bounds__(kGplThreads, 3) k_fstream(const __grid_constant__ FlashArgs a) {
   if constexpr (sizeof(Tin) == 2 && sizeof(Tout) == 2 && S1::SB == S2::SB) {
     extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ int s_last;
     const uint32_t sb = smem_u32(smem);
     const uint32_t bars = sb + (uint32_t)a.fp_bars;
     const int G = (int)gridDim.x, cta = (int)blockIdx.x;
@@ -1607,33 +2007,52 @@ __global__ void __launch_bounds__(kGplThreads, 3) k_fstream(const __grid_constan
     const int P = nr * (a.world - 1);
     const int B = a.fp_chunk;
     const int nch = (a.tiles + B - 1) / B;
+    uint32_t* ctr = fctr(a, a.rank_lo);
+    const uint32_t ep = flag_epoch(a);  // the round's epoch (k_epoch_bump ran before this launch)
     int nb = 0;
+    uint64_t* tp = a.tprof ? a.tprof + (int64_t)cta * FC_ROLE_PROFILE_U64 : nullptr;
+    if (tp && threadIdx.x == 0) tp[9] = globaltimer();
 #pragma unroll 1
     for (int s = 0; s < nch + 2; ++s) {
 #pragma unroll 1
       for (int role = 0; role < 3; ++role) {
         const int c = s - role;
         if (c < 0 || c >= nch) continue;
+        if (role == 2 && cta >= a.fp_dctas) continue;  // measurement option: fewer gather CTAs
         const int t0 = c * B, bt = min(B, a.tiles - t0);
         const int per = role == 1 ? nr : P;
-        const int items = per * bt;
-        // item i of this (role, chunk) runs on CTA (base + i) mod G
-        const int base = (int)(((int64_t)c * per * B + (int64_t)role * (G / 3)) % G);
-        const int first = cta >= base ? cta - base : cta - base + G;
-        if (first >= items) continue;
         fused_role_switch(bars, nb);
-        const RoundIter it(items, per, first, G, t0);
-        if (role == 0) {
-          q_role_gpl<Tin, S1, true>(a, sb, a.q_stages_f, it, bars);
-          nb = 2 * a.q_stages_f;
-        } else if (role == 1) {
-          r_role_gpl<Tin, Tout, S1, S2, true>(a, sb, 1, it, bars);
-          nb = 4 + a.world;
-        } else {
-          d_role<Tout, S2, true, RoundIter, kGplWarps>(a, sb, a.d_stages_f, it, bars);
-          nb = 2 * a.d_stages_f;
+        const uint64_t r0 = tp ? globaltimer() : 0;
+        const DynIter it{ctr + role * kFusedMaxChunks + c, per * bt, per, t0, sb + (uint32_t)a.fp_meta, ep};
+        if (role == 0) q_role_gpl<Tin, S1, true>(a, sb, a.q_stages_f, it, bars);
+        else if (role == 1) r_role_gpl<Tin, Tout, S1, S2, true>(a, sb, 1, it, bars);
+        else d_role<Tout, S2, true, DynIter, kGplWarps>(a, sb, a.d_stages_f, it, bars);
+        nb = role == 0 ? 2 * a.q_stages_f : role == 1 ? 4 + a.world : 2 * a.d_stages_f;
+        if (tp) {
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            const uint64_t r1 = globaltimer();
+            if (!tp[role]) tp[role] = r0;
+            tp[3 + role] = r1;
+            tp[6 + role] += r1 - r0;
+          }
         }
       }
+    }
+    // the last CTA to finish zeroes the (role, chunk) counters for the next launch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(ctr + 3 * kFusedMaxChunks, 1u) == (uint32_t)(G - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+      for (int i = threadIdx.x; i < 3 * nch; i += blockDim.x) ctr[(i / nch) * kFusedMaxChunks + i % nch] = 0u;
+      if (threadIdx.x == 0) ctr[3 * kFusedMaxChunks] = 0u;
+    }
+    if (tp) {
+      __syncthreads();
+      if (threadIdx.x == 0) tp[10] = globaltimer();
     }
   }
 }

@@ -147,16 +147,19 @@ def fused_tune():
     print(json.dumps({"kernel": "flash_split", "ms": t, "frac": alg / t / 1e6 / PEAK}), flush=True)
     comm.set_option(_lib.OPT_FUSED, 1)
     tiles = seg // 8192
-    for chunk in (0, tiles // 2, tiles // 4, tiles // 8):
-        for qs, ds, cap in ((0, 0, 0), (4, 4, 0), (4, 8, 0), (6, 0, 0), (4, 0, 2)):
+    for chunk in (0, tiles // 4):
+        for qs, ds, cap, gc in ((0, 0, 0, 0), (4, 4, 0, 0), (4, 8, 0, 0), (6, 0, 0, 0), (0, 0, 0, 1), (0, 6, 0, 1),
+                                (0, 0, 0, 2), (4, 0, 2, 0)):
             comm.set_option(_lib.OPT_FUSED_CHUNK, chunk)
             comm.set_option(_lib.OPT_SCATTER_STAGES, qs)
             comm.set_option(_lib.OPT_GATHER_STAGES, ds)
             comm.set_option(_lib.OPT_CTAS_PER_SM, cap)
+            comm.set_option(_lib.OPT_FUSED_GATHER_CTAS, gc)
             t = timeit(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), iters=10, warm=3)
             comm.check()
             print(json.dumps({"kernel": "flash_fused_tune", "chunk": chunk, "q_stages": qs, "d_stages": ds,
-                              "cta_cap": cap, "ms": t, "frac": alg / t / 1e6 / PEAK}), flush=True)
+                              "cta_cap": cap, "gather_ctas_per_sm": gc, "ms": t, "frac": alg / t / 1e6 / PEAK}),
+                  flush=True)
     comm.close()
 
 
