@@ -507,11 +507,18 @@ def bench_local(args, cfg, peaks):
     # ---- per-phase kernels (measurement option: one phase per call), CUDA events on the launch stream
     b1 = wire_len(cfg["bits"], cfg["group"], seg) / seg
     b2 = b1
-    phase_bytes = {"scatter": tp * (tp - 1) * seg * (e + b1),
-                   "reduce": tp * seg * (2 * e + (tp - 1) * (b1 + b2)),
+    # g = 128 (one storage width) runs the 2-lanes-per-group reduce, which reads every source
+    # piece from the receive slots, the own one too: the scatter then also quantizes the own
+    # piece (ownq, fc_stream.cuh r_role_gpl). Per-phase bytes are what each kernel must move;
+    # the step's algorithmic bytes stay the minimum (own piece kept on chip), so
+    # the ownq detour (+2 b1 per own element) counts against the step fraction
+    ownq = 1 if cfg["group"] == 128 else 0
+    phase_bytes = {"scatter": tp * (tp - 1 + ownq) * seg * (e + b1),
+                   "reduce": tp * seg * ((tp - 1 + ownq) * b1 + (1 - ownq) * e + (tp - 1) * b2 + e),
                    "gather": tp * (tp - 1) * seg * (b2 + e)}
-    # INT4 g = 128 runs the group-per-lane scatter and the 2-lanes-per-group reduce
-    # (fc_stream.cuh q_role_gpl / r_role_gpl; the reduce needs whole tiles, true for every config here)
+    # per rank: input read + output write (2 e M) + the N-1 peer pieces of both stages written and read once
+    alg_step = tp * (2 * e * m + 2 * (tp - 1) * seg * (b1 + b2))
+    # INT4 g = 128 runs the group-per-lane scatter (q_role_gpl)
     gpl = cfg["group"] == 128 and cfg["bits"] == 4
     phase_kernel = {"scatter": "k_qstream_gpl" if gpl else "k_qstream",
                     "reduce": "k_rstream_gpl" if cfg["group"] == 128 else "k_rstream", "gather": "k_dstream"}
@@ -537,7 +544,6 @@ def bench_local(args, cfg, peaks):
     comm.set_option(_lib.OPT_FUSED, 1 if args.fused else -1)
     dom = max(phases, key=lambda k: phases[k]["us"])
     traffic = load_traffic(args.config).get(phases[dom]["kernel"])
-    alg_step = sum(phase_bytes.values())
     roofline = {"bound": "hbm", "kernel": phases[dom]["kernel"], "achieved": phases[dom]["gbs"],
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": phases[dom]["frac"],
                 "traffic": traffic, "alg_bytes_per_launch": phases[dom]["alg_bytes"],

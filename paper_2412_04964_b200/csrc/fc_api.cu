@@ -320,7 +320,7 @@ fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
       break;
     case FC_OPT_LAG: c->lag = std::max<int64_t>(0, value); break;
     case FC_OPT_FAST: c->fast = value < 0 ? 0 : (value > 2 ? 2 : value); break;
-    case FC_OPT_REDUCE_STAGES: c->reduce_stages = std::max<int64_t>(0, std::min<int64_t>(4, value)); break;
+    case FC_OPT_REDUCE_STAGES: c->reduce_stages = std::max<int64_t>(0, std::min<int64_t>(32, value)); break;
     case FC_OPT_SCATTER_STAGES: c->q_stages = std::max<int64_t>(0, std::min<int64_t>(8, value)); break;
     case FC_OPT_GATHER_STAGES: c->d_stages = std::max<int64_t>(0, std::min<int64_t>(12, value)); break;
     case FC_OPT_CTAS_PER_SM: c->ctas_per_sm = std::max<int64_t>(0, std::min<int64_t>(16, value)); break;

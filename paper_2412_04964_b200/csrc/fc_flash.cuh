@@ -48,6 +48,9 @@ struct FlashArgs {
   int fp_bars;              // fused stream kernel: byte offset of the barrier region in shared memory
   int fp_meta;              // fused stream kernel: byte offset of the DynIter id ring in shared memory
   int q_stages_f, d_stages_f;  // fused stream kernel ring depths of the scatter / gather roles
+  int r_ring_f;             // fused stream kernel: piece-slot ring depth of the reduce role
+  int ownq;                 // 1: the scatter also stage-1 quantizes the own piece into recv_slot[r][r]
+                            // (the group-lane reduce reads every source from the slots)
   int sys_scope;            // flags cross GPUs: system-scope fences; else gpu scope (one GPU)
   int dbg;                  // FC_OPT_STREAM_MASK A/B bits (include/flashcomm.h)
   DevCodec c1, c2;
@@ -283,6 +286,16 @@ __device__ __forceinline__ void pair_of(const FlashArgs& a, int y, int& r, int& 
   j = r + 1 + y % P;
   if (j >= a.world) j -= a.world;
 }
+
+// scatter job y -> (rank r, destination j): with ownq every rank has world jobs,
+// the last one its own piece (j == r), else world - 1 (peers only)
+__device__ __forceinline__ void qpair_of(const FlashArgs& a, int y, int& r, int& j) {
+  const int P = a.world - 1 + a.ownq;
+  r = a.rank_lo + y / P;
+  j = r + 1 + y % P;
+  if (j >= a.world) j -= a.world;
+}
+__device__ __forceinline__ int q_jobs(const FlashArgs& a) { return (a.rank_hi - a.rank_lo) * (a.world - 1 + a.ownq); }
 
 __device__ __forceinline__ int lane_valid(int64_t len, int64_t p0) {
   const int64_t d = len - p0;

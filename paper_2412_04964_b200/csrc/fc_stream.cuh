@@ -56,7 +56,7 @@ __device__ __forceinline__ QJob<Tin> qjob(const FlashArgs& a, int y) {
     return q;
   }
   int r, j;
-  pair_of(a, y, r, j);
+  qpair_of(a, y, r, j);
   const int64_t off = (int64_t)j * a.seg + a.sub_off;
   q.src = reinterpret_cast<const Tin*>(a.in[r]) + off;
   q.limit = a.M - off;
@@ -324,7 +324,7 @@ __device__ __forceinline__ void publish_flag(const FlashArgs& a, uint32_t* f, ui
 __device__ __forceinline__ void publish_scatter(const FlashArgs& a, int y, int t, uint32_t ep) {
   if (a.dbg & 512) return;  // measurement only
   int r, j;
-  pair_of(a, y, r, j);
+  qpair_of(a, y, r, j);
   publish_flag(a, rflag(a, j, r) + t, ep);
 }
 __device__ __forceinline__ void publish_reduce(const FlashArgs& a, int y, int t, uint32_t ep) {
@@ -424,7 +424,7 @@ __device__ __forceinline__ void q_role(const FlashArgs& a, uint32_t sbase, int S
       consumers_sync();
       if (threadIdx.x == 0) {
         int r, j;
-        pair_of(a, it.y, r, j);
+        qpair_of(a, it.y, r, j);
         if (a.sys_scope) {
           __threadfence_system();
           st_relaxed_sys(rflag(a, j, r) + it.t, flag_epoch(a));
@@ -1072,34 +1072,52 @@ __device__ __forceinline__ float acc_get(const uint64_t* acc, int e) {
   }
 }
 
-// INT4 g = 128 reduce with 64 elements per lane, 2 lanes per group
-// (k_rstream_gpl). The 32-element layout of r_role spreads a group over 4
-// lanes, so each lane repeats both quantizations' bound reductions (two
-// shuffle steps), float64 scales and zero points; here a lane pair shares a
-// group (one shuffle step, half the repeated tail), and the lane keeps its
-// 64 fp32 accumulators in registers (32 pairs in the INT4 pairing: decode,
-// accumulate and re-encode never move registers). Own-group stage-1 QDQ
-// (collectives.py:364-365), rank-ordered fp32 sum (collectives.py:182-187),
-// stage-2 quantize, peers' gather slots, own output. Whole tiles only
-// (launch_rstream falls back to r_role otherwise). Two rings: two own-input
-// slots (the next tile's own input lands while this one runs; the lane's
-// 128-B region of its slot parks its own codes during the sum and stages its
-// output, XOR-swizzled, before one coalesced copy per warp) and one slot for
-// the N-1 peer pieces, handed back right after the source loop.
+// g = 128 reduce with 64 elements per lane, 2 lanes per group (k_rstream_gpl).
+// Every source piece -- the own one included -- comes from the receive slots:
+// with FlashArgs::ownq the scatter also stage-1 quantizes the rank's own piece
+// into recv_slot[j][j] (collectives.py:364-365: the own piece is QDQ'd like
+// the others), so the reduce never reads the bf16 input and never repeats the
+// stage-1 group statistics; it decodes N pieces in ascending source rank
+// (collectives.py:182-187), stage-2 quantizes the fp32 sum, stores the codes
+// into every peer's gather slot [j] and decodes its own output
+// (collectives.py:378). The 32-element layout of r_role spreads a group over 4
+// lanes; here a lane pair shares a group (one shuffle step) and a lane keeps
+// its 64 fp32 accumulators as 32 register pairs in the codec's pairing
+// (decode, accumulate and re-encode never move registers).
+// Shared memory: a ring of R piece slots (codes | fp16 scales | zeros, one
+// source's share of a tile, full/empty mbarrier per slot) that the producer
+// warp streams continuously -- piece (item k, source s) lands in slot
+// (k N + s) % R and is handed back by the 4 consumer warps as soon as they
+// decoded it, so the next tile's pieces land during this tile's sum, stage-2
+// quantize and stores -- plus a 4-KB output staging buffer per warp (the
+// output leaves as one coalesced 512-B store per warp instruction).
+// FUSED: the producer waits for every source's rflag of the tile before its
+// copies and publishes gflag of item k-2 once the consumers' done barrier of
+// that item completed (every stage-2 store into a peer's gather slot issued).
+// Whole tiles only (launch_rstream falls back to r_role otherwise).
 constexpr int kRgEpl = 64;                              // elements per lane
 constexpr int kRgLpg = kGplG / kRgEpl;                  // lanes per group (2)
 constexpr int kRgWpt = kTileElems / (32 * kRgEpl);      // warps per tile (4)
+constexpr uint32_t kRgStage = kTileElems * 2;           // output staging bytes (4 KB per warp)
+constexpr int kRgMaxRing = 32;                          // piece slots at most
+constexpr int kRgDone = 4;                              // FUSED: done-barrier ring (publish lag 2)
 
-// peer slot bytes and total shared memory of the group-lane reduce (2 own slots + 1 peer slot)
-__host__ __device__ inline uint32_t rg_peer_bytes(const DevCodec& c1, int world) {
-  return (uint32_t)(world - 1) * (peer_codes_bytes(c1) + peer_meta_bytes(c1));
+// bytes of one piece slot, the barrier region, the whole layout for a ring of R slots
+__host__ __device__ inline uint32_t rg_piece_bytes(const DevCodec& c1) { return peer_codes_bytes(c1) + peer_meta_bytes(c1); }
+__host__ __device__ inline uint32_t rg_bars_off(const DevCodec& c1, int R) { return kRgStage + (uint32_t)R * rg_piece_bytes(c1); }
+__host__ __device__ inline uint32_t rg_smem_bytes(const DevCodec& c1, int R) {
+  return rg_bars_off(c1, R) + 8 * (2 * R + kRgDone) + 4 * (R + kRgDone);
 }
-__host__ __device__ inline uint32_t rg2_smem_bytes(const DevCodec& c1, int world) {
-  return 2 * kTileElems * 2 + rg_peer_bytes(c1, world) + 8 * (4 + world);
+// ring depth for a per-CTA shared-memory budget (at least 2)
+__host__ __device__ inline int rg_ring_for(const DevCodec& c1, uint32_t budget) {
+  const uint32_t per = rg_piece_bytes(c1) + 8 * 2 + 4;
+  const uint32_t fixed = kRgStage + 12 * kRgDone;
+  int R = budget > fixed ? (int)((budget - fixed) / per) : 0;
+  return R < 2 ? 2 : (R > kRgMaxRing ? kRgMaxRing : R);
 }
 
 template <typename Tin, typename Tout, class S1, class S2, bool FUSED, class Iter>
-__device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0, uint32_t bars_in = 0) {
+__device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, int R, Iter it0, uint32_t bars_in = 0) {
   static_assert(sizeof(Tin) == 2 && sizeof(Tout) == 2, "16-bit inputs and outputs");
   static_assert(S1::SB == S2::SB, "one storage width for both stages");
   static_assert(kGplWarps == kRgWpt, "one tile per pass of the consumer warps");
@@ -1108,112 +1126,93 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   constexpr int CWPC = SB / 4;           // code words per chunk
   constexpr int NW = NC * CWPC;          // code words per lane
   const uint32_t PC = peer_codes_bytes(a.c1), PM = peer_meta_bytes(a.c1), SCB = peer_scale_bytes(a.c1);
+  const uint32_t PB = PC + PM;
   const int NP = a.world;
-  // two rings: own-input slots (2 x 16 KB: the next tile's own input lands while this one
-  // runs; a slot also stages the lane's parked own codes and its output) and one slot for
-  // the N-1 peer pieces (handed back right after the source loop)
-  const uint32_t peer0 = sbase + 2 * kTileElems * 2;
-  const uint32_t bars = bars_in ? bars_in : peer0 + rg_peer_bytes(a.c1, a.world);
-  const uint32_t own_full = bars, own_empty = bars + 16, peer_full = bars + 32, peer_empty = peer_full + 8 * (NP - 1);
+  const uint32_t ring0 = sbase + kRgStage;
+  const uint32_t bars = bars_in ? bars_in : sbase + rg_bars_off(a.c1, R);
+  const uint32_t full0 = bars, empty0 = bars + 8 * R, done0 = bars + 16 * R;
+  const uint32_t meta = done0 + 8 * kRgDone;  // FUSED: item id beside the slot of its first piece
+  const uint32_t hist = meta + 4 * R;         // FUSED: ids of the last kRgDone items (producer)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(own_full + 8 * s, 1);
-      mbar_init(own_empty + 8 * s, kRgWpt);
+    for (int s = 0; s < R; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, kRgWpt);
     }
-    for (int s = 0; s < NP - 1; ++s) mbar_init(peer_full + 8 * s, 1);
-    mbar_init(peer_empty, kRgWpt);
+    for (int s = 0; s < kRgDone; ++s) mbar_init(done0 + 8 * s, kRgWpt);
     fence_mbar_init();
   }
   __syncthreads();
-  (void)S;
-  if (warp == kGplWarps) {  // producer (lane 0 issues; FUSED: the warp waits for the peers' tile flags)
-    int k = 0;
-    // item (y, t) as the k-th of this CTA: own input into own slot k & 1, peer pieces into the peer slot
-    auto issue = [&](int y, int t) {
+  if (warp == kGplWarps) {  // producer (lane 0 issues; FUSED: the warp waits for the tile's rflags)
+    // ring position of the next piece: slot, phase, whether the slot was used before
+    // (incremental: a runtime modulo costs ~20 instructions per piece)
+    uint32_t psl = 0, pph = 0;
+    bool pused = false;
+    auto slot_acquire = [&]() -> uint32_t {  // lane 0: the next ring slot, once handed back
+      const uint32_t sl = psl;
+      if (pused) mbar_wait(empty0 + 8 * sl, pph ^ 1u);
+      if (++psl == (uint32_t)R) {
+        psl = 0;
+        pph ^= 1u;
+        pused = true;
+      }
+      return sl;
+    };
+    auto issue = [&](int y, int t, int id) {
       const int j = a.rank_lo + y;
       const int64_t e0 = (int64_t)t * kTileElems;
-      const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
       const int64_t grp0 = e0 >> a.c1.gshift;
-      const int os = k & 1;
+      if constexpr (FUSED)  // lane s waits for rank s's stage-1 piece of tile t (rflag[j][s][t])
+        warp_wait_flags(a, j, rflag(a, j, lane) + t, lane, lane < a.world, kPhReduce);
       if (lane == 0) {
-        mbar_arrive_expect_tx(own_full + 8 * os, kTileElems * 2);
-        bulk_g2s(sbase + os * (kTileElems * 2), reinterpret_cast<const Tin*>(a.in[j]) + seg0 + e0, kTileElems * 2,
-                 own_full + 8 * os);
-      }
-      if constexpr (FUSED)  // lanes s != j wait for rank s's stage-1 piece of tile t (rflag[j][s][t])
-        warp_wait_flags(a, j, rflag(a, j, lane) + t, lane, lane < a.world && lane != j, kPhReduce);
-      if (lane == 0) {
-        if (k >= 1) mbar_wait(peer_empty, (k & 1) ^ 1);
-        uint32_t dst = peer0;
-        int piece = 0;
-        for (int s = 0; s < a.world; ++s) {
-          if (s == j) continue;
-          const uint32_t bar = peer_full + 8 * piece++;
-          const uint8_t* slot = recv_slot(a, j, s);
-          const uint32_t zb = S1::SYM ? 0u : PM - SCB;
+        const uint32_t zb = S1::SYM ? 0u : PM - SCB;
+        for (int s = 0; s < NP; ++s) {
+          const uint32_t sl = slot_acquire();
+          if (FUSED && s == 0) sts32(meta + 4 * sl, id);
+          const uint32_t bar = full0 + 8 * sl, dst = ring0 + sl * PB;
+          const uint8_t* src = recv_slot(a, j, s);
           mbar_arrive_expect_tx(bar, PC + SCB + zb);
-          bulk_g2s(dst, slot + e0 * SB / 8, PC, bar);
-          bulk_g2s(dst + PC, slot + a.c1.scales_off + grp0 * 2, SCB, bar);
-          if (zb) bulk_g2s(dst + PC + SCB, slot + a.c1.zeros_off + grp0, zb, bar);
-          dst += PC + PM;
+          bulk_g2s(dst, src + e0 * SB / 8, PC, bar);
+          bulk_g2s(dst + PC, src + a.c1.scales_off + grp0 * 2, SCB, bar);
+          if (zb) bulk_g2s(dst + PC + SCB, src + a.c1.zeros_off + grp0, zb, bar);
         }
       }
       __syncwarp();
     };
     if constexpr (!FUSED) {
-      for (Iter it = it0; it.ok(); it.next(), ++k) {
-        if (lane == 0 && k >= 2) mbar_wait(own_empty + 8 * (k & 1), ((k >> 1) & 1) ^ 1);
-        issue(it.y, it.t);
-      }
+      for (Iter it = it0; it.ok(); it.next()) issue(it.y, it.t, 0);
     } else {
-      // dynamic dealing (DynIter); when own slot k & 1 comes back, item k-2 has stored its stage-2
-      // codes into every peer's gather slot: publish its gflags (publish_reduce)
+      // dynamic dealing (DynIter); after issuing item k, wait for item k-2's done barrier (its
+      // stage-2 codes are stored into every peer's gather slot) and publish its gflags
       const DynIter& D = it0;
-      int id = 0;
+      int id = 0, k = 0;
       if (lane == 0) id = D.grab();
       id = __shfl_sync(0xffffffffu, id, 0);
-      for (;; ++k) {
-        int nid = 0, old = -1;
+      auto publish_k = [&](int kk) {
         if (lane == 0) {
-          if (id < D.items) nid = D.grab();  // the next id is in flight during this item
-          if (k >= 2) {
-            mbar_wait(own_empty + 8 * (k & 1), ((k >> 1) & 1) ^ 1);
-            old = lds_id(D.meta + 4 * (k & 1));
-          }
-          if (id < D.items) sts32(D.meta + 4 * (k & 1), id);
-        }
-        if (id >= D.items) {
-          if (lane == 0 && old >= 0) {
-            int y, t;
-            D.decode(old, y, t);
-            publish_reduce(a, y, t, D.ep);
-          }
-          break;
-        }
-        int y, t;
-        D.decode(id, y, t);
-        issue(y, t);
-        if (lane == 0 && old >= 0) {  // item k-2 stored its stage-2 codes into every peer's gather slot
-          int yo, to;
-          D.decode(old, yo, to);
-          publish_reduce(a, yo, to, D.ep);
-        }
-        id = __shfl_sync(0xffffffffu, nid, 0);
-      }
-      if (lane == 0) {
-        // end sentinel (every consumer warp reads it) in the slot recycled above, then the last
-        // real item's flags once its slot is back
-        sts32(D.meta + 4 * (k & 1), -1);
-        mbar_arrive(own_full + 8 * (k & 1));
-        if (k >= 1) {
-          const int kp = k - 1;
-          mbar_wait(own_empty + 8 * (kp & 1), (uint32_t)(kp >> 1) & 1u);
+          mbar_wait(done0 + 8 * (kk % kRgDone), (uint32_t)(kk / kRgDone) & 1u);
           int y, t;
-          D.decode(lds_id(D.meta + 4 * (kp & 1)), y, t);
+          D.decode(lds_id(hist + 4 * (kk % kRgDone)), y, t);
           publish_reduce(a, y, t, D.ep);
         }
+      };
+      for (;; ++k) {
+        int nid = 0;
+        if (lane == 0 && id < D.items) nid = D.grab();  // the next id is in flight during this item
+        if (id >= D.items) break;
+        int y, t;
+        D.decode(id, y, t);
+        if (lane == 0) sts32(hist + 4 * (k % kRgDone), id);
+        issue(y, t, id);
+        if (k >= 2) publish_k(k - 2);
+        id = __shfl_sync(0xffffffffu, nid, 0);
       }
+      if (lane == 0) {  // end sentinel in the slot of the next item's first piece
+        const uint32_t sl = slot_acquire();
+        sts32(meta + 4 * sl, -1);
+        mbar_arrive(full0 + 8 * sl);
+      }
+      for (int kk = k >= 2 ? k - 2 : 0; kk < k; ++kk) publish_k(kk);
       __syncwarp();
     }
     return;
@@ -1223,136 +1222,51 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   const int gt = li / kRgLpg;              // tile-local group
   const bool lead = (li & (kRgLpg - 1)) == 0;
   const uint32_t xr1 = rep_xor(a.c1), xr2 = rep_xor(a.c2);
-  const uint32_t qmax1 = (1u << a.c1.bits) - 1u, qmax2 = (1u << a.c2.bits) - 1u;
+  const uint32_t qmax2 = (1u << a.c2.bits) - 1u;
+  const uint32_t lb = sbase + li * (kRgEpl * 2);  // the lane's 128-B region of the output staging
+  uint32_t csl = 0, cph = 0;                      // ring position of the next piece to consume
   auto item = [&](int k, int y, int t) {
     const int j = a.rank_lo + y;
     const int64_t seg0 = (int64_t)j * a.seg + a.sub_off;
     const int64_t e0 = (int64_t)t * kTileElems;
     const int64_t p0 = e0 + li * kRgEpl;  // lane slice start in the round
-    const int os = k & 1;
-    const uint32_t own_base = sbase + os * (kTileElems * 2);
-    const uint32_t lb = own_base + li * (kRgEpl * 2);  // the lane's 128-B region of the own slot
-    const uint32_t ph = k & 1;                          // peer-slot phase
-    // ---- own group: stage-1 QDQ
-    uint32_t own[NW];
-    const uint32_t own_park = lb;  // consumed input region; rewritten by the output later
-    float s1;
-    uint32_t z1;
-    bool bad;
-    mbar_wait(own_full + 8 * os, (k >> 1) & 1);
-    {
-      uint32_t x[NC][4];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const uint4 u = lds128_(lb + 16 * (c ^ m));
-        x[c][0] = u.x;
-        x[c][1] = u.y;
-        x[c][2] = u.z;
-        x[c][3] = u.w;
-      }
-      uint32_t mn, mx;
-      if constexpr (S1::SYM) {
-        mx = x[0][0] & 0x7FFF7FFFu;
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (c | i) mx = h2max<Tin>(mx, x[c][i] & 0x7FFF7FFFu);
-        mn = mx;
-      } else {
-        mn = h2min<Tin>(x[0][0], x[0][1]);
-        mx = h2max<Tin>(x[0][0], x[0][1]);
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (c > 0 || i > 1) {
-              mn = h2min<Tin>(mn, x[c][i]);
-              mx = h2max<Tin>(mx, x[c][i]);
-            }
-      }
-      // the lane's bounds, then one shuffle step with the group partner
-      float hi, lo;
-      {
-        float lh = fmax_nan(h_lo<Tin>(mx), h_hi<Tin>(mx));
-        float ll = S1::SYM ? -lh : fmin_nan(h_lo<Tin>(mn), h_hi<Tin>(mn));
-        lh = fmax_nan(lh, __shfl_xor_sync(0xffffffffu, lh, 1));
-        ll = fmin_nan(ll, __shfl_xor_sync(0xffffffffu, ll, 1));
-        hi = lh;
-        lo = S1::SYM ? -hi : ll;
-      }
-      bad = !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
-      GroupQ g;
-      group_params<S1>(a.c1, lo, hi, g);
-      if (bad) g.z = S1::SYM ? g.z : 0u;
-      if (g.normal) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) chunk_codes_packed<S1, Tin>(x[c], g, qmax1, own + c * CWPC);
-      } else {
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-          chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax1, own + c * CWPC);
-      }
-      unswizzle_chunks<NC, CWPC>(own, m);
-      // park the own codes in the lane's (still unused) output staging slot until their rank
-      // position comes up in the sum: 8-16 registers fewer across the source loop
-#pragma unroll
-      for (int v = 0; v < NW / 4; ++v)
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(own_park + 16 * v), "r"(own[4 * v]),
-                     "r"(own[4 * v + 1]), "r"(own[4 * v + 2]), "r"(own[4 * v + 3])
-                     : "memory");
-      s1 = g.s;
-      z1 = g.z;
-    }
-    // ---- fp32 sum in ascending source rank, the own group at its rank position
+    // ---- fp32 sum of the N stage-1 pieces in ascending source rank
     uint64_t acc[4 * NC];
 #pragma unroll
     for (int e = 0; e < 4 * NC; ++e) acc[e] = 0ull;
-    uint32_t pbar = peer_full - 8, src = peer0;
-    for (int s = 0; s < a.world; ++s) {
-      if (s == j) {  // uniform
-        uint32_t ow[NW];
+    for (int s = 0; s < NP; ++s) {
+      mbar_wait(full0 + 8 * csl, cph);
+      const uint32_t src = ring0 + csl * PB;
+      uint32_t cw[NW];
 #pragma unroll
-        for (int v = 0; v < NW / 4; ++v) {
-          const uint4 u = lds128_(own_park + 16 * v);
-          ow[4 * v] = u.x;
-          ow[4 * v + 1] = u.y;
-          ow[4 * v + 2] = u.z;
-          ow[4 * v + 3] = u.w;
-        }
-        decode_words<SB, NW>(ow, s1, 8388608.0f + (float)z1, acc);
-      } else {
-        pbar += 8;
-        mbar_wait(pbar, ph);
-        uint32_t cw[NW];
-#pragma unroll
-        for (int v = 0; v < NW / 4; ++v) {
-          const uint4 u = lds128_(src + li * (kRgEpl * SB / 8) + 16 * v);
-          cw[4 * v] = u.x;
-          cw[4 * v + 1] = u.y;
-          cw[4 * v + 2] = u.z;
-          cw[4 * v + 3] = u.w;
-        }
-        unsigned short sh;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(src + PC + 2 * gt));
-        float zf;
-        if constexpr (S1::SYM) {
-          zf = (float)(1 << (a.c1.bits - 1));
-#pragma unroll
-          for (int q = 0; q < NW; ++q) cw[q] ^= xr1;
-        } else {
-          uint32_t zz;
-          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(src + PC + SCB + gt));
-          zf = (float)zz;
-        }
-        decode_words<SB, NW>(cw, __half2float(__ushort_as_half(sh)), 8388608.0f + zf, acc);
-        src += PC + PM;
+      for (int v = 0; v < NW / 4; ++v) {
+        const uint4 u = lds128_(src + li * (kRgEpl * SB / 8) + 16 * v);
+        cw[4 * v] = u.x;
+        cw[4 * v + 1] = u.y;
+        cw[4 * v + 2] = u.z;
+        cw[4 * v + 3] = u.w;
       }
+      unsigned short sh;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(src + PC + 2 * gt));
+      float zf;
+      if constexpr (S1::SYM) {
+        zf = (float)(1 << (a.c1.bits - 1));
+#pragma unroll
+        for (int w = 0; w < NW; ++w) cw[w] ^= xr1;
+      } else {
+        uint32_t zz;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(src + PC + SCB + gt));
+        zf = (float)zz;
+      }
+      // the slot's shared loads are consumed once their values are in registers
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * csl);
+      if (++csl == (uint32_t)R) {
+        csl = 0;
+        cph ^= 1u;
+      }
+      decode_words<SB, NW>(cw, __half2float(__ushort_as_half(sh)), 8388608.0f + zf, acc);
     }
-    // every shared load of the peer slot has been consumed: hand it back to the producer now,
-    // so the next tile's pieces land during the stage-2 quantize, the stores and the output
-    __syncwarp();
-    if (lane == 0) mbar_arrive(peer_empty);
     // ---- stage-2 quantize of the sum
     float lo2, hi2;
     {
@@ -1372,11 +1286,10 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
       hi2 = b0;
       lo2 = S2::SYM ? -b0 : a0;
     }
-    const bool bad2 = !(fabsf(lo2) <= 3.402823466e38f && fabsf(hi2) <= 3.402823466e38f);
-    bad |= bad2;
+    const bool bad = !(fabsf(lo2) <= 3.402823466e38f && fabsf(hi2) <= 3.402823466e38f);
     GroupQ g2;
     group_params<S2>(a.c2, lo2, hi2, g2);
-    if (bad2) g2.z = S2::SYM ? g2.z : 0u;
+    if (bad) g2.z = S2::SYM ? g2.z : 0u;
     uint32_t w2[NW];
     if (g2.normal) {
       const uint64_t R2 = f2_splat(g2.r), NS2 = f2_splat(-g2.s), C2 = f2_splat(12582912.0f);
@@ -1411,11 +1324,11 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
 #pragma unroll
         for (int e = 0; e < EPW; ++e) {
           const float xv = acc_get<SB>(acc, EPW * i + e);
-          const float t = xv * r;
-          const float q1 = fmaf(fmaf(-t, g2.s, xv), r, t);
+          const float tq = xv * r;
+          const float q1 = fmaf(fmaf(-tq, g2.s, xv), r, tq);
           const float qc = fminf(fmaxf(q1, lob), hib);
-          const float y = S2::CEIL ? __fadd_ru(qc, 12582912.0f) : __fadd_rn(qc, 12582912.0f);
-          wv |= (uint32_t)(__float_as_int(y) + zb) << (SB * e);
+          const float yv = S2::CEIL ? __fadd_ru(qc, 12582912.0f) : __fadd_rn(qc, 12582912.0f);
+          wv |= (uint32_t)(__float_as_int(yv) + zb) << (SB * e);
         }
         w2[i] = wv;
       }
@@ -1441,11 +1354,13 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         }
       }
     }
+    if constexpr (FUSED) {  // this item's gather-slot stores are issued (the producer publishes gflag)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(done0 + 8 * (k % kRgDone));
+    }
     // ---- own output: the owner decodes its own payload (collectives.py:378), staged
     // through the warp's own 4-KB buffer (swizzled), then one coalesced copy
     {
-      const uint32_t ob0 = own_base + warp * (32 * kRgEpl * 2);
-      const uint32_t lo_b = lb;
 #pragma unroll
       for (int e = 0; e < 4 * NC; ++e) acc[e] = 0ull;
       decode_words<SB, NW>(w2, g2.s, 8388608.0f + (float)g2.z, acc);  // 0 + (c - z) s: exact, never -0
@@ -1453,25 +1368,23 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
       for (int c = 0; c < NC; ++c) {
         uint32_t h[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          h[q] = pack2(acc_get<SB>(acc, 8 * c + 2 * q), acc_get<SB>(acc, 8 * c + 2 * q + 1), (Tout*)nullptr);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(lo_b + 16 * (c ^ m)), "r"(h[0]), "r"(h[1]),
+        for (int qq = 0; qq < 4; ++qq)
+          h[qq] = pack2(acc_get<SB>(acc, 8 * c + 2 * qq), acc_get<SB>(acc, 8 * c + 2 * qq + 1), (Tout*)nullptr);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(lb + 16 * (c ^ m)), "r"(h[0]), "r"(h[1]),
                      "r"(h[2]), "r"(h[3])
                      : "memory");
       }
       __syncwarp();
-      fence_proxy_async_smem();  // the staging st.shared before the slot's next bulk fill
-      const uint32_t wbase = ob0;
+      const uint32_t wbase = sbase + warp * (32 * kRgEpl * 2);
       uint8_t* ob = reinterpret_cast<uint8_t*>(reinterpret_cast<Tout*>(a.out[j]) + seg0 + e0 + warp * (32 * kRgEpl));
-      // byte 512 v + 16 lane of the warp's output = chunk q = lane % 8 of slice l = 4 v + lane / 8,
-      // stored at l * 128 + 16 (q ^ (l & 7)) (conflict-free for each 8-lane phase)
+      // byte 512 v + 16 lane of the warp's output = chunk qq = lane % 8 of slice l = 4 v + lane / 8,
+      // stored at l * 128 + 16 (qq ^ (l & 7)) (conflict-free for each 8-lane phase)
 #pragma unroll
       for (int v = 0; v < NC; ++v) {
-        const int l = 4 * v + (lane >> 3), q = lane & 7;
-        st_v4(ob + 512 * v + 16 * lane, lds128_(wbase + l * (kRgEpl * 2) + 16 * (q ^ (l & 7))));
+        const int l = 4 * v + (lane >> 3), qq = lane & 7;
+        st_v4(ob + 512 * v + 16 * lane, lds128_(wbase + l * (kRgEpl * 2) + 16 * (qq ^ (l & 7))));
       }
-      __syncwarp();  // the copy's loads are complete: the own slot can be refilled
-      if (lane == 0) mbar_arrive(own_empty + 8 * os);
+      __syncwarp();  // the staging buffer's loads are complete before the next item rewrites it
     }
     if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
   };
@@ -1481,8 +1394,8 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   } else {
     const DynIter& D = it0;
     for (int k = 0;; ++k) {
-      mbar_wait(own_full + 8 * (k & 1), (k >> 1) & 1);
-      const int id = lds_id(D.meta + 4 * (k & 1));
+      mbar_wait(full0 + 8 * csl, cph);
+      const int id = lds_id(meta + 4 * csl);
       if (id < 0) break;
       int y, t;
       D.decode(id, y, t);
@@ -1900,7 +1813,7 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
 template <typename Tin, class S1>
 __global__ void __launch_bounds__(kStreamThreads) k_qstream(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
+  const int njobs = a.mode == 1 ? 1 : q_jobs(a);
   q_role<Tin, S1, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
@@ -1908,7 +1821,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_qstream(FlashArgs a) {
 template <typename Tin, class S1>
 __global__ void __launch_bounds__(kGplThreads, 3) k_qstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
+  const int njobs = a.mode == 1 ? 1 : q_jobs(a);
   q_role_gpl<Tin, S1, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
@@ -1916,7 +1829,7 @@ __global__ void __launch_bounds__(kGplThreads, 3) k_qstream_gpl(FlashArgs a) {
 template <typename Tin, class S1, int G>
 __global__ void __launch_bounds__(kGplThreads, 4) k_qstream_gq(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
+  const int njobs = a.mode == 1 ? 1 : q_jobs(a);
   q_role_gq<Tin, S1, G, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
@@ -1927,9 +1840,9 @@ __global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
                                    RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
-// g = 128 reduce, two lanes per group (r_role_gpl); one storage width, whole tiles only
+// g = 128 reduce, two lanes per group (r_role_gpl, a.stages piece slots); one storage width, whole tiles only
 template <typename Tin, typename Tout, class S1, class S2>
-__global__ void __launch_bounds__(kGplThreads, 3) k_rstream_gpl(FlashArgs a) {
+__global__ void __launch_bounds__(kGplThreads, 4) k_rstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   if constexpr (sizeof(Tout) == 2 && S1::SB == S2::SB)
     r_role_gpl<Tin, Tout, S1, S2, false>(a, smem_u32(smem), a.stages,
@@ -1949,18 +1862,20 @@ __global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
 // and one barrier region behind it, so a role's barriers never overlay
 // another role's data
 struct FusedSmem {
-  int q_stages, d_stages, data_bytes, bars_off, max_bars, meta_off, total;
+  int q_stages, d_stages, r_ring, data_bytes, bars_off, max_bars, meta_off, total;
 };
-__host__ __device__ inline FusedSmem fused_smem(const DevCodec& c1, const DevCodec& c2, int world, int qs, int ds) {
+__host__ __device__ inline FusedSmem fused_smem(const DevCodec& c1, const DevCodec& c2, int qs, int ds, int rr) {
   FusedSmem f;
   f.q_stages = qs;
   f.d_stages = ds;
+  f.r_ring = rr;
   const int q = qs * kTileElems * 2;
-  const int r = 2 * kTileElems * 2 + (int)rg_peer_bytes(c1, world);
+  const int r = (int)rg_bars_off(c1, rr);
   const int d = ds * (int)dstage_bytes(c2);
   f.data_bytes = q > r ? (q > d ? q : d) : (r > d ? r : d);
   f.bars_off = (f.data_bytes + 127) & ~127;
-  const int nq = 2 * qs, nr = 4 + world, nd = 2 * ds;
+  // the reduce role keeps its item-id ring (one int per piece slot) behind its barriers
+  const int nq = 2 * qs, nr = 2 * rr + kRgDone + (rr + kRgDone + 1) / 2, nd = 2 * ds;
   f.max_bars = nq > nr ? (nq > nd ? nq : nd) : (nr > nd ? nr : nd);
   f.meta_off = f.bars_off + 8 * f.max_bars;  // DynIter id ring: one int per stage (<= 16)
   f.total = f.meta_off + 64;
@@ -1981,7 +1896,7 @@ __device__ __forceinline__ void fused_role_switch(uint32_t bars, int nb) {
 // the paper's fused kernel. Every CTA runs the three roles
 // of the group-lane codec — scatter (q_role_gpl: stage-1 quantize, codes
 // stored straight into the owners' receive slots, peer memory over NVLink),
-// reduce (r_role_gpl: N-1 received pieces + own QDQ -> fp32 rank-ordered sum ->
+// reduce (r_role_gpl: the N stage-1 pieces, own one included -> fp32 rank-ordered sum ->
 // stage-2 quantize -> every peer's gather slot) and gather (d_role: decode the
 // owners' stage-2 pieces) — synchronised only by per-tile epoch flags (rflag /
 // gflag: published by a role's producer warp once the tile's stores are
@@ -2004,7 +1919,8 @@ __global__ void __launch_bounds__(kGplThreads, 3) k_fstream(const __grid_constan
     const uint32_t bars = sb + (uint32_t)a.fp_bars;
     const int G = (int)gridDim.x, cta = (int)blockIdx.x;
     const int nr = a.rank_hi - a.rank_lo;
-    const int P = nr * (a.world - 1);
+    const int P = nr * (a.world - 1);   // gather jobs (peers' pieces)
+    const int PQ = nr * (a.world - 1 + a.ownq);  // scatter jobs (ownq: the own piece too)
     const int B = a.fp_chunk;
     const int nch = (a.tiles + B - 1) / B;
     uint32_t* ctr = fctr(a, a.rank_lo);
@@ -2020,14 +1936,14 @@ __global__ void __launch_bounds__(kGplThreads, 3) k_fstream(const __grid_constan
         if (c < 0 || c >= nch) continue;
         if (role == 2 && cta >= a.fp_dctas) continue;  // measurement option: fewer gather CTAs
         const int t0 = c * B, bt = min(B, a.tiles - t0);
-        const int per = role == 1 ? nr : P;
+        const int per = role == 0 ? PQ : role == 1 ? nr : P;
         fused_role_switch(bars, nb);
         const uint64_t r0 = tp ? globaltimer() : 0;
         const DynIter it{ctr + role * kFusedMaxChunks + c, per * bt, per, t0, sb + (uint32_t)a.fp_meta, ep};
         if (role == 0) q_role_gpl<Tin, S1, true>(a, sb, a.q_stages_f, it, bars);
-        else if (role == 1) r_role_gpl<Tin, Tout, S1, S2, true>(a, sb, 1, it, bars);
+        else if (role == 1) r_role_gpl<Tin, Tout, S1, S2, true>(a, sb, a.r_ring_f, it, bars);
         else d_role<Tout, S2, true, DynIter, kGplWarps>(a, sb, a.d_stages_f, it, bars);
-        nb = role == 0 ? 2 * a.q_stages_f : role == 1 ? 4 + a.world : 2 * a.d_stages_f;
+        nb = role == 0 ? 2 * a.q_stages_f : role == 1 ? 2 * a.r_ring_f + kRgDone : 2 * a.d_stages_f;
         if (tp) {
           __syncthreads();
           if (threadIdx.x == 0) {
