@@ -74,10 +74,16 @@ struct GenSpec {
   static constexpr int SB = 0;
   static constexpr bool SYM = false, CEIL = false;
 };
+#ifndef FC_STAGED
+#define FC_STAGED 0  // make STAGED=1: also compile the cp.async-staged kernels for the compile-time presets (A/B)
+#endif
 template <int SB_, bool SYM_, bool CEIL_>
 struct IntSpec {
   static constexpr bool kFast = true;
-  static constexpr bool kLegacy = !SYM_ && !CEIL_;  // staged kernels only for the asym-nearest presets
+  // the staged kernels of the compile-time presets are an A/B build option (FC_STAGED); the
+  // streaming, fused and small-message kernels are the product path, the runtime-codec
+  // (GenSpec) staged kernels serve every other scheme
+  static constexpr bool kLegacy = FC_STAGED && !SYM_ && !CEIL_;
   static constexpr int SB = SB_;  // storage bits: 4 (bits 2..4) or 8 (bits 5..8)
   static constexpr bool SYM = SYM_;
   static constexpr bool CEIL = CEIL_;

@@ -1,7 +1,8 @@
 """One process per rank over CUDA IPC (the torchrun path), exercised on a
 single GPU: 2-8 processes share cuda:0, map each other's blocks with
 cudaIpcOpenMemHandle and run the fused flag-synchronised kernel (OPT_FUSED 1)
-or the phase-split kernels with IPC barriers (OPT_FUSED 0). Parity vs the
+or the phase-split kernels with IPC barriers (OPT_FUSED 0, OPT_ONESHOT 0), or the
+one-launch small-message kernel (default at decode sizes, k_small). Parity vs the
 oracle, plus the fault path: a rank that never arrives -> ProtocolError
 naming the stuck peer (fabric.py:158-178)."""
 
@@ -47,8 +48,11 @@ def _worker(rank, world, port, q, mode):
             comm.set_option(_lib.OPT_FUSED, 1)
         if mode == "split":
             comm.set_option(_lib.OPT_FUSED, 0)
+            comm.set_option(_lib.OPT_ONESHOT, 0)
         if mode == "generic":
             comm.set_option(_lib.OPT_FAST, 0)
+        # 3 tiles per segment: the default ("small") takes the one-launch small-message kernel
+        # (k_small); "split" / "fused" force the streaming kernels at the same size
         m = 8192 * world * 3 + (0 if mode != "generic" else 100)
         xs = orc.gen_rank_activations(8192, -(-m // 8192), 21, world)
         xs = [orc.round_to_bf16(x.ravel()[:m]) for x in xs]
@@ -101,7 +105,7 @@ def _run(world, mode):
 
 
 @pytest.mark.parametrize("world,mode", [(2, "fused"), (4, "fused"), (8, "fused"), (2, "split"), (4, "split"),
-                                        (8, "split"), (3, "generic")])
+                                        (8, "split"), (2, "small"), (4, "small"), (8, "small"), (3, "generic")])
 def test_ipc_parity(world, mode):
     _run(world, mode)
 

@@ -13,13 +13,13 @@ dev = torch.device("cuda", 0)
 stream = torch.cuda.current_stream(dev)
 cfg = fc.FlashConfig.from_bits(4)
 for tp in (8,):
-    for bs in (1, 8, 64):
+    for bs in (1, 8, 16, 32, 64):
         m = bs * 8192
         comm = FlashComm.local([0] * tp, slot_bytes_for(-(-m // tp), cfg.stage1_codec, cfg.stage2_codec))
         ins = [torch.randn(m, device=dev).to(torch.bfloat16) for _ in range(tp)]
         outs = [torch.empty_like(t) for t in ins]
         res = {}
-        for name, opts in (("oneshot", {_lib.OPT_ONESHOT: 1}), ("split", {_lib.OPT_ONESHOT: 0}),
+        for name, opts in (("small", {_lib.OPT_ONESHOT: 1}), ("split", {_lib.OPT_ONESHOT: 0}),
                            ("fused", {_lib.OPT_FUSED: 1})):
             comm.set_option(_lib.OPT_ONESHOT, 1)
             comm.set_option(_lib.OPT_FUSED, -1)
@@ -27,6 +27,14 @@ for tp in (8,):
                 comm.set_option(k, v)
             res[name] = graph_time(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), 20, stream) * 1e3
             comm.check()
+            if name == "small":  # eager: host call + launch, CUDA events around 20 calls
+                import time
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                for _ in range(20):
+                    comm.all_reduce_local(ins, cfg, outs=outs, check=False)
+                torch.cuda.synchronize()
+                res["small_eager_wall"] = (time.perf_counter() - t0) / 20 * 1e6
         comm.set_option(_lib.OPT_ONESHOT, 0)
         comm.set_option(_lib.OPT_FUSED, -1)
         for ph, name in ((1, "scatter"), (2, "reduce"), (4, "gather")):

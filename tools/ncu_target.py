@@ -13,8 +13,10 @@ from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "fused"
 tp, M = 8, 8 * 1024 * 8192
+if mode.startswith("c4"):  # decode regime: bs x 8192 per rank (c4 -> bs 8, c4_64 -> bs 64)
+    M = (int(mode[3:]) if len(mode) > 2 else 8) * 8192
 cfg = fc.FlashConfig.from_bits(4)
-if mode in ("fused", "split"):
+if mode in ("fused", "split") or mode.startswith("c4"):
     comm = FlashComm.local([0] * tp, slot_bytes_for(M // tp, cfg.stage1_codec, cfg.stage2_codec))
     comm.set_option(_lib.OPT_FUSED, int(mode == "fused"))
     ins = [torch.randn(M, device="cuda").to(torch.bfloat16) for _ in range(tp)]
