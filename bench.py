@@ -594,8 +594,9 @@ def bench_local(args, cfg, peaks):
     x = ins[0]
     xo = torch.empty(m, device=dev, dtype=dt)
     sdt = {torch.bfloat16: _lib.DTYPE_BF16, torch.float16: _lib.DTYPE_F16}[dt]
-    for bits, grp in [(b, g_) for b in (4, 8) for g_ in (32, 64, 128, 256)]:
-        cc = fc.CodecConfig(bits=bits, group_size=grp)
+    for bits, grp in [(b, g_) for b in (4, 8) for g_ in (32, 64, 128, 256)] + [("e4m3", 128), ("e2m1", 128)]:
+        cc = fc.CodecConfig(bits=bits, group_size=grp) if isinstance(bits, int) else \
+            fc.CodecConfig(number_format=bits, group_size=grp)
         L = cc.device_layout(m)
         qbuf = torch.empty(int(L.total_bytes), dtype=torch.uint8, device=dev)
         cfc = cc.to_fc()
@@ -605,11 +606,39 @@ def bench_local(args, cfg, peaks):
             qbuf.data_ptr(), m, C.byref(cfc), xo.data_ptr(), sdt, torch.cuda.current_stream().cuda_stream))
         qms, dms = graph_time(qf, 10, stream), graph_time(df, 10, stream)
         ab = e * m + int(L.wire_bytes)
-        codec[f"int{bits}_g{grp}"] = {
+        codec[(f"int{bits}" if isinstance(bits, int) else bits) + f"_g{grp}"] = {
             "quantize_us": qms * 1e3, "quantize_gbs": ab / (qms * 1e-3) / 1e9,
             "dequantize_us": dms * 1e3, "dequantize_gbs": ab / (dms * 1e-3) / 1e9,
             "frac_quantize": ab / (qms * 1e-3) / 1e9 / peaks["hbm_gbs"],
             "frac_dequantize": ab / (dms * 1e-3) / 1e9 / peaks["hbm_gbs"], "alg_bytes": ab}
+    # ---- lane-8 path (fc_l8.cuh) on the C2 workload: e4m3 stage codecs (cvt.rn.satfinite) and
+    # INT4 g128 with the Hadamard rotation (block 128, seeded signs) fused into the prologue /
+    # epilogue; 8 logical ranks on this GPU, three launches per step
+    lane8 = {}
+    for name, lcfg in (("e4m3_g128", fc.FlashConfig.uniform(fc.CodecConfig(number_format="e4m3"))),
+                       ("int4_g128_rot128", fc.FlashConfig(fc.CodecConfig(bits=4), fc.CodecConfig(bits=4),
+                                                           rotation=fc.HadamardBlock(128, sign_seed=1)))):
+        lcomm = FlashComm.local([0] * tp, slot_bytes_for(seg, lcfg.stage1_codec, lcfg.stage2_codec))
+        louts = [torch.empty(m, device=dev, dtype=dt) for _ in range(tp)]
+        signs = None
+        if lcfg.rotation is not None:
+            signs = [lcfg.rotation._device_signs(dev) for _ in range(tp)]
+            lcomm.set_rotation(lcfg.rotation, signs)
+        lstep = lambda: lcomm.all_reduce_local(ins, lcfg, outs=louts, check=False)  # noqa: E731
+        for _ in range(3):
+            lstep()
+        lcomm.check()
+        lms, _ = _events_time(lstep, max(5, args.steps // 2), stream)
+        lcomm.check()
+        b1l = lcfg.stage1_codec.device_layout(seg).wire_bytes / seg
+        lb = tp * (2 * e * m + 2 * (tp - 1) * seg * 2 * b1l)
+        lane8[name] = {"ms_per_step": lms, "value_gbs": tp * e * m / (lms * 1e-3) / 1e9,
+                       "hbm_alg_bytes": lb, "frac": lb / (lms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                       "launches_per_step": lcomm.get_option(_lib.OPT_LAST_LAUNCHES),
+                       "kernels": "k_l8_scatter | k_l8_reduce | k_l8_gather"}
+        lcomm.set_rotation(None)
+        lcomm.close()
+        del louts, signs
     del ins, xo
     torch.cuda.empty_cache()
 
@@ -654,6 +683,7 @@ def bench_local(args, cfg, peaks):
         "latency_us": ms * 1e3, "latency_us_median": statistics.median(per) * 1e3,
         "algbw_gbs": e * m / (ms * 1e-3) / 1e9,
         "roofline": roofline, "phases": phases, "fused_one_gpu": fused, "codec_c5": codec, "decode_c4": decode,
+        "lane8": lane8,
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(args.steps * launches_per_step),
         "clocks": clk, "nccl_bf16": None,
     }

@@ -194,6 +194,19 @@ FC_API fc_status fc_flash_all_reduce_host_rank(fc_comm* comm, const void* host_i
 FC_API fc_status fc_flash_all_reduce(fc_comm* comm, const void* in, void* out, int64_t n, int32_t in_dtype,
                               int32_t out_dtype, const fc_flash_cfg* cfg, void* stream);
 
+/* ---- fused rotation (FlashConfig.rotation, collectives.py:350-351 / 390-391) ----
+ * Sets the blocked Hadamard rotation (rotation.py:38-83) the next flash runs of
+ * `comm` fuse into the scatter / reduce prologue (H(D x)) and the reduce /
+ * gather epilogue (D(H y)): dim (power of two, 8..256; 0 clears), normalize,
+ * signs = `dim` device floats of +-1 on the rank's device or NULL; rank -1 sets
+ * every rank of a local communicator. fc_flash_rotation_fusable tells whether
+ * a run of n elements per rank with `cfg` can fuse a rotation of `dim` (the
+ * round and segment sizes must be multiples of dim, group sizes 8..256); runs
+ * that cannot fail with FC_ERR_CONFIG while a rotation is set. */
+FC_API fc_status fc_comm_set_rotation(fc_comm* comm, int32_t rank, int32_t dim, int32_t normalize,
+                                      const float* signs);
+FC_API int32_t fc_flash_rotation_fusable(fc_comm* comm, int64_t n, const fc_flash_cfg* cfg, int32_t dim);
+
 /* Synchronize rank's device work and map its error word: a timed-out wait
  * -> FC_ERR_PROTOCOL "deadlock: rank r timed out waiting on rank p"
  * (fabric.py:171-175); non-finite input -> FC_ERR_DOMAIN (codec.py:230). */

@@ -85,6 +85,8 @@ _SIGS = {
     "fc_comm_topology": (C.c_int, [_P, C.POINTER(_I32), C.POINTER(_I32)]),
     "fc_comm_role_profile": (C.c_int, [_P, _I32, C.POINTER(C.c_uint64), _I32, C.POINTER(_I32)]),
     "fc_hadamard": (C.c_int, [_P, _I32, _I64, _I64, _I32, _I32, _P, _I32, _P, _I32, _I64, _P]),
+    "fc_comm_set_rotation": (C.c_int, [_P, _I32, _I32, _I32, _P]),
+    "fc_flash_rotation_fusable": (_I32, [_P, _I64, C.POINTER(fc_flash_cfg), _I32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -32,8 +32,9 @@ METHODS = ("exact", "ring", "flash")
 class FlashConfig:
     """Stage codecs and blocking of the two-step quantized all-reduce
     (collectives.py:37-109). `chunk_size` is validated like the reference but
-    never changes results (collectives.py:14-16). `rotation` (Hadamard,
-    rotation.py) is not on the B200 path yet and must be None."""
+    never changes results (collectives.py:14-16). `rotation` (rotation.HadamardBlock,
+    rotation.py) is fused into the lane-8 kernels when its block (<= 256) tiles the
+    rank segments, else applied as separate passes around the all-reduce."""
 
     stage1_codec: CodecConfig
     stage2_codec: CodecConfig
@@ -178,8 +179,20 @@ def flash_all_reduce(tensors: Sequence, cfg: FlashConfig, topology: Optional[Fab
     if comm is None:
         comm = local_comm(devices, slot_bytes_for(seg, cfg.stage1_codec, cfg.stage2_codec))
     comm.set_timeout(timeout if timeout is not None else 3600.0)
-    if cfg.rotation is not None:
-        # rotate the zero-padded rank tensors (float32), all-reduce, rotate back, trim
+    if cfg.rotation is not None and comm.rotation_fusable(m, cfg, cfg.rotation):
+        # the rotation fused into the lane-8 kernels: H(D x) in the scatter / reduce prologue,
+        # D(H y) in the reduce / gather epilogue (fc_l8.cuh), no float32 copies of the tensors
+        rot = cfg.rotation
+        signs = [rot._device_signs(f.device) for f in flats]  # alive until the call has synchronised
+        comm.set_rotation(rot, signs)
+        try:
+            outs = comm.all_reduce_local(flats, cfg, out_dtype=odt, check=True)
+        finally:
+            comm.set_rotation(None)
+    elif cfg.rotation is not None:
+        # not fusable here (rotation block > 256, segment not a multiple of it, or a group size
+        # the lane-8 kernels do not take): rotate the zero-padded rank tensors (float32),
+        # all-reduce, rotate back, trim -- three passes
         from .rotation import hadamard_apply, hadamard_inverse
 
         rot = cfg.rotation

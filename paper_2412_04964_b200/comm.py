@@ -235,6 +235,26 @@ class FlashComm:
     def set_timeout(self, seconds: float) -> None:
         self.set_option(_lib.OPT_TIMEOUT_MS, max(1, int(round(seconds * 1000))))
 
+    # ---------------------------------------------------------------- fused rotation
+    def rotation_fusable(self, n: int, cfg, block) -> bool:
+        """Whether a run of n elements per rank can fuse `block` (rotation.HadamardBlock)
+        into its prologue / epilogue (fc_flash_rotation_fusable)."""
+        cs = self._cfg(cfg)
+        return bool(_lib.lib().fc_flash_rotation_fusable(self._h, int(n), C.byref(cs), int(block.dimension)))
+
+    def set_rotation(self, block, signs: Optional[Sequence[Optional[torch.Tensor]]] = None) -> None:
+        """Fuse `block` into the next runs (None clears). signs: per-rank device tensors of the
+        seeded +-1 diagonal on the ranks' devices (block.signs()), or None."""
+        L = _lib.lib()
+        if block is None:
+            _lib.check(L.fc_comm_set_rotation(self._h, -1, 0, 1, None))
+            return
+        for r in range(self.world_size):
+            if self.rank is not None and r != self.rank:
+                continue
+            sp = signs[r].data_ptr() if signs is not None and signs[r] is not None else None
+            _lib.check(L.fc_comm_set_rotation(self._h, r, int(block.dimension), int(bool(block.normalize)), sp))
+
     # ---------------------------------------------------------------- calls
     @staticmethod
     def _cfg(cfg) -> _lib.fc_flash_cfg:

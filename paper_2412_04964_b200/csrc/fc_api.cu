@@ -425,6 +425,8 @@ fc_status fc_flash_all_reduce_local(fc_comm* c, const void* const* ins, void* co
   cudaStream_t st[kMaxRanks];
   for (int r = 0; r < c->world; ++r) st[r] = streams ? (cudaStream_t)streams[r] : (cudaStream_t)0;
   if (c->world == 1) return FC_DISPATCH2(in_dtype, out_dtype, identity_typed, ins[0], outs[0], n, c->devices[0], st[0]);
+  if (l8_wanted(c, cfg, n)) return run_l8(in_dtype, out_dtype, c, ins, outs, n, cfg, st, -1);
+  if (c->rot_dim) return fail(FC_ERR_CONFIG, "rotation cannot be fused at this size / codec");
   return FC_DISPATCH_RUN(in_dtype, out_dtype, c, ins, outs, n, cfg, st, -1);
 }
 
@@ -443,7 +445,29 @@ fc_status fc_flash_all_reduce(fc_comm* c, const void* in, void* out, int64_t n, 
   ins[r] = in;
   outs[r] = out;
   st[r] = (cudaStream_t)stream;
+  if (l8_wanted(c, cfg, n)) return run_l8(in_dtype, out_dtype, c, ins, outs, n, cfg, st, r);
+  if (c->rot_dim) return fail(FC_ERR_CONFIG, "rotation cannot be fused at this size / codec");
   return FC_DISPATCH_RUN(in_dtype, out_dtype, c, ins, outs, n, cfg, st, r);
+}
+
+fc_status fc_comm_set_rotation(fc_comm* c, int32_t rank, int32_t dim, int32_t normalize, const float* signs) {
+  if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
+  if (dim < 0 || (dim & (dim - 1)) != 0) return fail(FC_ERR_CONFIG, "rotation dimension must be a power of two");
+  if (rank < -1 || rank >= c->world) return fail(FC_ERR_CONFIG, "rank %d outside world %d", rank, c->world);
+  c->rot_dim = dim;
+  c->rot_normalize = normalize ? 1 : 0;
+  for (int r = 0; r < c->world; ++r)
+    if (rank < 0 || r == rank) c->rot_signs[r] = dim ? signs : nullptr;
+  return FC_OK;
+}
+
+int32_t fc_flash_rotation_fusable(fc_comm* c, int64_t n, const fc_flash_cfg* cfg, int32_t dim) {
+  if (!c || !cfg || dim <= 0) return 0;
+  const int32_t keep = c->rot_dim;
+  c->rot_dim = dim;
+  const bool ok = l8_wanted(c, cfg, n);
+  c->rot_dim = keep;
+  return ok ? 1 : 0;
 }
 
 fc_status fc_comm_check(fc_comm* c, int32_t rank) {
@@ -596,7 +620,8 @@ fc_status host_pipeline(fc_comm* c, const void* const* hin, void* const* hout, i
       c->span_lo = lo;
       c->span_hi = hi;
       if (only_rank >= 0) FC_CUDA_TRY(cudaSetDevice(c->devices[only_rank]));
-      status = FC_DISPATCH_RUN(in_dt, out_dt, c, din, dout, n, cfg, st, only_rank);
+      status = l8_wanted(c, cfg, n) ? run_l8(in_dt, out_dt, c, din, dout, n, cfg, st, only_rank)
+                                    : FC_DISPATCH_RUN(in_dt, out_dt, c, din, dout, n, cfg, st, only_rank);
       c->span_lo = 0;
       c->span_hi = -1;
     }

@@ -306,10 +306,17 @@ static void quant_generic(const T* x, int64_t n, const DevCodec& dc, uint8_t* ds
   k_gen_codes<<<(unsigned)((units + 255) / 256), 256, 0, st>>>(src, n, dc, dst, err, 0u);
 }
 
+// group-scaled minifloat codecs: the lane-8 kernels (fc_l8.cuh, cvt.rn.satfinite), g = 8..256
+static bool l8_codec_ok(const fc_codec& c) {
+  return c.kind == FC_KIND_MINIFLOAT && c.group_size >= 8 && c.group_size <= 256 &&
+         (c.group_size & (c.group_size - 1)) == 0;
+}
+
 fc_status launch_quantize(const void* x, int in_dtype, int64_t n, const fc_codec& c, void* dst, uint32_t* err,
                           cudaStream_t st, bool allow_fast) {
   const fc_layout L = layout_of(c, n);
   const DevCodec dc = dev_codec(c, L);
+  if (allow_fast && l8_codec_ok(c)) return l8_codec_quantize(x, in_dtype, n, dc, dst, err, st);
   const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)dst % 16 == 0);
   if (allow_fast && fast_group(c) && aligned) {
     const int64_t tiles = (n + kTileElems - 1) / kTileElems;
@@ -368,6 +375,7 @@ fc_status launch_dequantize(const void* src, int64_t n, const fc_codec& c, void*
                             cudaStream_t st, bool allow_fast) {
   const fc_layout L = layout_of(c, n);
   const DevCodec dc = dev_codec(c, L);
+  if (allow_fast && l8_codec_ok(c)) return l8_codec_dequantize(src, n, dc, out, out_dtype, st);
   const uint8_t* s = (const uint8_t*)src;
   const bool aligned = ((uintptr_t)src % 16 == 0) && ((uintptr_t)out % 16 == 0);
   if (allow_fast && fast_group(c) && aligned) {

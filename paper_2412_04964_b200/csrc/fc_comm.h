@@ -55,6 +55,10 @@ struct fc_comm {
   int64_t hs_in_bytes[kMaxRanks] = {0}, hs_out_bytes[kMaxRanks] = {0};
   cudaStream_t hs_h2d[kMaxRanks] = {nullptr}, hs_comp[kMaxRanks] = {nullptr}, hs_d2h[kMaxRanks] = {nullptr};
   std::vector<cudaEvent_t> hs_ev;  // [chunk][rank][in, out]
+  // fused Hadamard rotation of the next runs (fc_comm_set_rotation; dim 0: none): block size,
+  // normalize flag, per-rank device pointer to the dim seeded signs (or null)
+  int32_t rot_dim = 0, rot_normalize = 1;
+  const float* rot_signs[kMaxRanks] = {nullptr};
   // last call (debug export)
   fc_codec last_c1{}, last_c2{};
   int64_t last_R = 0, last_sub_len = 0;

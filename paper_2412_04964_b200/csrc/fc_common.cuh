@@ -57,6 +57,7 @@ struct DevCodec {
   int64_t zeros_off;
   // minifloat (FC_KIND_MINIFLOAT): e/m bits, bias, largest finite magnitude
   int mf_exp, mf_mant, mf_bias;
+  int mf_fmt;      // fc_minifloat_format
   double mf_max;
 };
 

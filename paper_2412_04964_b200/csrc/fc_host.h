@@ -128,6 +128,7 @@ inline DevCodec dev_codec(const fc_codec& c, const fc_layout& L) {
     d.mf_exp = f.e;
     d.mf_mant = f.m;
     d.mf_bias = f.bias;
+    d.mf_fmt = c.reserved;
     d.mf_max = f.max_finite;
     d.qdiv = f.max_finite;  // raw scale = absmax / max_finite (codec.py:345)
     d.bits = 1 + f.e + f.m;
@@ -143,6 +144,13 @@ inline int dtype_size(int dt) { return dt == FC_DTYPE_F32 ? 4 : 2; }
 inline bool dtype_ok(int dt) { return dt == FC_DTYPE_F32 || dt == FC_DTYPE_F16 || dt == FC_DTYPE_BF16; }
 
 fc_status validate_codec(const fc_codec* c);
+// lane-8 path (fc_l8_run.cu): minifloat stages / fused Hadamard rotation
+bool l8_wanted(const fc_comm* c, const fc_flash_cfg* cfg, int64_t n);
+fc_status run_l8(int in_dt, int out_dt, fc_comm* c, const void* const* ins, void* const* outs, int64_t n,
+                 const fc_flash_cfg* cfg, cudaStream_t* st, int only_rank);
+fc_status l8_codec_quantize(const void* x, int in_dt, int64_t n, const DevCodec& dc, void* dst, uint32_t* err,
+                            cudaStream_t st);
+fc_status l8_codec_dequantize(const void* src, int64_t n, const DevCodec& dc, void* out, int out_dt, cudaStream_t st);
 
 // kernels (fc_codec.cu)
 fc_status launch_quantize(const void* x, int in_dtype, int64_t n, const fc_codec& c, void* dst,

@@ -56,8 +56,13 @@ def _worker(rank, world, port, q, mode):
         m = 8192 * world * 3 + (0 if mode != "generic" else 100)
         xs = orc.gen_rank_activations(8192, -(-m // 8192), 21, world)
         xs = [orc.round_to_bf16(x.ravel()[:m]) for x in xs]
-        cfg = fc.FlashConfig.from_bits(4)
-        want = orc.flash_all_reduce(xs, orc.Codec(bits=4), orc.Codec(bits=4)).outputs[0]
+        if mode == "minifloat":  # e4m3 stages: the lane-8 kernels with IPC barriers
+            cfg = fc.FlashConfig.uniform(fc.CodecConfig(number_format="e4m3"))
+            oc = orc.Codec(kind="e4m3")
+        else:
+            cfg = fc.FlashConfig.from_bits(4)
+            oc = orc.Codec(bits=4)
+        want = orc.flash_all_reduce(xs, oc, oc).outputs[0]
         for it in range(3):
             x = torch.from_numpy(xs[rank]).cuda().to(torch.bfloat16)
             out = comm.all_reduce(x, cfg, out_dtype=torch.float32, check=True)
@@ -105,7 +110,8 @@ def _run(world, mode):
 
 
 @pytest.mark.parametrize("world,mode", [(2, "fused"), (4, "fused"), (8, "fused"), (2, "split"), (4, "split"),
-                                        (8, "split"), (2, "small"), (4, "small"), (8, "small"), (3, "generic")])
+                                        (8, "split"), (2, "small"), (4, "small"), (8, "small"), (3, "generic"),
+                                        (4, "minifloat")])
 def test_ipc_parity(world, mode):
     _run(world, mode)
 

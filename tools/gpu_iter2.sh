@@ -13,6 +13,8 @@ try:
     for k, v in d["phases"].items(): print(" ", k, v["kernel"], round(v["us"], 1), "us", round(v["frac"], 3))
     print(" fused", d.get("fused_one_gpu"))
     print(" c4", d.get("decode_c4"))
+    print(" lane8", {k: (round(v["ms_per_step"], 4), round(v["frac"], 3)) for k, v in (d.get("lane8") or {}).items()})
+    print(" c5", {k: (round(v["quantize_us"], 1), round(v["frac_quantize"], 3), round(v["dequantize_us"], 1), round(v["frac_dequantize"], 3)) for k, v in d["codec_c5"].items()})
 except Exception as e:
     print("bench parse failed", e)
 PY
