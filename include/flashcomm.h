@@ -211,6 +211,12 @@ FC_API int32_t fc_flash_rotation_fusable(fc_comm* comm, int64_t n, const fc_flas
  * -> FC_ERR_PROTOCOL "deadlock: rank r timed out waiting on rank p"
  * (fabric.py:171-175); non-finite input -> FC_ERR_DOMAIN (codec.py:230). */
 FC_API fc_status fc_comm_check(fc_comm* comm, int32_t rank);
+/* Teardown check of an IPC communicator (fabric.py:228-236): every rank has
+ * completed the same number of rounds (device epoch counters, read over the
+ * peer mappings); a rank that ran a round its peers never joined left
+ * messages nobody consumed -> FC_ERR_PROTOCOL naming the ranks. Synchronises
+ * the device; call after the ranks' last collective (e.g. behind a barrier). */
+FC_API fc_status fc_comm_teardown_check(fc_comm* comm);
 
 /* Debug/parity: layout of rank's stage-1 receive slot `src` (stage 1) or
  * stage-2 gather slot `src` (stage 2) as written by the last round of the

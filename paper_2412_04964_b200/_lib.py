@@ -81,6 +81,7 @@ _SIGS = {
     "fc_flash_all_reduce_host_rank": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, C.POINTER(fc_flash_cfg)]),
     "fc_flash_all_reduce": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, C.POINTER(fc_flash_cfg), _P]),
     "fc_comm_check": (C.c_int, [_P, _I32]),
+    "fc_comm_teardown_check": (C.c_int, [_P]),
     "fc_comm_slot": (C.c_int, [_P, _I32, _I32, _I32, _P, C.POINTER(fc_layout)]),
     "fc_comm_topology": (C.c_int, [_P, C.POINTER(_I32), C.POINTER(_I32)]),
     "fc_comm_role_profile": (C.c_int, [_P, _I32, C.POINTER(C.c_uint64), _I32, C.POINTER(_I32)]),

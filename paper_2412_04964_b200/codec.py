@@ -201,11 +201,53 @@ def _stream_of(t: torch.Tensor) -> int:
 
 
 class QuantizedTensor:
-    """Packed codes plus per-group fp16 scales and uint8 zeros, on the GPU
-    (codec.py:165-219). `codes`, `scales`, `zeros` are views into one device
-    buffer laid out as include/flashcomm.h `fc_layout` describes."""
+    """Packed codes plus per-group scale / zero metadata (codec.py:165-219),
+    held on the GPU in one device buffer laid out as include/flashcomm.h
+    `fc_layout` describes: `codes` (packed uint8, little nibble first),
+    `scales_f16` (the fp16 wire scales) and `zeros` (uint8, asymmetric int
+    only) are views into it; `scales` is the reference's float32 array.
 
-    def __init__(self, buffer: torch.Tensor, element_count: int, config: CodecConfig):
+    The constructor takes the reference's fields, QuantizedTensor(codes,
+    scales, zeros, element_count, config) -- numpy arrays, tensors, or a
+    packed-bytes object -- and checks them like codec.py:172-181
+    (IntegrityError); the library builds instances from device buffers
+    (`_from_buffer`)."""
+
+    def __init__(self, codes, scales, zeros, element_count: int, config: CodecConfig, device=None):
+        n = int(element_count)
+        L = config.device_layout(n)
+        groups = config.group_count(n)
+        sc = np.asarray(scales.cpu().numpy() if isinstance(scales, torch.Tensor) else scales, dtype=np.float32)
+        if sc.shape != (groups,):
+            raise IntegrityError(f"expected {groups} scales, got {sc.shape}")
+        asym = config.is_int and not config.symmetric
+        if asym:
+            if zeros is None or np.asarray(zeros.cpu() if isinstance(zeros, torch.Tensor) else zeros).shape != (groups,):
+                raise IntegrityError("asymmetric tensor requires one zero per group")
+        elif zeros is not None:
+            raise IntegrityError("zeros are only present for asymmetric integer codecs")
+        raw = codes.data if hasattr(codes, "data") and isinstance(getattr(codes, "data"), (bytes, bytearray)) else codes
+        cb = np.frombuffer(bytes(raw), np.uint8) if isinstance(raw, (bytes, bytearray)) else \
+            np.asarray(raw.cpu().numpy() if isinstance(raw, torch.Tensor) else raw, dtype=np.uint8).ravel()
+        if cb.size != L.codes_bytes:
+            raise IntegrityError(f"expected {L.codes_bytes} code bytes, got {cb.size}")
+        host = np.zeros(L.total_bytes, np.uint8)
+        host[: L.codes_bytes] = cb
+        if groups:
+            host[L.scales_offset: L.scales_offset + 2 * groups] = sc.astype(np.float16).view(np.uint8)
+        if asym:
+            z = zeros.cpu().numpy() if isinstance(zeros, torch.Tensor) else zeros
+            host[L.zeros_offset: L.zeros_offset + groups] = np.asarray(z, dtype=np.uint8)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._init(torch.from_numpy(host).to(dev), n, config)
+
+    @classmethod
+    def _from_buffer(cls, buffer: torch.Tensor, element_count: int, config: CodecConfig) -> "QuantizedTensor":
+        q = cls.__new__(cls)
+        q._init(buffer, int(element_count), config)
+        return q
+
+    def _init(self, buffer: torch.Tensor, element_count: int, config: CodecConfig) -> None:
         self.config = config
         self.element_count = int(element_count)
         self._buf = buffer
@@ -213,10 +255,15 @@ class QuantizedTensor:
         self._layout = L
         self.codes = buffer[: L.codes_bytes]
         if config.is_passthrough:
-            self.scales = torch.empty(0, dtype=torch.float16, device=buffer.device)
+            self.scales_f16 = torch.empty(0, dtype=torch.float16, device=buffer.device)
         else:
-            self.scales = buffer[L.scales_offset: L.scales_offset + 2 * L.groups].view(torch.float16)
+            self.scales_f16 = buffer[L.scales_offset: L.scales_offset + 2 * L.groups].view(torch.float16)
         self.zeros = buffer[L.zeros_offset: L.zeros_offset + L.groups] if (config.is_int and not config.symmetric) else None
+
+    @property
+    def scales(self) -> torch.Tensor:
+        """float32, one per group (codec.py:168); the wire holds them as fp16 (scales_f16)."""
+        return self.scales_f16.float()
 
     @property
     def group_count(self) -> int:
@@ -229,8 +276,8 @@ class QuantizedTensor:
     def to_bytes(self) -> bytes:
         """Reference wire format: codes || fp16 scales || zero bytes (codec.py:193-200)."""
         parts = [self.codes.cpu().numpy().tobytes()]
-        if self.scales.numel():
-            parts.append(self.scales.cpu().numpy().tobytes())
+        if self.scales_f16.numel():
+            parts.append(self.scales_f16.cpu().numpy().tobytes())
         if self.zeros is not None:
             parts.append(self.zeros.cpu().numpy().tobytes())
         return b"".join(parts)
@@ -251,7 +298,7 @@ class QuantizedTensor:
             host[L.scales_offset: L.scales_offset + 2 * g] = raw[L.codes_bytes: L.codes_bytes + 2 * g]
             if config.is_int and not config.symmetric:
                 host[L.zeros_offset: L.zeros_offset + g] = raw[L.codes_bytes + 2 * g:]
-        return cls(torch.from_numpy(host).to(dev), element_count, config)
+        return cls._from_buffer(torch.from_numpy(host).to(dev), element_count, config)
 
     def validate(self) -> None:
         """The reference's decode-time integrity checks (codec.py:360-382):
@@ -262,7 +309,7 @@ class QuantizedTensor:
         cfg = self.config
         if cfg.is_passthrough:
             return
-        s = self.scales.float()
+        s = self.scales_f16.float()
         dev = self.codes.device
         bad_scale = (~torch.isfinite(s)).any() | (s <= 0).any()
         bad_code = torch.zeros((), dtype=torch.bool, device=dev)
@@ -308,7 +355,7 @@ def quantize(x, config: CodecConfig, *, check: bool = True) -> QuantizedTensor:
                                           err.data_ptr() if check else None, stream))
         if check:
             _lib.check(_lib.lib().fc_error_word_check(err.data_ptr(), stream))
-    return QuantizedTensor(buf, n, config)
+    return QuantizedTensor._from_buffer(buf, n, config)
 
 
 def dequantize(q: QuantizedTensor, dtype: torch.dtype = torch.float32, *, validate: bool = True) -> torch.Tensor:

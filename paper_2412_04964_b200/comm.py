@@ -395,6 +395,12 @@ class FlashComm:
             self.check()
         return out
 
+    def teardown_check(self) -> None:
+        """fabric.py:228-236: ProtocolError when the ranks did not all complete the same
+        number of rounds (messages left unconsumed). IPC communicators; call after the
+        ranks' last collective."""
+        _lib.check(_lib.lib().fc_comm_teardown_check(self._h))
+
     def check(self, rank: int = -1) -> None:
         """Synchronize and raise the device-side error of `rank` (all if -1)."""
         _lib.check(_lib.lib().fc_comm_check(self._h, int(rank)))
@@ -414,8 +420,8 @@ class FlashComm:
         qt._buf = raw
         qt._layout = L
         qt.codes = raw[: L.codes_bytes]
-        qt.scales = (raw[L.scales_offset: L.scales_offset + 2 * L.groups].view(torch.float16)
-                     if not config.is_passthrough else torch.empty(0, dtype=torch.float16, device=dev))
+        qt.scales_f16 = (raw[L.scales_offset: L.scales_offset + 2 * L.groups].view(torch.float16)
+                         if not config.is_passthrough else torch.empty(0, dtype=torch.float16, device=dev))
         qt.zeros = raw[L.zeros_offset: L.zeros_offset + L.groups] if (config.is_int and not config.symmetric) else None
         return qt
 
@@ -427,4 +433,57 @@ class FlashComm:
         names = sorted({torch.cuda.get_device_name(d) for d in set(self.devices)})
         return {"world_size": N, "devices": list(self.devices), "device_names": names,
                 "peer_access": [[int(acc[a * N + b]) for b in range(N)] for a in range(N)],
-                "multicast_supported": bool(mc.value), "ipc": self.rank is not None}
+                "multicast_supported": bool(mc.value), "ipc": self.rank is not None,
+                "nvlink": nvlink_topology(sorted(set(self.devices)))}
+
+
+def nvlink_topology(devices: Sequence[int]) -> dict:
+    """NVML view of the box (one 8xB200 NVSwitch node): per CUDA device its PCI bus id,
+    active NVLink links and their remote PCI ids (NVSwitch ports on an HGX B200), and the
+    NVML P2P status between the devices. Missing NVML or NVLink reports empty fields
+    (a single-GPU box has no active links); it never raises."""
+    out = {"nvml": False, "devices": {}}
+    try:
+        import pynvml as nv
+
+        nv.nvmlInit()
+    except Exception as e:  # pragma: no cover - NVML absent
+        out["error"] = repr(e)
+        return out
+    out["nvml"] = True
+    try:
+        handles = {}
+        for d in devices:
+            props = torch.cuda.get_device_properties(d)
+            h = nv.nvmlDeviceGetHandleByUUID(f"GPU-{props.uuid}")  # CUDA ordinal -> NVML handle
+            handles[d] = h
+            pci = nv.nvmlDeviceGetPciInfo(h)
+            bus = pci.busId.decode() if isinstance(pci.busId, bytes) else str(pci.busId)
+            links = []
+            for ln in range(18):  # NVML_NVLINK_MAX_LINKS on Blackwell
+                try:
+                    if nv.nvmlDeviceGetNvLinkState(h, ln) == nv.NVML_FEATURE_ENABLED:
+                        rp = nv.nvmlDeviceGetNvLinkRemotePciInfo_v2(h, ln)
+                        links.append({"link": ln, "remote_bus": rp.busId.decode() if isinstance(rp.busId, bytes)
+                                      else str(rp.busId)})
+                except Exception:
+                    break
+            out["devices"][str(d)] = {"pci_bus_id": bus, "nvlink_active": len(links), "links": links}
+        p2p = {}
+        for a in devices:
+            for b in devices:
+                if a < b:
+                    try:
+                        st = nv.nvmlDeviceGetP2PStatus(handles[a], handles[b], nv.NVML_P2P_CAPS_INDEX_NVLINK)
+                        p2p[f"{a}-{b}"] = "ok" if st == nv.NVML_P2P_STATUS_OK else f"status {st}"
+                    except Exception as e:
+                        p2p[f"{a}-{b}"] = repr(e)
+        out["p2p_nvlink"] = p2p
+    except Exception as e:
+        out["error"] = repr(e)
+    finally:
+        try:
+            nv.nvmlShutdown()
+        except Exception:
+            pass
+    return out

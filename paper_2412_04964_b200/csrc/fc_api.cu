@@ -450,6 +450,29 @@ fc_status fc_flash_all_reduce(fc_comm* c, const void* in, void* out, int64_t n, 
   return FC_DISPATCH_RUN(in_dtype, out_dtype, c, ins, outs, n, cfg, st, r);
 }
 
+fc_status fc_comm_teardown_check(fc_comm* c) {
+  if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
+  if (!c->ipc) return FC_OK;  // one process drives every rank: the ranks run in lockstep
+  FC_CUDA_TRY(cudaSetDevice(c->devices[c->my_rank]));
+  FC_CUDA_TRY(cudaDeviceSynchronize());
+  uint32_t ep[kMaxRanks] = {0};
+  for (int r = 0; r < c->world; ++r) {
+    if (!c->blk[r]) return fail(FC_ERR_PROTOCOL, "rank %d has not mapped rank %d", c->my_rank, r);
+    const uint32_t* e = reinterpret_cast<const uint32_t*>(c->blk[r] + blk_misc_off(c->world, c->slot_bytes, c->flags_cap)) + 8;
+    FC_CUDA_TRY(cudaMemcpy(&ep[r], e, 4, cudaMemcpyDeviceToHost));
+  }
+  std::string un;
+  for (int r = 0; r < c->world; ++r)
+    if (ep[r] != ep[c->my_rank]) {
+      char b[96];
+      snprintf(b, sizeof b, "%s(rank %d: %u rounds, rank %d: %u)", un.empty() ? "" : ", ", c->my_rank,
+               ep[c->my_rank], r, ep[r]);
+      un += b;
+    }
+  if (!un.empty()) return fail(FC_ERR_PROTOCOL, "unconsumed messages at teardown: %s", un.c_str());
+  return FC_OK;
+}
+
 fc_status fc_comm_set_rotation(fc_comm* c, int32_t rank, int32_t dim, int32_t normalize, const float* signs) {
   if (!c) return fail(FC_ERR_CONFIG, "NULL communicator");
   if (dim < 0 || (dim & (dim - 1)) != 0) return fail(FC_ERR_CONFIG, "rotation dimension must be a power of two");

@@ -88,6 +88,18 @@ __device__ __forceinline__ uint32_t* errw(const FlashArgs& a, int owner) {
   return reinterpret_cast<uint32_t*>(a.blk[owner] + blk_misc_off(a.world, a.slot_bytes, a.flags_cap));
 }
 __device__ __forceinline__ uint32_t* fctr(const FlashArgs& a, int owner) { return errw(a, owner) + 128; }
+
+// a wait of `rank` on `peer` timed out: latch the ProtocolError in the rank's own error word
+// and propagate the same word into every other rank's (peer memory, system scope), so their
+// waits give up at once instead of each running into its own timeout -- the reference's
+// fabric abort (fabric.py:140, 168-172, 203-205); every rank then reports the originator
+static __device__ __noinline__ void raise_timeout(const FlashArgs& a, int rank, int peer, uint32_t phase) {
+  const uint32_t w = make_err(kErrTimeout, phase, peer, rank);
+  atomicCAS(errw(a, rank), 0u, w);
+  for (int p = 0; p < a.world; ++p)
+    if (p != rank && a.blk[p]) atomicCAS_system(errw(a, p), 0u, w);
+  __threadfence_system();
+}
 __device__ __forceinline__ uint32_t* barflag(const FlashArgs& a, int owner, int phase, int src) {
   return errw(a, owner) + 16 + phase * kMaxRanks + src;
 }
@@ -191,7 +203,7 @@ __device__ __forceinline__ bool wait_flags(const FlashArgs& a, int rank, uint32_
         break;
       }
       if ((++spins & 63u) == 0 && globaltimer() - t0 > a.timeout_ns) {
-        atomicCAS(errw(a, rank), 0u, make_err(kErrTimeout, phase, peers[threadIdx.x], rank));
+        raise_timeout(a, rank, peers[threadIdx.x], phase);
         *s_abort = 1;
         break;
       }
@@ -525,7 +537,7 @@ static __global__ void k_barrier(FlashArgs a, int rank, int phase) {
     while ((int32_t)(ld_acquire_sys(f) - ep) < 0) {
       if ((*ew >> 28) == kErrTimeout) break;
       if (globaltimer() - t0 > a.timeout_ns) {
-        atomicCAS(errw(a, rank), 0u, make_err(kErrTimeout, kPhBarrier, p, rank));
+        raise_timeout(a, rank, p, kPhBarrier);
         break;
       }
       __nanosleep(100);

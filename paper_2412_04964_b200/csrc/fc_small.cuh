@@ -58,7 +58,7 @@ __device__ __forceinline__ bool small_wait(const FlashArgs& a, int rank, const u
   while ((int32_t)((a.sys_scope ? ld_acquire_sys(f) : ld_acquire_gpu(f)) - ep) < 0) {
     if ((*ew >> 28) == kErrTimeout) return false;
     if ((++spins & 63u) == 0 && globaltimer() - t0 > a.timeout_ns) {
-      atomicCAS(errw(a, rank), 0u, make_err(kErrTimeout, phase, peer, rank));
+      raise_timeout(a, rank, peer, phase);
       return false;
     }
     __nanosleep(32);

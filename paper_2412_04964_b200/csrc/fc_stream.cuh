@@ -283,7 +283,7 @@ __device__ __forceinline__ bool warp_wait_flags(const FlashArgs& a, int rank, co
         break;
       }
       if ((++spins & 63u) == 0 && globaltimer() - t0 > a.timeout_ns) {
-        atomicCAS(errw(a, rank), 0u, make_err(kErrTimeout, phase, peer, rank));
+        raise_timeout(a, rank, peer, phase);
         ok = false;
         break;
       }

@@ -67,7 +67,7 @@ def test_large_c5_shape_bitexact_sample():
     xs = x.reshape(-1)[lo:hi].float().cpu().numpy()
     oq = orc.quantize(xs, orc.Codec(bits=4))
     assert np.array_equal(q.codes[lo // 2: hi // 2].cpu().numpy(), orc.pack(oq.codes, 4))
-    assert np.array_equal(q.scales[lo // 128: hi // 128].cpu().numpy().view(np.uint16), oq.scales.view(np.uint16))
+    assert np.array_equal(q.scales_f16[lo // 128: hi // 128].cpu().numpy().view(np.uint16), oq.scales.view(np.uint16))
     assert np.array_equal(q.zeros[lo // 128: hi // 128].cpu().numpy(), oq.zeros)
 
 
@@ -187,3 +187,33 @@ def test_flash_adversarial_groups_vs_oracle(bits):
     run = fc.flash_all_reduce([t.cuda() for t in ts], fc.FlashConfig.from_bits(bits), out_dtype=torch.float32)
     for o in run.outputs:
         assert np.array_equal(o.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+def test_quantized_tensor_reference_constructor():
+    """QuantizedTensor(codes, scales, zeros, element_count, config) as in
+    codec.py:165-181: float32 scales, shape checks -> IntegrityError, the wire
+    bytes and the decode equal the oracle's."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(1000).astype(np.float32)
+    for oc, cc in ((orc.Codec(bits=4), fc.CodecConfig(bits=4)), (orc.Codec(bits=8, symmetric=True),
+                   fc.CodecConfig(bits=8, symmetric=True)), (orc.Codec(kind="e4m3"), fc.CodecConfig(number_format="e4m3"))):
+        oq = orc.quantize(x, oc)
+        q = fc.QuantizedTensor(orc.pack(oq.codes, oc.storage_bits), oq.scales.astype(np.float32),
+                               oq.zeros if cc.is_int and not cc.symmetric else None, x.size, cc)
+        assert q.scales.dtype == torch.float32 and q.to_bytes() == oq.wire_bytes()
+        assert np.array_equal(fc.dequantize(q).cpu().numpy().view(np.uint32), orc.dequantize(oq).view(np.uint32))
+        with pytest.raises(fc.IntegrityError):
+            fc.QuantizedTensor(np.zeros(1, np.uint8), oq.scales, None, x.size, cc)
+        with pytest.raises(fc.IntegrityError):
+            fc.QuantizedTensor(q.codes, oq.scales[:-1], q.zeros, x.size, cc)
+
+
+def test_topology_nvml():
+    from paper_2412_04964_b200.comm import FlashComm
+
+    comm = FlashComm.local([0, 0], 1 << 16)
+    t = comm.topology()
+    comm.close()
+    assert t["world_size"] == 2 and t["peer_access"][0][1] == 1 and "B200" in " ".join(t["device_names"])
+    nv = t["nvlink"]
+    assert nv["nvml"] and "0" in nv["devices"] and nv["devices"]["0"]["nvlink_active"] >= 0

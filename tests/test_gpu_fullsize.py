@@ -85,10 +85,10 @@ def test_fullsize_vs_reference_digests(name, mode):
                 if s == j:
                     continue
                 q = comm.slot(j, 1, s, cfg.stage1_codec)
-                got = [sha(q.codes), sha(q.scales.view(torch.uint8)), sha(q.zeros)]
+                got = [sha(q.codes), sha(q.scales_f16.view(torch.uint8)), sha(q.zeros)]
                 assert got == d["stage1"][f"{s}->{j}"], f"stage-1 slot {s}->{j}"
                 q2 = comm.slot(s, 2, j, cfg.stage2_codec)
-                got2 = [sha(q2.codes), sha(q2.scales.view(torch.uint8)), sha(q2.zeros)]
+                got2 = [sha(q2.codes), sha(q2.scales_f16.view(torch.uint8)), sha(q2.zeros)]
                 assert got2 == d["stage2"][str(j)], f"stage-2 payload of owner {j} at rank {s}"
         ref32 = outs[0].clone()
         del outs

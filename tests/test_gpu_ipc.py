@@ -68,8 +68,9 @@ def _worker(rank, world, port, q, mode):
             out = comm.all_reduce(x, cfg, out_dtype=torch.float32, check=True)
             got = out.cpu().numpy()
             assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), f"iteration {it}"
+        dist.barrier()
+        comm.teardown_check()  # every rank ran the same rounds
         if mode == "timeout":
-            dist.barrier()
             if rank == 0:
                 comm.set_timeout(2.0)
                 x = torch.from_numpy(xs[0]).cuda().to(torch.bfloat16)
@@ -79,6 +80,28 @@ def _worker(rank, world, port, q, mode):
                     raise AssertionError("expected ProtocolError")
                 except fc.ProtocolError as e:
                     assert "timed out waiting on rank" in str(e), str(e)
+            dist.barrier()
+            # rank 0 ran a round rank 1 never joined: unconsumed at teardown (fabric.py:228-236)
+            try:
+                comm.teardown_check()
+                raise AssertionError("expected ProtocolError")
+            except fc.ProtocolError as e:
+                assert "unconsumed" in str(e), str(e)
+        if mode == "abort":
+            # ranks 0 and 1 call, rank 2 never does; rank 0 (2 s timeout) gives up first and its
+            # abort reaches rank 1 (60 s timeout) at once (fabric.py:168-172, 203-205)
+            import time
+            if rank < 2:
+                comm.set_timeout(2.0 if rank == 0 else 60.0)
+                x = torch.from_numpy(xs[rank]).cuda().to(torch.bfloat16)
+                t0 = time.perf_counter()
+                comm.all_reduce(x, cfg)
+                try:
+                    comm.check()
+                    raise AssertionError("expected ProtocolError")
+                except fc.ProtocolError as e:
+                    assert "rank 0 timed out waiting on rank 2" in str(e), str(e)
+                assert time.perf_counter() - t0 < 20.0, "abort did not propagate"
             dist.barrier()
         comm.close()
         dist.destroy_process_group()
@@ -118,3 +141,7 @@ def test_ipc_parity(world, mode):
 
 def test_ipc_timeout_names_peer():
     _run(2, "timeout")
+
+
+def test_ipc_abort_propagates():
+    _run(3, "abort")
