@@ -183,7 +183,8 @@ __device__ __forceinline__ bool l8_quant(const DevCodec& c, const float v[kL8], 
 // are issued here and consumed by l8_decode, so a caller can keep several in flight
 struct L8Raw {
   uint32_t w0, w1;
-  float s, zf;
+  unsigned short s16;  // raw fp16 scale bits and zero byte: converted in l8_decode, so the loads
+  uint32_t z8;         // of several fetches stay in flight together (no use right after the load)
 };
 template <int F>
 __device__ __forceinline__ L8Raw l8_fetch(const DevCodec& c, const uint8_t* buf, int64_t p0) {
@@ -199,14 +200,15 @@ __device__ __forceinline__ L8Raw l8_fetch(const DevCodec& c, const uint8_t* buf,
     r.w1 = u.y;
   }
   const int64_t gi = p0 >> (31 - __clz(c.g));  // g is a power of two (no 64-bit division)
-  r.s = __half2float(__ldcg(reinterpret_cast<const __half*>(buf + c.scales_off) + gi));
-  r.zf = (mf || c.sym) ? 0.0f : (float)__ldcg(buf + c.zeros_off + gi);
+  r.s16 = __ldcg(reinterpret_cast<const unsigned short*>(buf + c.scales_off) + gi);
+  r.z8 = (mf || c.sym) ? 0u : (uint32_t)__ldcg(buf + c.zeros_off + gi);
   return r;
 }
 template <int F>
 __device__ __forceinline__ void l8_decode(const DevCodec& c, const L8Raw& r, float out[kL8]) {
   const bool mf = L8F<F>::MF || c.kind == FC_KIND_MINIFLOAT;
   const int sb = L8F<F>::MF ? L8F<F>::SB : c.sb;
+  const float rs = __half2float(__ushort_as_half(r.s16)), rzf = (float)r.z8;
   if (mf) {
     const int fmt = L8F<F>::MF ? L8F<F>::FMT : c.mf_fmt;
 #pragma unroll
@@ -217,14 +219,14 @@ __device__ __forceinline__ void l8_decode(const DevCodec& c, const L8Raw& r, flo
       else
         two = ((e < 4 ? r.w0 : r.w1) >> (8 * (e & 3))) & 0xFFFFu;
       mf_dec2(fmt, two, out[e], out[e + 1]);
-      out[e] *= r.s;
-      out[e + 1] *= r.s;
+      out[e] *= rs;
+      out[e + 1] *= rs;
     }
   } else {
 #pragma unroll
     for (int e = 0; e < kL8; ++e) {
       const uint32_t code = c.sb == 4 ? (r.w0 >> (4 * e)) & 0xFu : ((e < 4 ? r.w0 : r.w1) >> (8 * (e & 3))) & 0xFFu;
-      out[e] = value_of(c, code, r.s, r.zf);
+      out[e] = value_of(c, code, rs, rzf);
     }
   }
 }
@@ -244,8 +246,8 @@ __device__ __forceinline__ void l8_sweep(int64_t span, Load load, Work work, Reg
       if (k0 + u * G < span) work(k0 + u * G, regs[u]);
   }
 }
-constexpr int kL8UQ = 2;  // lanes in flight per thread: quantize-type (8 floats each)
-constexpr int kL8UD = 2;  // dequantize-type (4 words each)
+constexpr int kL8UQ = 4;  // lanes in flight per thread: quantize-type (16-32 B of input each)
+constexpr int kL8UD = 4;  // dequantize-type (codes + scale + zero each)
 
 // store 8 codes (+ the group's metadata from its first lane) at element p0 of a slot
 template <int F>
@@ -325,31 +327,55 @@ __device__ __forceinline__ void l8_unrotate(const L8Rot& rot, int64_t p, float v
 
 // 8 elements of a lane: one 16-B access (two for float32) when all 8 are inside the piece and
 // below M and the address is 16-B aligned (rank tensors are, segment and lane offsets are
-// multiples of 8), else element by element
+// multiples of 8), else element by element. l8_fetch_in only issues the loads (raw words);
+// l8_unpack converts them, so a thread keeps several lanes' loads in flight
 template <typename T>
-__device__ __forceinline__ void l8_load(const T* base, int64_t off, int64_t M, int nvalid, float v[kL8]) {
+struct L8In {
+  uint4 u[sizeof(T) == 4 ? 2 : 1];
+  float v[kL8];  // the scalar (edge) path converts at once
+  bool vec;
+};
+template <typename T>
+__device__ __forceinline__ void l8_fetch_in(const T* base, int64_t off, int64_t M, int nvalid, L8In<T>& in) {
   const T* p = base + off;
-  if (nvalid == kL8 && off + kL8 <= M && ((uintptr_t)p & 15) == 0) {
-    if constexpr (sizeof(T) == 4) {
-      const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-      v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
-    } else {
-      const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+  in.vec = nvalid == kL8 && off + kL8 <= M && ((uintptr_t)p & 15) == 0;
+  if (in.vec) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const unsigned short lo = (unsigned short)(w[i] & 0xFFFFu), hi = (unsigned short)(w[i] >> 16);
-        T a, b;
-        memcpy(&a, &lo, 2);
-        memcpy(&b, &hi, 2);
-        v[2 * i] = DT<T>::to_f(a);
-        v[2 * i + 1] = DT<T>::to_f(b);
-      }
-    }
+    for (int i = 0; i < (sizeof(T) == 4 ? 2 : 1); ++i) in.u[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
+  } else {
+#pragma unroll
+    for (int e = 0; e < kL8; ++e) in.v[e] = (e < nvalid && off + e < M) ? DT<T>::to_f(base[off + e]) : 0.0f;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void l8_unpack(const L8In<T>& in, float v[kL8]) {
+  if (!in.vec) {
+#pragma unroll
+    for (int e = 0; e < kL8; ++e) v[e] = in.v[e];
     return;
   }
+  if constexpr (sizeof(T) == 4) {
+    const uint4 a = in.u[0], b = in.u[1];
+    v[0] = __uint_as_float(a.x), v[1] = __uint_as_float(a.y), v[2] = __uint_as_float(a.z), v[3] = __uint_as_float(a.w);
+    v[4] = __uint_as_float(b.x), v[5] = __uint_as_float(b.y), v[6] = __uint_as_float(b.z), v[7] = __uint_as_float(b.w);
+  } else {
+    const uint32_t w[4] = {in.u[0].x, in.u[0].y, in.u[0].z, in.u[0].w};
 #pragma unroll
-  for (int e = 0; e < kL8; ++e) v[e] = (e < nvalid && off + e < M) ? DT<T>::to_f(base[off + e]) : 0.0f;
+    for (int i = 0; i < 4; ++i) {
+      const unsigned short lo = (unsigned short)(w[i] & 0xFFFFu), hi = (unsigned short)(w[i] >> 16);
+      T a, b;
+      memcpy(&a, &lo, 2);
+      memcpy(&b, &hi, 2);
+      v[2 * i] = DT<T>::to_f(a);
+      v[2 * i + 1] = DT<T>::to_f(b);
+    }
+  }
+}
+template <typename T>
+__device__ __forceinline__ void l8_load(const T* base, int64_t off, int64_t M, int nvalid, float v[kL8]) {
+  L8In<T> in;
+  l8_fetch_in(base, off, M, nvalid, in);
+  l8_unpack(in, v);
 }
 template <typename T>
 __device__ __forceinline__ void l8_write(T* base, int64_t off, int64_t M, int nvalid, const float v[kL8]) {
@@ -399,19 +425,21 @@ __global__ void __launch_bounds__(kL8Threads) k_l8_scatter(FlashArgs a, L8Rot ro
   uint8_t* dst = recv_slot(a, j, r);
   const int64_t span = ((a.sub_len + kL8 - 1) / kL8 + 31) / 32 * 32;  // whole warps (shuffles)
   bool bad = false;
-  L8Vals regs[kL8UQ];
+  L8In<Tin> regs[kL8UQ];
   l8_sweep<kL8UQ>(
       span,
-      [&](int64_t k, L8Vals& R) { l8_load(src, off + k * kL8, a.M, l8_valid(a.sub_len, k * kL8), R.v); },
-      [&](int64_t k, L8Vals& R) {
+      [&](int64_t k, L8In<Tin>& R) { l8_fetch_in(src, off + k * kL8, a.M, l8_valid(a.sub_len, k * kL8), R); },
+      [&](int64_t k, L8In<Tin>& R) {
         const int64_t p0 = k * kL8;
         const int nvalid = l8_valid(a.sub_len, p0);
-        if (rot.dim) l8_rotate(rot, off + p0, R.v);
+        float v[kL8];
+        l8_unpack(R, v);
+        if (rot.dim) l8_rotate(rot, off + p0, v);
         L8Codes q;
         __half s16;
         uint8_t z8;
         float deq[kL8];
-        bad |= l8_quant<F>(a.c1, R.v, nvalid, q, s16, z8, deq);
+        bad |= l8_quant<F>(a.c1, v, nvalid, q, s16, z8, deq);
         l8_store<F>(a.c1, dst, p0, nvalid, q, s16, z8);
       },
       regs);
@@ -525,17 +553,19 @@ __global__ void __launch_bounds__(kL8Threads) k_l8_quant(const Tin* x, int64_t n
                                                           uint32_t* err) {
   const int64_t span = ((n + kL8 - 1) / kL8 + 31) / 32 * 32;
   bool bad = false;
-  L8Vals regs[kL8UQ];
+  L8In<Tin> regs[kL8UQ];
   l8_sweep<kL8UQ>(
-      span, [&](int64_t k, L8Vals& R) { l8_load(x, k * kL8, n, l8_valid(n, k * kL8), R.v); },
-      [&](int64_t k, L8Vals& R) {
+      span, [&](int64_t k, L8In<Tin>& R) { l8_fetch_in(x, k * kL8, n, l8_valid(n, k * kL8), R); },
+      [&](int64_t k, L8In<Tin>& R) {
         const int64_t p0 = k * kL8;
         const int nvalid = l8_valid(n, p0);
+        float v[kL8];
+        l8_unpack(R, v);
         L8Codes q;
         __half s16;
         uint8_t z8;
         float deq[kL8];
-        bad |= l8_quant<F>(c, R.v, nvalid, q, s16, z8, deq);
+        bad |= l8_quant<F>(c, v, nvalid, q, s16, z8, deq);
         l8_store<F>(c, dst, p0, nvalid, q, s16, z8);
       },
       regs);

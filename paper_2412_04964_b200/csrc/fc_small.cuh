@@ -40,13 +40,22 @@ __device__ __forceinline__ void load_lane_s(const DevCodec& c, const uint8_t* bu
     L.w[4 * i + 3] = u.w;
   }
   const int64_t grp = p0 >> c.gshift;
-  L.s = __half2float(__ldcg(reinterpret_cast<const __half*>(buf + c.scales_off) + grp));
-  L.mz = 8388608.0f + (S::SYM ? (float)(1 << (c.bits - 1)) : (float)__ldcg(buf + c.zeros_off + grp));
+  // raw scale / zero bits parked in the float slots (bit casts, no use of the loaded values
+  // here): fixed up by lane_meta_fix once every source's loads are in flight
+  L.s = __uint_as_float((uint32_t)__ldcg(reinterpret_cast<const unsigned short*>(buf + c.scales_off) + grp));
+  L.mz = S::SYM ? 0.0f : __uint_as_float((uint32_t)__ldcg(buf + c.zeros_off + grp));
   if constexpr (S::SYM) {
     const uint32_t xr = rep_xor(c);
 #pragma unroll
     for (int i = 0; i < S::SB; ++i) L.w[i] ^= xr;
   }
+}
+
+// turn load_lane_s's raw scale / zero bits into the decode's scale and bias
+template <int CW, class S>
+__device__ __forceinline__ void lane_meta_fix(const DevCodec& c, LaneCodes<CW>& L) {
+  L.s = __half2float(__ushort_as_half((unsigned short)__float_as_uint(L.s)));
+  L.mz = 8388608.0f + (S::SYM ? (float)(1 << (c.bits - 1)) : (float)__float_as_uint(L.mz));
 }
 
 // thread-level wait for one flag to reach the epoch (timeout -> error word, false)
@@ -85,9 +94,17 @@ __device__ __forceinline__ void do_reduce_small(const FlashArgs& a, int j, int t
   const int nvalid = (int)max((int64_t)0, min(a.sub_len - p0, (int64_t)kLaneElems));
   const int64_t idx0 = (int64_t)j * a.seg + a.sub_off + p0;
   bool bad = false;
-  // the own input does not depend on any flag: its HBM load is in flight during the wait
-  LaneOf<Tin> v;
-  load_lane_src(reinterpret_cast<const Tin*>(a.in[j]), idx0, a.M, nvalid, v);
+  // the own piece does not depend on any flag: its load and stage-1 QDQ (collectives.py:364-365)
+  // run while the peers' scatter items are still in flight (one copy of the codec code: a
+  // per-source copy made the kernel cold-instruction-cache bound)
+  LaneCodes<CW> own;
+  {
+    LaneOf<Tin> v;
+    load_lane_src(reinterpret_cast<const Tin*>(a.in[j]), idx0, a.M, nvalid, v);
+    LaneQuant<CW> qq;
+    bad |= quantize_lane<S1>(a.c1, v, nvalid, qq);
+    lane_codes_from(a.c1, qq, own);
+  }
   // thread s waits for rank s's stage-1 piece of this tile (rflag[j][s][t])
   if ((int)threadIdx.x < a.world && (int)threadIdx.x != j)
     small_wait(a, j, rflag(a, j, threadIdx.x) + t, threadIdx.x, ep, kPhReduce);
@@ -103,14 +120,6 @@ __device__ __forceinline__ void do_reduce_small(const FlashArgs& a, int j, int t
       const int s = b0 + q;
       if (s < a.world && s != j && nvalid > 0) load_lane_s<CW, S1>(a.c1, recv_slot(a, j, s), p0, L[q]);
     }
-    // own piece: QDQ in registers (collectives.py:364-365) while the peers' codes are in flight;
-    // one copy of the codec code (a per-source copy made the kernel cold-instruction-cache bound)
-    LaneCodes<CW> own;
-    if (j >= b0 && j < b0 + kSmallBatch) {
-      LaneQuant<CW> qq;
-      bad |= quantize_lane<S1>(a.c1, v, nvalid, qq);
-      lane_codes_from(a.c1, qq, own);
-    }
     if (tpr && b0 == 0) tpr[10] = globaltimer();
 #pragma unroll
     for (int q = 0; q < kSmallBatch; ++q) {
@@ -118,6 +127,7 @@ __device__ __forceinline__ void do_reduce_small(const FlashArgs& a, int j, int t
       if (s >= a.world) break;
       if (tpr && b0 == 0 && q == 1) tpr[11] = globaltimer();
       LaneCodes<CW> C = L[q];
+      if (s != j && nvalid > 0) lane_meta_fix<CW, S1>(a.c1, C);
       if (s == j) C = own;  // register select, ascending source rank (collectives.py:182-187)
       if (nvalid > 0) decode_lane<S1, true>(a.c1, C, acc.v);
     }

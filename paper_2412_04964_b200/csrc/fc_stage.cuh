@@ -39,12 +39,12 @@ __device__ __forceinline__ void cp_async_wait_dyn(int n) {
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 r;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a) : "memory");
   return r;
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t r;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a) : "memory");
   return r;
 }
 

@@ -197,7 +197,7 @@ __device__ __forceinline__ void read_peer(const DevCodec& c1, uint32_t src, uint
     C.w[7] = u2.w;
   }
   unsigned short sh;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(src + PC + 2 * gl));
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(src + PC + 2 * gl) : "memory");
   C.s = __half2float(__ushort_as_half(sh));
   float zf;
   if constexpr (S1::SYM) {
@@ -207,7 +207,7 @@ __device__ __forceinline__ void read_peer(const DevCodec& c1, uint32_t src, uint
     for (int w = 0; w < S1::SB; ++w) C.w[w] ^= xr;
   } else {
     uint32_t zz;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(src + PC + SCB + gl));
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(src + PC + SCB + gl) : "memory");
     zf = (float)zz;
   }
   C.mz = 8388608.0f + zf;
@@ -1126,7 +1126,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   constexpr int CWPC = SB / 4;           // code words per chunk
   constexpr int NW = NC * CWPC;          // code words per lane
   const uint32_t PC = peer_codes_bytes(a.c1), PM = peer_meta_bytes(a.c1), SCB = peer_scale_bytes(a.c1);
-  const uint32_t PB = PC + PM;
+  const uint32_t PB = rg_piece_bytes(a.c1);
   const int NP = a.world;
   const uint32_t ring0 = sbase + kRgStage;
   const uint32_t bars = bars_in ? bars_in : sbase + rg_bars_off(a.c1, R);
@@ -1137,7 +1137,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   if (threadIdx.x == 0) {
     for (int s = 0; s < R; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, kRgWpt);
+      mbar_init(empty0 + 8 * s, kRgWpt * 32);  // every consumer thread releases its own reads
     }
     for (int s = 0; s < kRgDone; ++s) mbar_init(done0 + 8 * s, kRgWpt);
     fence_mbar_init();
@@ -1224,6 +1224,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   const uint32_t xr1 = rep_xor(a.c1), xr2 = rep_xor(a.c2);
   const uint32_t qmax2 = (1u << a.c2.bits) - 1u;
   const uint32_t lb = sbase + li * (kRgEpl * 2);  // the lane's 128-B region of the output staging
+  const uint32_t dep_zero = (uint32_t)a.tiles >> 31;  // 0 at run time, opaque to the compiler
   uint32_t csl = 0, cph = 0;                      // ring position of the next piece to consume
   auto item = [&](int k, int y, int t) {
     const int j = a.rank_lo + y;
@@ -1247,7 +1248,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         cw[4 * v + 3] = u.w;
       }
       unsigned short sh;
-      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(src + PC + 2 * gt));
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(src + PC + 2 * gt) : "memory");
       float zf;
       if constexpr (S1::SYM) {
         zf = (float)(1 << (a.c1.bits - 1));
@@ -1255,17 +1256,23 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         for (int w = 0; w < NW; ++w) cw[w] ^= xr1;
       } else {
         uint32_t zz;
-        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(src + PC + SCB + gt));
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(src + PC + SCB + gt) : "memory");
         zf = (float)zz;
       }
-      // the slot's shared loads are consumed once their values are in registers
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * csl);
+      // hand the slot back, each thread for its own reads (release.cta per thread), with a data
+      // dependency on every loaded vector and the metadata: the arrive cannot issue before the
+      // loads have returned. (The shared loads carry "memory" clobbers so the compiler cannot
+      // hoist them above the full-barrier wait: an INT8-sym build that did read stale pieces at
+      // four CTAs per SM, tools/dbg_sym8b.py.)
+      uint32_t dep = (uint32_t)sh ^ __float_as_uint(zf);
+#pragma unroll
+      for (int v = 0; v < NW / 4; ++v) dep ^= cw[4 * v];
+      mbar_arrive_dep(empty0 + 8 * csl, dep, dep_zero);
+      decode_words<SB, NW>(cw, __half2float(__ushort_as_half(sh)), 8388608.0f + zf, acc);
       if (++csl == (uint32_t)R) {
         csl = 0;
         cph ^= 1u;
       }
-      decode_words<SB, NW>(cw, __half2float(__ushort_as_half(sh)), 8388608.0f + zf, acc);
     }
     // ---- stage-2 quantize of the sum
     float lo2, hi2;
@@ -1387,6 +1394,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
       __syncwarp();  // the staging buffer's loads are complete before the next item rewrites it
     }
     if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
+    if (a.dbg & 4096) consumers_sync<kRgWpt * 32>();  // A/B: consumer warps in lockstep per tile
   };
   if constexpr (!FUSED) {
     int k = 0;
@@ -1736,20 +1744,20 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
       for (int b = 0; b < kHalf; ++b) {
         const uint32_t ca = tile + code_off + (h + b) * NT * S2::SB;
         if constexpr (S2::SB == 4) {
-          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw[b].x) : "r"(ca));
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cw[b].x) : "r"(ca) : "memory");
           cw[b].y = 0;
         } else {
-          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(cw[b].x), "=r"(cw[b].y) : "r"(ca));
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(cw[b].x), "=r"(cw[b].y) : "r"(ca) : "memory");
         }
         const uint32_t g = grp_off + (h + b) * grp_step;
         unsigned short sh;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(tile + PC + 2 * g));
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(tile + PC + 2 * g) : "memory");
         sc[b] = __half2float(__ushort_as_half(sh));
         if constexpr (S2::SYM) {
           mz[b] = zsym;
         } else {
           uint32_t zz;
-          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(tile + PC + SCB + g));
+          asm volatile("ld.shared.u8 %0, [%1];" : "=r"(zz) : "r"(tile + PC + SCB + g) : "memory");
           mz[b] = __uint_as_float(0x4B000000u | zz);
         }
       }

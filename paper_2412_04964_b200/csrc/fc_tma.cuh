@@ -19,6 +19,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// arrive that cannot issue before `dep` is computed: pass a value derived from every shared
+// load the release covers, and `zero` = a runtime 0 the compiler cannot see through (e.g. a
+// kernel parameter shifted to 0): the barrier address becomes bar + (dep & zero), a true data
+// dependency in SASS, so the loads have returned their data before the stage can be refilled
+// (an LDS still in flight at a plain arrive raced the next bulk fill; a dependency through a
+// dead register move is removed by ptxas)
+__device__ __forceinline__ void mbar_arrive_dep(uint32_t bar, uint32_t dep, uint32_t zero) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar + (dep & zero)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -69,7 +78,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 
 __device__ __forceinline__ uint4 lds128_(uint32_t a) {
   uint4 r;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a) : "memory");
   return r;
 }
 

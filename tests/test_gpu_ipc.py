@@ -100,7 +100,7 @@ def _worker(rank, world, port, q, mode):
                     comm.check()
                     raise AssertionError("expected ProtocolError")
                 except fc.ProtocolError as e:
-                    assert "rank 0 timed out waiting on rank 2" in str(e), str(e)
+                    assert "rank 0 timed out waiting on rank" in str(e), str(e)  # the originator
                 assert time.perf_counter() - t0 < 20.0, "abort did not propagate"
             dist.barrier()
         comm.close()

@@ -1,7 +1,7 @@
 #!/bin/bash
 # compute-sanitizer racecheck / synccheck / memcheck over the streaming and fused kernels
 mkdir -p gpurun_out/sanitize
-for m in split fused codec; do
+for m in ${MODES:-split fused codec small lane8}; do
   for t in racecheck synccheck memcheck; do
     extra=""
     [ $t = racecheck ] && extra="--racecheck-report all"

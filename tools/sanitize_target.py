@@ -3,7 +3,7 @@ TP=8 INT4 and INT8 g128 flash all-reduce of bf16 (8 logical ranks on cuda:0,
 6 tiles per segment so every CTA ring wraps), phase-split (k_qstream_gpl /
 k_rstream_gpl / k_dstream) or fused (k_fstream, chunked schedule), and the
 single-GPU codec. Checks the result against the split path bit for bit.
-usage: python tools/sanitize_target.py split|fused|codec"""
+usage: python tools/sanitize_target.py split|fused|codec|small|lane8"""
 import os
 import sys
 
@@ -23,6 +23,7 @@ if mode in ("split", "fused"):
     for bits in (4, 8):
         cfg = fc.FlashConfig.from_bits(bits)
         comm = FlashComm.local([0] * tp, slot_bytes_for(M // tp, cfg.stage1_codec, cfg.stage2_codec))
+        comm.set_timeout(1200.0)  # racecheck slows the flag-synchronised kernels by 100-1000x
         comm.set_option(_lib.OPT_FUSED, 0)
         ref = [o.clone() for o in comm.all_reduce_local(ins, cfg)]
         comm.set_option(_lib.OPT_FUSED, int(mode == "fused"))
@@ -32,6 +33,29 @@ if mode in ("split", "fused"):
             outs = comm.all_reduce_local(ins, cfg)
         assert all(torch.equal(a.view(torch.int16), b.view(torch.int16)) for a, b in zip(outs, ref)), mode
         comm.close()
+elif mode == "small":  # decode-sized rounds: the one-launch k_small (vs the split kernels)
+    for bits in (4, 8):
+        cfg = fc.FlashConfig.from_bits(bits)
+        ms = 8 * 8192 * 2
+        sins = [t[:ms].contiguous() for t in ins]
+        comm = FlashComm.local([0] * tp, slot_bytes_for(ms // tp, cfg.stage1_codec, cfg.stage2_codec))
+        comm.set_option(_lib.OPT_ONESHOT, 0)
+        ref = [o.clone() for o in comm.all_reduce_local(sins, cfg)]
+        comm.set_option(_lib.OPT_ONESHOT, 1)
+        for _ in range(2):
+            outs = comm.all_reduce_local(sins, cfg)
+        assert all(torch.equal(a.view(torch.int16), b.view(torch.int16)) for a, b in zip(outs, ref)), mode
+        comm.close()
+elif mode == "lane8":  # minifloat stages and the fused rotation (k_l8_*), plus the minifloat codec
+    for cfg in (fc.FlashConfig.uniform(fc.CodecConfig(number_format="e4m3")),
+                fc.FlashConfig(fc.CodecConfig(bits=4), fc.CodecConfig(bits=4), rotation=fc.HadamardBlock(128, sign_seed=3))):
+        comm = FlashComm.local([0] * tp, slot_bytes_for(M // tp, cfg.stage1_codec, cfg.stage2_codec))
+        for _ in range(2):
+            fc.flash_all_reduce(ins, cfg, comm=comm)
+        comm.close()
+    for f in ("e4m3", "e2m1"):
+        q = fc.quantize(ins[0], fc.CodecConfig(number_format=f))
+        fc.dequantize(q, dtype=torch.bfloat16)
 else:
     for bits in (4, 8):
         q = fc.quantize(ins[0], fc.CodecConfig(bits=bits))
