@@ -157,7 +157,8 @@ typedef enum {
   FC_OPT_PHASES = 11,       /* measurement only: run just these phases (bit 0/1/2) of a one-GPU split call */
   FC_OPT_FUSED_CHUNK = 12,  /* fused kernel schedule: tiles per chunk (step s scatters chunk s, reduces s-1,
                                gathers s-2); 0 = auto: the whole round on one GPU, a quarter across GPUs */
-  FC_OPT_ONESHOT = 13,      /* one GPU: small calls as one cooperative launch with grid barriers (default 1) */
+  FC_OPT_ONESHOT = 13,      /* decode-sized rounds (<= 8 tiles per segment) as ONE flag-synchronised launch per rank
+                               (k_small) across GPUs / processes: 1 (default), 0 off, 2 also on one GPU */
   FC_OPT_HOST_CHUNK_BYTES = 14, /* fc_flash_all_reduce_host: H2D bytes per rank per pipeline chunk (0 = auto) */
   FC_OPT_FUSED_GATHER_CTAS = 15, /* fused kernel: gather-role CTAs per SM (0 = auto) */
   FC_OPT_ROLE_PROFILE = 16  /* measurement: record the fused kernel's per-CTA role timeline (fc_comm_role_profile) */

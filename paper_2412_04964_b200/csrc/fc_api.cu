@@ -326,7 +326,7 @@ fc_status fc_comm_set_option(fc_comm* c, int32_t option, int64_t value) {
     case FC_OPT_CTAS_PER_SM: c->ctas_per_sm = std::max<int64_t>(0, std::min<int64_t>(16, value)); break;
     case FC_OPT_STREAM_MASK: c->stream_mask = value & 65535; break;
     case FC_OPT_PHASES: c->phases = value & 7; break;
-    case FC_OPT_ONESHOT: c->oneshot = value != 0; break;
+    case FC_OPT_ONESHOT: c->oneshot = value < 0 ? 0 : (value > 2 ? 2 : value); break;
     case FC_OPT_FUSED_CHUNK: c->fused_chunk = std::max<int64_t>(0, value); break;
     case FC_OPT_HOST_CHUNK_BYTES: c->host_chunk_bytes = std::max<int64_t>(0, value); break;
     case FC_OPT_FUSED_GATHER_CTAS: c->fused_gather_ctas = std::max<int64_t>(0, std::min<int64_t>(16, value)); break;

@@ -36,7 +36,7 @@ struct fc_comm {
   int64_t fused = -1, ctas = 0, timeout_ms = 5000, lag = 0, fast = 1;  // fused: -1 auto
   int64_t stream_mask = 0;
   int64_t phases = 0;
-  int64_t oneshot = 1;  // one-GPU small messages: single cooperative launch (k_oneshot)
+  int64_t oneshot = 1;  // decode-sized rounds: the one-launch k_small (1: across GPUs/processes, 2: also one GPU)
   int64_t role_profile = 0;  // record the fused kernel's per-CTA role timeline
   uint64_t* tprof[kMaxRanks] = {nullptr};
   int32_t tprof_ctas[kMaxRanks] = {0};

@@ -359,3 +359,30 @@ def test_fused_kernel_vs_split_and_oracle(tp, codec):
                     assert comm.slot(s, 2, j, cfg.stage2_codec).to_bytes() == res.stage2[j].wire_bytes()
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+@pytest.mark.parametrize("bs", [1, 8, 64])
+def test_small_message_kernel_vs_oracle(bits, bs):
+    """The one-launch small-message kernel (k_small; the default across GPUs for
+    decode-sized rounds), forced on one GPU with OPT_ONESHOT 2: TP=8, bs x 8192
+    bf16 per rank, bit-exact against the oracle, three calls in a row (the
+    in-kernel epoch bump)."""
+    from paper_2412_04964_b200 import _lib
+    from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for
+
+    tp, m = 8, bs * 8192
+    xs = orc.gen_rank_activations(8192, bs, bits, tp)
+    xs = [orc.round_to_bf16(x.ravel()) for x in xs]
+    cfg = fc.FlashConfig.from_bits(bits)
+    oc = orc.Codec(bits=bits)
+    want = orc.flash_all_reduce(xs, oc, oc).outputs[0]
+    comm = FlashComm.local([0] * tp, slot_bytes_for(-(-m // tp), cfg.stage1_codec, cfg.stage2_codec))
+    comm.set_option(_lib.OPT_ONESHOT, 2)
+    ts = [torch.from_numpy(x).cuda().to(torch.bfloat16) for x in xs]
+    for _ in range(3):
+        outs = comm.all_reduce_local(ts, cfg, out_dtype=torch.float32)
+        for o in outs:
+            assert np.array_equal(o.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    assert comm.get_option(_lib.OPT_LAST_LAUNCHES) == 1
+    comm.close()

@@ -19,7 +19,7 @@ for tp in (8,):
         ins = [torch.randn(m, device=dev).to(torch.bfloat16) for _ in range(tp)]
         outs = [torch.empty_like(t) for t in ins]
         res = {}
-        for name, opts in (("small", {_lib.OPT_ONESHOT: 1}), ("split", {_lib.OPT_ONESHOT: 0}),
+        for name, opts in (("small", {_lib.OPT_ONESHOT: 2}), ("split", {_lib.OPT_ONESHOT: 0}),
                            ("fused", {_lib.OPT_FUSED: 1})):
             comm.set_option(_lib.OPT_ONESHOT, 1)
             comm.set_option(_lib.OPT_FUSED, -1)

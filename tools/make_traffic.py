@@ -22,10 +22,11 @@ for r in rows[2:]:
     name = d.get("Kernel Name", "")
     short = name.split("<")[0].split("(")[0].split()[-1]
     try:
-        # ncu reports MB in the raw page for dram__bytes_*.sum (unit row says Mbyte)
-        unit = dict(zip(hdr, rows[1])).get("dram__bytes_read.sum", "byte")
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-        b = (float(d["dram__bytes_read.sum"].replace(",", "")) + float(d["dram__bytes_write.sum"].replace(",", ""))) * scale
+        # the raw page's unit row gives each metric its own unit (byte / Kbyte / Mbyte / Gbyte)
+        units = dict(zip(hdr, rows[1]))
+        sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        b = sum(float(d[k].replace(",", "")) * sc.get(units.get(k, "byte"), 1)
+                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     except (KeyError, ValueError):
         continue
     res.setdefault(short, b)

@@ -33,7 +33,20 @@ for r in rows[2:]:
     if not re.search(kre, d.get("Kernel Name", "")):
         continue
     print(d["Kernel Name"][:70])
-    print("  " + "  ".join(f"{v}={d.get(k, '?')}" for k, v in keys.items()))
+    units = dict(zip(hdr, rows[1]))
+    sc = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}
+
+    def val(k):
+        x = d.get(k, "?")
+        u = units.get(k, "")
+        if k in ("dram__bytes_read.sum", "dram__bytes_write.sum") and u in sc:  # -> MB
+            return f"{float(x.replace(',', '')) * sc[u]:.1f}MB"
+        if k == "dram__bytes.sum.per_second" and u.endswith("/s") and u[:-2] in sc:  # -> GB/s
+            return f"{float(x.replace(',', '')) * sc[u[:-2]] / 1e3:.0f}GB/s"
+        if k == "gpu__time_duration.sum" and u in ("nsecond", "usecond", "msecond"):
+            return f"{float(x.replace(',', '')) * {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3}[u]:.1f}us"
+        return x
+    print("  " + "  ".join(f"{v}={val(k)}" for k, v in keys.items()))
     st = []
     for i in stall_cols:
         try:

@@ -23,6 +23,7 @@ tp = 8
 for bs, warm in ((8, 0), (16, 0)):
     m = bs * 8192
     comm = FlashComm.local([0] * tp, slot_bytes_for(-(-m // tp), cfg.stage1_codec, cfg.stage2_codec))
+    comm.set_option(_lib.OPT_ONESHOT, 2)  # the small-message kernel also on one GPU
     ins = [torch.randn(m, device=dev).to(torch.bfloat16) for _ in range(tp)]
     outs = [torch.empty_like(t) for t in ins]
     res = {}
