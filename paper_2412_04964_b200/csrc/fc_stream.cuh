@@ -611,7 +611,7 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, kGplWpt);
+      mbar_init(empty0 + 8 * s, kGplWpt * 32);  // every consumer thread releases its own reads
     }
     fence_mbar_init();
   }
@@ -776,9 +776,9 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
         const int64_t grp = p0 >> a.c1.gshift;
         *reinterpret_cast<unsigned short*>(jb.dst + a.c1.scales_off + 2 * grp) = g.s16;
         if constexpr (!S1::SYM) jb.dst[a.c1.zeros_off + grp] = (uint8_t)g.z;
-        // the tile's stores are issued: hand the stage back (FUSED: the producer then publishes rflag)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        // the tile's stores are issued (each store consumed the thread's shared loads): every
+        // thread hands the stage back for its own reads (FUSED: the producer then publishes rflag)
+        mbar_arrive(empty0 + 8 * st);
         if (bad && jb.err) atomicOr(jb.err, jb.ecode);
       } else {
         // ragged tail: the 32-element lane codec over this warp's 4096 elements, 1024 at a time
@@ -792,8 +792,7 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
           bad |= quantize_lane<S1>(a.c1, L, nvalid, q);
           store_codes<S1>(a.c1, jb.dst, q0, nvalid, q, lane);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        mbar_arrive(empty0 + 8 * st);
         if (bad && jb.err) atomicOr(jb.err, jb.ecode);
       }
   };
