@@ -261,7 +261,10 @@ static fc_status quant_stream(const T* x, int64_t n, const DevCodec& dc, uint8_t
   // lanes (k_qstream: four float64 group tails per slice cost more than the shuffles;
   // profiles/r02_codec_ab.txt)
   const bool gq_ok = dc.g == 32 || dc.g == 64 || dc.g == 128 || dc.g == 256;
-  const bool gq_auto = dc.g != 32 && !(Spec::SB == 4 && dc.g == kGplG);
+  // INT4 g in {64, 128, 256}: the register-resident group-per-lane kernel (k_qstream_gpl<G>)
+  // (g = 32, four groups per slice, measured slower than the 32-element lanes: 40.8 vs 35.6 us)
+  const bool gpl_ok = Spec::SB == 4 && (dc.g == 64 || dc.g == 128 || dc.g == 256);
+  const bool gq_auto = dc.g != 32 && !gpl_ok;
   if (gq_ok && (sel == 3 || (sel == 0 && gq_auto))) {
     a.stages = 3;
     switch (dc.g) {
@@ -271,11 +274,17 @@ static fc_status quant_stream(const T* x, int64_t n, const DevCodec& dc, uint8_t
       default: return quant_gq<T, Spec, 256>(a, st);
     }
   }
-  if (sel != 1 && Spec::SB == 4 && dc.g == kGplG) {  // one lane per group (INT4; see launch_qstream)
-    const void* k = (const void*)k_qstream_gpl<T, Spec>;
-    FC_TRY(ensure_smem_attr(k, smem));
-    k_qstream_gpl<T, Spec><<<stream_grid_cur(k, kGplThreads, smem, a.tiles), kGplThreads, smem, st>>>(a);
-    return FC_OK;
+  if (sel != 1 && gpl_ok) {  // a lane per 128-element slice, the slice's groups in registers (INT4)
+    auto launch = [&](const void* k, auto kern) -> fc_status {
+      FC_TRY(ensure_smem_attr(k, smem));
+      kern<<<stream_grid_cur(k, kGplThreads, smem, a.tiles), kGplThreads, smem, st>>>(a);
+      return FC_OK;
+    };
+    switch (dc.g) {
+      case 64: return launch((const void*)k_qstream_gpl<T, Spec, 64>, k_qstream_gpl<T, Spec, 64>);
+      case 256: return launch((const void*)k_qstream_gpl<T, Spec, 256>, k_qstream_gpl<T, Spec, 256>);
+      default: return launch((const void*)k_qstream_gpl<T, Spec, 128>, k_qstream_gpl<T, Spec, 128>);
+    }
   }
   const void* k = (const void*)k_qstream<T, Spec>;
   FC_TRY(ensure_smem_attr(k, smem));

@@ -600,9 +600,10 @@ __device__ __forceinline__ void unswizzle_chunks(uint32_t* w, int m) {
   }
 }
 
-template <typename Tin, class S1, bool FUSED, class Iter>
+template <typename Tin, class S1, bool FUSED, class Iter, int G = 128>
 __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, int S, Iter it0, uint32_t bars = 0) {
   static_assert(sizeof(Tin) == 2, "16-bit inputs");
+  static_assert(G == 32 || G == 64 || G == 128 || G == 256, "a lane's 128-element slice holds 4, 2, 1 or half a group");
   constexpr uint32_t STAGE = kTileElems * 2;
   constexpr int NC = kGplG / 8;      // 8-element chunks per group
   constexpr int CWPC = S1::SB / 4;   // code words per chunk
@@ -703,42 +704,62 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
           x[c][2] = u.z;
           x[c][3] = u.w;
         }
-        // group bounds in 16-bit packed arithmetic (exact), then fp32
-        uint32_t mn, mx;
-        if constexpr (S1::SYM) {
-          mx = x[0][0] & 0x7FFF7FFFu;
+        // group bounds in 16-bit packed arithmetic (exact), then fp32. The slice holds NG groups
+        // of CPG chunks (G = 32: four; 64: two; 128: one; 256: half a group, the partner lane --
+        // the adjacent slice -- holds the other half: one shuffle). x[c] is physical chunk c ^ m
+        // (m < 8), whose group is (c / CPG) ^ (m / CPG): the "virtual" group c / CPG of the
+        // step order (equal to the physical one for CPG >= 8) maps to physical group v ^ mg.
+        constexpr int NG = G >= 128 ? 1 : 128 / G;
+        constexpr int CPG = NC / NG;
+        GroupQ gq[NG];
+        bool bad = false;
 #pragma unroll
-          for (int c = 0; c < NC; ++c)
+        for (int v = 0; v < NG; ++v) {
+          uint32_t mn, mx;
+          if constexpr (S1::SYM) {
+            mx = x[v * CPG][0] & 0x7FFF7FFFu;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (c | i) mx = h2max<Tin>(mx, x[c][i] & 0x7FFF7FFFu);
-          mn = mx;
-        } else {
-          mn = h2min<Tin>(x[0][0], x[0][1]);
-          mx = h2max<Tin>(x[0][0], x[0][1]);
+            for (int c = v * CPG; c < (v + 1) * CPG; ++c)
 #pragma unroll
-          for (int c = 0; c < NC; ++c)
+              for (int i = 0; i < 4; ++i)
+                if (c != v * CPG || i) mx = h2max<Tin>(mx, x[c][i] & 0x7FFF7FFFu);
+            mn = mx;
+          } else {
+            mn = h2min<Tin>(x[v * CPG][0], x[v * CPG][1]);
+            mx = h2max<Tin>(x[v * CPG][0], x[v * CPG][1]);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (c > 0 || i > 1) {
-                mn = h2min<Tin>(mn, x[c][i]);
-                mx = h2max<Tin>(mx, x[c][i]);
-              }
+            for (int c = v * CPG; c < (v + 1) * CPG; ++c)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (c > v * CPG || i > 1) {
+                  mn = h2min<Tin>(mn, x[c][i]);
+                  mx = h2max<Tin>(mx, x[c][i]);
+                }
+          }
+          float hi = fmax_nan(h_lo<Tin>(mx), h_hi<Tin>(mx));
+          float lo = S1::SYM ? -hi : fmin_nan(h_lo<Tin>(mn), h_hi<Tin>(mn));
+          if constexpr (G == 256) {
+            hi = fmax_nan(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+            lo = S1::SYM ? -hi : fmin_nan(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+          }
+          const bool bv = !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
+          bad |= bv;
+          group_params<S1>(a.c1, lo, hi, gq[v]);
+          if (bv) gq[v].z = S1::SYM ? gq[v].z : 0u;
         }
-        float hi = fmax_nan(h_lo<Tin>(mx), h_hi<Tin>(mx));
-        float lo = S1::SYM ? -hi : fmin_nan(h_lo<Tin>(mn), h_hi<Tin>(mn));
-        const bool bad = !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
-        GroupQ g;
-        group_params<S1>(a.c1, lo, hi, g);
-        if (bad) g.z = S1::SYM ? g.z : 0u;
         const uint32_t qmax = (1u << a.c1.bits) - 1u;
         uint32_t w[NC * CWPC];
-        if (g.normal) {
 #pragma unroll
-          for (int c = 0; c < NC; ++c) chunk_codes_packed<S1, Tin>(x[c], g, qmax, w + c * CWPC);
-        } else {
+        for (int v = 0; v < NG; ++v) {
+          const GroupQ& g = gq[v];
+          if (g.normal) {
 #pragma unroll
-          for (int c = 0; c < NC; ++c) chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax, w + c * CWPC);
+            for (int c = v * CPG; c < (v + 1) * CPG; ++c) chunk_codes_packed<S1, Tin>(x[c], g, qmax, w + c * CWPC);
+          } else {
+#pragma unroll
+            for (int c = v * CPG; c < (v + 1) * CPG; ++c)
+              chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax, w + c * CWPC);
+          }
         }
         if constexpr (S1::SYM) {
           const uint32_t xr = rep_xor(a.c1);
@@ -773,9 +794,16 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
           for (int v = 0; v < NV; ++v)
             *reinterpret_cast<uint4*>(cd + 16 * v) = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
         }
-        const int64_t grp = p0 >> a.c1.gshift;
-        *reinterpret_cast<unsigned short*>(jb.dst + a.c1.scales_off + 2 * grp) = g.s16;
-        if constexpr (!S1::SYM) jb.dst[a.c1.zeros_off + grp] = (uint8_t)g.z;
+        const int64_t grp = p0 >> a.c1.gshift;  // the slice's first group
+        const int mg = G == 32 ? (m >> 2) : 0;   // virtual -> physical group (G = 32)
+        if (G != 256 || (lane & 1) == 0) {
+#pragma unroll
+          for (int v = 0; v < NG; ++v) {
+            const int64_t gp = grp + (v ^ mg);
+            *reinterpret_cast<unsigned short*>(jb.dst + a.c1.scales_off + 2 * gp) = gq[v].s16;
+            if constexpr (!S1::SYM) jb.dst[a.c1.zeros_off + gp] = (uint8_t)gq[v].z;
+          }
+        }
         // the tile's stores are issued (each store consumed the thread's shared loads): every
         // thread hands the stage back for its own reads (FUSED: the producer then publishes rflag)
         mbar_arrive(empty0 + 8 * st);
@@ -1825,11 +1853,12 @@ __global__ void __launch_bounds__(kStreamThreads) k_qstream(FlashArgs a) {
 }
 
 // g = 128 scatter / codec quantize, one lane per group (q_role_gpl)
-template <typename Tin, class S1>
+template <typename Tin, class S1, int G = 128>
 __global__ void __launch_bounds__(kGplThreads, 3) k_qstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int njobs = a.mode == 1 ? 1 : q_jobs(a);
-  q_role_gpl<Tin, S1, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+  q_role_gpl<Tin, S1, false, RangeIter, G>(a, smem_u32(smem), a.stages,
+                                          RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
 }
 
 // any g in {32, 64, 128, 256}, INT4 or INT8, one lane per 128-element slice (q_role_gq)

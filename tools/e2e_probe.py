@@ -49,7 +49,19 @@ def main():
     print(f"alloc pinned outputs: {wall(lambda: [torch.empty(m, dtype=dt, pin_memory=True) for _ in range(tp)]):.2f} ms")
     print(f"H2D only: {wall(lambda: [d.copy_(h, non_blocking=True) for h, d in zip(hs, ds)]):.2f} ms")
     print(f"D2H only: {wall(lambda: [h.copy_(d, non_blocking=True) for h, d in zip(hs, ds)]):.2f} ms")
-    for mib in (4, 6, 8, 12, 16, 32):
+    # both directions at once (the floor of an all-outputs step): H2D on one stream, D2H on another
+    ho = [torch.empty(m, dtype=dt, pin_memory=True) for _ in range(tp)]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def both():
+        with torch.cuda.stream(s1):
+            for h, d in zip(hs, ds):
+                d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            for h, d in zip(ho, ds):
+                h.copy_(d, non_blocking=True)
+    print(f"H2D + D2H concurrently: {wall(both):.2f} ms")
+    for mib in (2, 4, 6, 8, 12, 16):
         comm.set_option(_lib.OPT_HOST_CHUNK_BYTES, mib << 20)
         comm.all_reduce_host(hs, fcfg)
         t_all = wall(lambda: comm.all_reduce_host(hs, fcfg))
