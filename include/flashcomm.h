@@ -222,8 +222,9 @@ FC_API fc_status fc_comm_teardown_check(fc_comm* comm);
 /* Debug/parity: layout of rank's stage-1 receive slot `src` (stage 1) or
  * stage-2 gather slot `src` (stage 2) as written by the last round of the
  * last call; if dst (device memory, layout->total_bytes) is not NULL the
- * slot is copied there (synchronous). In the fused fast path a rank's own
- * stage-1 piece stays in registers, so slot [rank] of stage 1 is not written. */
+ * slot is copied there (synchronous). Stage-1 slot [rank] (the rank's own
+ * piece) is written only by the kernels that read it back (the group-lane
+ * reduce and the fused kernel); the others keep the own piece in registers. */
 FC_API fc_status fc_comm_slot(fc_comm* comm, int32_t rank, int32_t stage, int32_t src, void* dst,
                               fc_layout* layout);
 /* Topology discovery: peer-access matrix (world*world ints) and NVLink
