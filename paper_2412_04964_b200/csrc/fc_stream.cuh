@@ -642,10 +642,32 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
         // dynamic dealing (DynIter): grab ids until the (role, chunk) is exhausted; a recycled
         // stage's previous item has its stores issued: publish its flag (publish_scatter)
         const DynIter& D = it0;
+        // flags of recycled items are published in batches of kPubBatch behind ONE release fence
+        // (a gpu/system-scope release per item stalled this thread ~3 us each -- it waits for the
+        // consumers' code stores -- and left the ring idle: fused scatter role 290 vs 233 us)
+        constexpr int kPubBatch = 8;
+        int pend[kPubBatch];
+        int npend = 0;
+        auto flush = [&]() {
+          if (npend == 0 || (a.dbg & 512)) {
+            npend = 0;
+            return;
+          }
+          if (a.sys_scope) __threadfence_system();
+          else __threadfence();
+#pragma unroll
+          for (int i = 0; i < kPubBatch; ++i)
+            if (i < npend) {
+              int y, t, r, j;
+              D.decode(pend[i], y, t);
+              qpair_of(a, y, r, j);
+              st_relaxed_sys(rflag(a, j, r) + t, D.ep);
+            }
+          npend = 0;
+        };
         auto publish_id = [&](int old) {
-          int y, t;
-          D.decode(old, y, t);
-          publish_scatter(a, y, t, D.ep);
+          pend[npend++] = old;
+          if (npend == kPubBatch) flush();
         };
         auto recycle = [&]() {
           mbar_wait(empty0 + 8 * st, ph ^ 1);
@@ -676,6 +698,7 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
           mbar_wait(empty0 + 8 * (kp % S), (uint32_t)(kp / S) & 1u);
           publish_id(lds_id(D.meta + 4 * (kp % S)));
         }
+        flush();
       }
     }
     return;
