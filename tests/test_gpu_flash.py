@@ -386,3 +386,60 @@ def test_small_message_kernel_vs_oracle(bits, bs):
             assert np.array_equal(o.cpu().numpy().view(np.uint32), want.view(np.uint32))
     assert comm.get_option(_lib.OPT_LAST_LAUNCHES) == 1
     comm.close()
+
+
+@pytest.mark.parametrize("codec", [dict(bits=4), dict(bits=8), dict(bits=4, symmetric=True),
+                                   dict(bits=8, symmetric=True), dict(bits=4, rounding="ceil")])
+def test_fused_kernel_matches_split_multi_tile(codec):
+    """The fused kernel (k_fstream: dynamic item dealing, per-tile flags, batched
+    flag publishing, chunked schedules) is bit-identical to the phase-split
+    kernels at TP=8 over 48 tiles per segment, for schedule chunks 1 / 2 / auto,
+    repeated calls (tools/fused_stress.py runs the same over more calls)."""
+    from paper_2412_04964_b200 import _lib
+    from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for
+
+    tp, m = 8, 8 * 8192 * 48
+    cfg = fc.FlashConfig.uniform(fc.CodecConfig(**codec))
+    comm = FlashComm.local([0] * tp, slot_bytes_for(m // tp, cfg.stage1_codec, cfg.stage2_codec))
+    g = torch.Generator(device="cuda").manual_seed(codec["bits"])
+    ts = [(torch.randn(m, device="cuda", generator=g) * (1 + r)).to(torch.bfloat16) for r in range(tp)]
+    comm.set_option(_lib.OPT_FUSED, 0)
+    ref = [o.clone() for o in comm.all_reduce_local(ts, cfg)]
+    comm.set_option(_lib.OPT_FUSED, 1)
+    for chunk in (1, 2, 0):
+        comm.set_option(_lib.OPT_FUSED_CHUNK, chunk)
+        for _ in range(3):
+            outs = comm.all_reduce_local(ts, cfg)
+            for a, b in zip(outs, ref):
+                assert torch.equal(a.view(torch.int16), b.view(torch.int16)), chunk
+    comm.close()
+
+
+@pytest.mark.parametrize("codec", [dict(bits=4), dict(bits=8), dict(bits=4, symmetric=True),
+                                   dict(bits=8, symmetric=True)])
+def test_reduce_kernel_deterministic(codec):
+    """The reduce kernel alone (FC_OPT_PHASES 2) on fixed receive slots gives the
+    same stage-2 bytes every time (the piece-ring release race of DESIGN.md
+    section 9 item 26 made INT8 sym non-deterministic at four CTAs per SM)."""
+    from paper_2412_04964_b200 import _lib
+    from paper_2412_04964_b200.comm import FlashComm, slot_bytes_for
+
+    tp = 8
+    m = tp * 8192 * 225
+    cc = fc.CodecConfig(**codec)
+    cfg = fc.FlashConfig.uniform(cc)
+    comm = FlashComm.local([0] * tp, slot_bytes_for(m // tp, cfg.stage1_codec, cfg.stage2_codec))
+    comm.set_option(_lib.OPT_FUSED, 0)
+    g = torch.Generator(device="cuda").manual_seed(tp)
+    ts = [(torch.randn(m, device="cuda", generator=g) * (1 + r)).to(torch.bfloat16) for r in range(tp)]
+    ts[0][5000:5128] = 1000.0
+    ts[1][9000:9128] += 3000.0
+    comm.all_reduce_local(ts, cfg)
+    comm.set_option(_lib.OPT_PHASES, 2)
+    runs = []
+    for _ in range(4):
+        comm.all_reduce_local(ts, cfg)
+        runs.append([comm.slot((j + 1) % tp, 2, j, cc).to_bytes() for j in range(tp)])
+    comm.set_option(_lib.OPT_PHASES, 0)
+    comm.close()
+    assert all(r == runs[0] for r in runs[1:])
