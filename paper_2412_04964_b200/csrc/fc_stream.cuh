@@ -1706,7 +1706,7 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, NCW);
+      mbar_init(empty0 + 8 * s, NCW * 32);  // every consumer thread releases its own reads
     }
     fence_mbar_init();
   }
@@ -1770,6 +1770,7 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
     return;
   }
   const uint32_t xr = rep_xor(c);
+  const uint32_t dep_zero = (uint32_t)a.tiles >> 31;  // 0 at run time, opaque to the compiler
   const float zsym = S2::SYM ? 8388608.0f + (float)(1 << (c.bits - 1)) : 0.0f;
   const uint32_t code_off = threadIdx.x * S2::SB;                // bytes of 8 codes of SB bits
   const uint32_t grp_off = (uint32_t)(threadIdx.x * 8) >> gs;    // tile-local group of block 0
@@ -1822,9 +1823,13 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
         decode8<S2>(w, sc[b], mz[b], val[b]);
       }
       if (h + kHalf >= kBlocks) {
-        // release the stage after the shared loads were consumed (see q_role)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * st);
+        // release the stage per thread, the arrive's address data-dependent on every value this
+        // thread loaded from it (see r_role_gpl: an arrive ahead of an outstanding LDS races the
+        // stage's next bulk fill)
+        uint32_t dep = 0;
+#pragma unroll
+        for (int b = 0; b < kHalf; ++b) dep ^= cw[b].x ^ cw[b].y ^ __float_as_uint(sc[b]) ^ __float_as_uint(mz[b]);
+        mbar_arrive_dep(empty0 + 8 * st, dep, dep_zero);
       }
       if (v >= kTileElems) {  // whole tile: no per-block checks
 #pragma unroll
