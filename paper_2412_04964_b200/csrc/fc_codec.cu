@@ -236,7 +236,7 @@ static int codec_qkernel() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("FC_CODEC_QKERNEL");
-    v = !e ? 0 : (!strcmp(e, "lane") ? 1 : !strcmp(e, "gpl") ? 2 : !strcmp(e, "gq") ? 3 : 0);
+    v = !e ? 0 : (!strcmp(e, "lane") ? 1 : !strcmp(e, "gpl") ? 2 : !strcmp(e, "gq") ? 3 : !strcmp(e, "l8") ? 4 : 0);
   }
   return v;
 }
@@ -321,10 +321,51 @@ static bool l8_codec_ok(const fc_codec& c) {
          (c.group_size & (c.group_size - 1)) == 0;
 }
 
+// minifloat codec on the TMA-fed streaming kernels: 16-bit inputs, g in {64, 128, 256}, whole
+// tiles (the ragged-tail path of q_role_gpl is the integer lane codec), 16-B aligned buffers
+static bool mf_stream_ok(const fc_codec& c, int dtype, int64_t n, const void* a, const void* b, bool quant) {
+  return c.kind == FC_KIND_MINIFLOAT && (c.group_size == 64 || c.group_size == 128 || c.group_size == 256) &&
+         dtype != FC_DTYPE_F32 && (!quant || n % kTileElems == 0) && (uintptr_t)a % 16 == 0 &&
+         (uintptr_t)b % 16 == 0 && codec_qkernel() != 4;  // FC_CODEC_QKERNEL=4: lane-8 kernels (A/B)
+}
+template <typename T, class Spec>
+static fc_status mf_quant_stream(const T* x, int64_t n, const DevCodec& dc, uint8_t* dst, uint32_t* err, cudaStream_t st) {
+  FlashArgs a = codec_args(x, dst, n, dc, err);
+  a.stages = 4;
+  const int smem = a.stages * (kTileElems * 2 + 16);
+  auto launch = [&](const void* k, auto kern) -> fc_status {
+    FC_TRY(ensure_smem_attr(k, smem));
+    kern<<<stream_grid_cur(k, kGplThreads, smem, a.tiles), kGplThreads, smem, st>>>(a);
+    return FC_OK;
+  };
+  switch (dc.g) {
+    case 64: return launch((const void*)k_qstream_gpl<T, Spec, 64>, k_qstream_gpl<T, Spec, 64>);
+    case 256: return launch((const void*)k_qstream_gpl<T, Spec, 256>, k_qstream_gpl<T, Spec, 256>);
+    default: return launch((const void*)k_qstream_gpl<T, Spec, 128>, k_qstream_gpl<T, Spec, 128>);
+  }
+}
+template <class Spec>
+static fc_status mf_quant_any(const void* x, int in_dtype, int64_t n, const DevCodec& dc, void* dst, uint32_t* err,
+                              cudaStream_t st) {
+  if (in_dtype == FC_DTYPE_F16) return mf_quant_stream<__half, Spec>((const __half*)x, n, dc, (uint8_t*)dst, err, st);
+  return mf_quant_stream<__nv_bfloat16, Spec>((const __nv_bfloat16*)x, n, dc, (uint8_t*)dst, err, st);
+}
+template <class Spec>
+static fc_status mf_dequant_any(const void* src, int64_t n, const DevCodec& dc, void* out, int out_dtype,
+                                cudaStream_t st);
+
 fc_status launch_quantize(const void* x, int in_dtype, int64_t n, const fc_codec& c, void* dst, uint32_t* err,
                           cudaStream_t st, bool allow_fast) {
   const fc_layout L = layout_of(c, n);
   const DevCodec dc = dev_codec(c, L);
+  if (allow_fast && mf_stream_ok(c, in_dtype, n, x, dst, true)) {
+    fc_status r = c.reserved == FC_FMT_E4M3 ? mf_quant_any<MfSpec<FC_FMT_E4M3>>(x, in_dtype, n, dc, dst, err, st)
+                  : c.reserved == FC_FMT_E5M2 ? mf_quant_any<MfSpec<FC_FMT_E5M2>>(x, in_dtype, n, dc, dst, err, st)
+                                               : mf_quant_any<MfSpec<FC_FMT_E2M1>>(x, in_dtype, n, dc, dst, err, st);
+    FC_TRY(r);
+    FC_CUDA_TRY(cudaGetLastError());
+    return FC_OK;
+  }
   if (allow_fast && l8_codec_ok(c)) return l8_codec_quantize(x, in_dtype, n, dc, dst, err, st);
   const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)dst % 16 == 0);
   if (allow_fast && fast_group(c) && aligned) {
@@ -380,10 +421,29 @@ fc_status launch_quantize(const void* x, int in_dtype, int64_t n, const fc_codec
   return FC_OK;
 }
 
+template <class Spec>
+static fc_status mf_dequant_any(const void* src, int64_t n, const DevCodec& dc, void* out, int out_dtype,
+                                cudaStream_t st) {
+  const uint8_t* s = (const uint8_t*)src;
+  switch (out_dtype) {
+    case FC_DTYPE_F32: return dequant_stream<float, Spec>(s, n, dc, (float*)out, st);
+    case FC_DTYPE_F16: return dequant_stream<__half, Spec>(s, n, dc, (__half*)out, st);
+    default: return dequant_stream<__nv_bfloat16, Spec>(s, n, dc, (__nv_bfloat16*)out, st);
+  }
+}
+
 fc_status launch_dequantize(const void* src, int64_t n, const fc_codec& c, void* out, int out_dtype,
                             cudaStream_t st, bool allow_fast) {
   const fc_layout L = layout_of(c, n);
   const DevCodec dc = dev_codec(c, L);
+  if (allow_fast && mf_stream_ok(c, FC_DTYPE_BF16, n, src, out, false)) {
+    fc_status r = c.reserved == FC_FMT_E4M3 ? mf_dequant_any<MfSpec<FC_FMT_E4M3>>(src, n, dc, out, out_dtype, st)
+                  : c.reserved == FC_FMT_E5M2 ? mf_dequant_any<MfSpec<FC_FMT_E5M2>>(src, n, dc, out, out_dtype, st)
+                                               : mf_dequant_any<MfSpec<FC_FMT_E2M1>>(src, n, dc, out, out_dtype, st);
+    FC_TRY(r);
+    FC_CUDA_TRY(cudaGetLastError());
+    return FC_OK;
+  }
   if (allow_fast && l8_codec_ok(c)) return l8_codec_dequantize(src, n, dc, out, out_dtype, st);
   const uint8_t* s = (const uint8_t*)src;
   const bool aligned = ((uintptr_t)src % 16 == 0) && ((uintptr_t)out % 16 == 0);

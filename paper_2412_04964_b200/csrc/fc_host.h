@@ -109,8 +109,8 @@ inline DevCodec dev_codec(const fc_codec& c, const fc_layout& L) {
   d.sb = storage_bits(c);
   d.lpg = (c.kind == FC_KIND_INT && fast_group(c)) ? c.group_size / kLaneElems : 1;
   d.gshift = -1;
-  for (int b = 0; b < 31; ++b)
-    if (c.kind == FC_KIND_INT && c.group_size == (1 << b)) d.gshift = b;
+  for (int b = 0; b < 31; ++b)  // integer and minifloat groups (the streaming codec kernels index by shift)
+    if ((c.kind == FC_KIND_INT || c.kind == FC_KIND_MINIFLOAT) && c.group_size == (1 << b)) d.gshift = b;
   if (c.kind == FC_KIND_INT) {
     if (c.symmetric) {
       d.qmax_f = (float)((1 << (c.bits - 1)) - 1);

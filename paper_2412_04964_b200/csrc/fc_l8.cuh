@@ -38,46 +38,6 @@ struct L8Rot {
   const float* signs;
 };
 
-// ------------------------------------------------------------------ minifloat codes (cvt)
-
-// two f32 quotients -> two codes: byte codes (e4m3 / e5m2) in the low / high byte of the
-// result, e2m1 nibbles in the low / high nibble; zero magnitude -> +0 pattern
-__device__ __forceinline__ uint32_t mf_enc2(int fmt, float x0, float x1) {
-  uint32_t r;
-  if (fmt == FC_FMT_E4M3) {
-    unsigned short h;
-    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(x1), "f"(x0));
-    r = h;
-    if ((r & 0x007Fu) == 0) r &= 0xFF00u;
-    if ((r & 0x7F00u) == 0) r &= 0x00FFu;
-  } else if (fmt == FC_FMT_E5M2) {
-    unsigned short h;
-    asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(h) : "f"(x1), "f"(x0));
-    r = h;
-    if ((r & 0x007Fu) == 0) r &= 0xFF00u;
-    if ((r & 0x7F00u) == 0) r &= 0x00FFu;
-  } else {
-    asm("{\n .reg .b8 t;\n cvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n cvt.u32.u8 %0, t;\n}" : "=r"(r) : "f"(x1), "f"(x0));
-    if ((r & 0x07u) == 0) r &= 0xF0u;
-    if ((r & 0x70u) == 0) r &= 0x0Fu;
-  }
-  return r;
-}
-
-// two codes (as packed by mf_enc2) -> two exact fp32 grid values
-__device__ __forceinline__ void mf_dec2(int fmt, uint32_t code2, float& v0, float& v1) {
-  uint32_t h2;
-  if (fmt == FC_FMT_E4M3) {
-    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"((unsigned short)code2));
-  } else if (fmt == FC_FMT_E5M2) {
-    asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h2) : "h"((unsigned short)code2));
-  } else {
-    asm("{\n .reg .b8 t;\n cvt.u8.u32 t, %1;\n cvt.rn.f16x2.e2m1x2 %0, t;\n}" : "=r"(h2) : "r"(code2 & 0xFFu));
-  }
-  v0 = __half2float(__ushort_as_half((unsigned short)(h2 & 0xFFFFu)));
-  v1 = __half2float(__ushort_as_half((unsigned short)(h2 >> 16)));
-}
-
 // ------------------------------------------------------------------ lane-8 codec
 
 // 8 codes packed in storage order (sb 4: one word, little nibble first; sb 8: two words)

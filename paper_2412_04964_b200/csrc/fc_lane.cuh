@@ -73,6 +73,7 @@ struct GenSpec {
   static constexpr bool kLegacy = true;  // the cp.async-staged kernels are compiled for this scheme
   static constexpr int SB = 0;
   static constexpr bool SYM = false, CEIL = false;
+  static constexpr bool MF = false;
 };
 #ifndef FC_STAGED
 #define FC_STAGED 0  // make STAGED=1: also compile the cp.async-staged kernels for the compile-time presets (A/B)
@@ -87,6 +88,19 @@ struct IntSpec {
   static constexpr int SB = SB_;  // storage bits: 4 (bits 2..4) or 8 (bits 5..8)
   static constexpr bool SYM = SYM_;
   static constexpr bool CEIL = CEIL_;
+  static constexpr bool MF = false;
+};
+// group-scaled minifloat codec (codec.py:332-351) on the streaming codec kernels
+// (k_qstream_gpl / k_dstream): absmax groups (SYM), no zero point, codes by
+// cvt.rn.satfinite (mf_enc2) and back by cvt.rn.f16x2 (mf_dec2)
+template <int FMT_>
+struct MfSpec {
+  static constexpr bool kFast = true;
+  static constexpr bool kLegacy = false;
+  static constexpr int SB = FMT_ == FC_FMT_E2M1 ? 4 : 8;
+  static constexpr bool SYM = true, CEIL = false;
+  static constexpr bool MF = true;
+  static constexpr int FMT = FMT_;
 };
 using SpecA4 = IntSpec<4, false, false>;  // INT4 asym nearest (FlashConfig.from_bits(4))
 using SpecA8 = IntSpec<8, false, false>;  // INT8 asym nearest (from_bits(8), INT6 stage 2)
@@ -437,6 +451,46 @@ __device__ __forceinline__ void decode_pairs(const LaneCodes<CW>& L, PairLane<Sp
       emit(2 * i + 1, __byte_perm(v, 0x4B000000u, 0x7441u), __byte_perm(v, 0x4B000000u, 0x7443u), NMZ2, S2);  // e+1, e+3
     }
   }
+}
+
+// ------------------------------------------------------------------ minifloat codes (cvt)
+
+// two f32 quotients -> two codes: byte codes (e4m3 / e5m2) in the low / high byte of the
+// result, e2m1 nibbles in the low / high nibble; zero magnitude -> +0 pattern
+__device__ __forceinline__ uint32_t mf_enc2(int fmt, float x0, float x1) {
+  uint32_t r;
+  if (fmt == FC_FMT_E4M3) {
+    unsigned short h;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(x1), "f"(x0));
+    r = h;
+    if ((r & 0x007Fu) == 0) r &= 0xFF00u;
+    if ((r & 0x7F00u) == 0) r &= 0x00FFu;
+  } else if (fmt == FC_FMT_E5M2) {
+    unsigned short h;
+    asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(h) : "f"(x1), "f"(x0));
+    r = h;
+    if ((r & 0x007Fu) == 0) r &= 0xFF00u;
+    if ((r & 0x7F00u) == 0) r &= 0x00FFu;
+  } else {
+    asm("{\n .reg .b8 t;\n cvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n cvt.u32.u8 %0, t;\n}" : "=r"(r) : "f"(x1), "f"(x0));
+    if ((r & 0x07u) == 0) r &= 0xF0u;
+    if ((r & 0x70u) == 0) r &= 0x0Fu;
+  }
+  return r;
+}
+
+// two codes (as packed by mf_enc2) -> two exact fp32 grid values
+__device__ __forceinline__ void mf_dec2(int fmt, uint32_t code2, float& v0, float& v1) {
+  uint32_t h2;
+  if (fmt == FC_FMT_E4M3) {
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"((unsigned short)code2));
+  } else if (fmt == FC_FMT_E5M2) {
+    asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h2) : "h"((unsigned short)code2));
+  } else {
+    asm("{\n .reg .b8 t;\n cvt.u8.u32 t, %1;\n cvt.rn.f16x2.e2m1x2 %0, t;\n}" : "=r"(h2) : "r"(code2 & 0xFFu));
+  }
+  v0 = __half2float(__ushort_as_half((unsigned short)(h2 & 0xFFFFu)));
+  v1 = __half2float(__ushort_as_half((unsigned short)(h2 >> 16)));
 }
 
 }  // namespace fc

@@ -551,6 +551,26 @@ __device__ __forceinline__ void chunk_codes_clamped(const uint32_t x[4], float s
   }
 }
 
+// minifloat codes of one 8-element chunk: RN32(x / s) by reciprocal + one FMA correction, then
+// cvt.rn.satfinite pairwise (mf_enc2: +0 for zero magnitudes); INT8-like byte storage (e4m3 /
+// e5m2: w[0] = elements 0..3, w[1] = 4..7) or nibbles little-nibble-first (e2m1: w[0])
+template <class Spec, typename Tin>
+__device__ __forceinline__ void chunk_codes_mf(const uint32_t x[4], const GroupQ& g, uint32_t* w) {
+  uint32_t two[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const float x0 = __uint_as_float(chunk_elem<Tin>(x, 2 * p)), x1 = __uint_as_float(chunk_elem<Tin>(x, 2 * p + 1));
+    const float t0 = x0 * g.r, t1 = x1 * g.r;
+    two[p] = mf_enc2(Spec::FMT, fmaf(fmaf(-t0, g.s, x0), g.r, t0), fmaf(fmaf(-t1, g.s, x1), g.r, t1));
+  }
+  if constexpr (Spec::SB == 8) {
+    w[0] = two[0] | (two[1] << 16);
+    w[1] = two[2] | (two[3] << 16);
+  } else {
+    w[0] = two[0] | (two[1] << 8) | (two[2] << 16) | (two[3] << 24);
+  }
+}
+
 // 16-bit packed min / max (NaN-propagating), bf16x2 or f16x2
 template <typename Tin>
 __device__ __forceinline__ uint32_t h2min(uint32_t a, uint32_t b) {
@@ -767,14 +787,27 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
           }
           const bool bv = !(fabsf(lo) <= 3.402823466e38f && fabsf(hi) <= 3.402823466e38f);
           bad |= bv;
-          group_params<S1>(a.c1, lo, hi, gq[v]);
-          if (bv) gq[v].z = S1::SYM ? gq[v].z : 0u;
+          if constexpr (S1::MF) {  // scale = absmax / max_finite (codec.py:345), no zero point
+            gq[v].s16 = __half_as_ushort(snap_scale((double)hi / a.c1.qdiv, a.c1.floor));
+            gq[v].s = __half2float(__ushort_as_half(gq[v].s16));
+            gq[v].r = __frcp_rn(gq[v].s);
+            gq[v].z = 0u;
+            gq[v].normal = true;
+          } else {
+            group_params<S1>(a.c1, lo, hi, gq[v]);
+            if (bv) gq[v].z = S1::SYM ? gq[v].z : 0u;
+          }
         }
         const uint32_t qmax = (1u << a.c1.bits) - 1u;
         uint32_t w[NC * CWPC];
 #pragma unroll
         for (int v = 0; v < NG; ++v) {
           const GroupQ& g = gq[v];
+          if constexpr (S1::MF) {
+#pragma unroll
+            for (int c = v * CPG; c < (v + 1) * CPG; ++c) chunk_codes_mf<S1, Tin>(x[c], g, w + c * CWPC);
+            continue;
+          }
           if (g.normal) {
 #pragma unroll
             for (int c = v * CPG; c < (v + 1) * CPG; ++c) chunk_codes_packed<S1, Tin>(x[c], g, qmax, w + c * CWPC);
@@ -784,7 +817,7 @@ __device__ __forceinline__ void q_role_gpl(const FlashArgs& a, uint32_t sbase, i
               chunk_codes_clamped<S1, Tin>(x[c], g.s, (int)g.z, (int)qmax, w + c * CWPC);
           }
         }
-        if constexpr (S1::SYM) {
+        if constexpr (S1::SYM && !S1::MF) {
           const uint32_t xr = rep_xor(a.c1);
 #pragma unroll
           for (int i = 0; i < NC * CWPC; ++i) w[i] ^= xr;
@@ -1629,6 +1662,16 @@ __device__ __forceinline__ void store8(Tout* p, const float v[8]) {
 // decode the 8 stored codes of one block into v[0..7] (element order)
 template <class Spec>
 __device__ __forceinline__ void decode8(uint2 cw, float s, float mz, float v[8]) {
+  if constexpr (Spec::MF) {  // minifloat codes: exact fp16 grid values, times the scale (exact)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t two = Spec::SB == 8 ? (((p < 2 ? cw.x : cw.y) >> (16 * (p & 1))) & 0xFFFFu) : ((cw.x >> (8 * p)) & 0xFFu);
+      mf_dec2(Spec::FMT, two, v[2 * p], v[2 * p + 1]);
+      v[2 * p] *= s;
+      v[2 * p + 1] *= s;
+    }
+    return;
+  }
   const uint64_t S2 = f2_splat(s), NMZ2 = f2_splat(-mz);
   auto two = [&](uint32_t ma, uint32_t mb, float& x, float& y) {
     uint64_t M;
@@ -1816,7 +1859,7 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
 #pragma unroll
       for (int b = 0; b < kHalf; ++b) {
         uint2 w = cw[b];
-        if constexpr (S2::SYM) {
+        if constexpr (S2::SYM && !S2::MF) {
           w.x ^= xr;
           w.y ^= xr;
         }

@@ -133,3 +133,30 @@ def test_minifloat_flash_ipc_free_path_launch_count():
     comm.all_reduce_local(ts, cfg)
     assert comm.get_option(_lib.OPT_LAST_LAUNCHES) == 3
     comm.close()
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("g", [64, 128, 256])
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+def test_minifloat_streaming_codec_vs_oracle(fmt, g, dt):
+    """16-bit inputs, whole tiles: the minifloat codec on the TMA-fed streaming
+    kernels (k_qstream_gpl<MfSpec> / k_dstream<MfSpec>), bit-exact against the
+    oracle: random groups over 16 binades plus the grid sweep (ties, subnormals,
+    saturation) rounded to the input dtype."""
+    rng = np.random.default_rng(g)
+    n = 8192 * 5
+    x = (rng.standard_normal(n) * np.exp(rng.uniform(-6, 6, n))).astype(np.float32)
+    sw = _grid_sweep(fmt)
+    if dt == torch.float16:  # e5m2 saturation probes exceed the fp16 range (inf would be a DomainError)
+        sw = np.clip(sw, -60000.0, 60000.0)
+    x[: sw.size] = sw
+    t = torch.from_numpy(x).to(dt).cuda()
+    xr = t.float().cpu().numpy()
+    cc = fc.CodecConfig(number_format=fmt, group_size=g)
+    q = fc.quantize(t, cc)
+    oq = orc.quantize(xr, orc.Codec(kind=fmt, group_size=g))
+    assert q.to_bytes() == oq.wire_bytes()
+    for odt in (torch.float32, dt):
+        d = fc.dequantize(q, dtype=odt).float().cpu().numpy()
+        want = torch.from_numpy(orc.dequantize(oq)).to(odt).float().numpy()
+        assert np.array_equal(d.view(np.uint32), want.view(np.uint32))
