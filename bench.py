@@ -611,14 +611,22 @@ def bench_local(args, cfg, peaks):
             "dequantize_us": dms * 1e3, "dequantize_gbs": ab / (dms * 1e-3) / 1e9,
             "frac_quantize": ab / (qms * 1e-3) / 1e9 / peaks["hbm_gbs"],
             "frac_dequantize": ab / (dms * 1e-3) / 1e9 / peaks["hbm_gbs"], "alg_bytes": ab}
-    # ---- lane-8 path (fc_l8.cuh) on the C2 workload: e4m3 stage codecs (cvt.rn.satfinite) and
-    # INT4 g128 with the Hadamard rotation (block 128, seeded signs) fused into the prologue /
-    # epilogue; 8 logical ranks on this GPU, three launches per step
+    # ---- minifloat and rotated flash on the C2 workload, 8 logical ranks on this GPU, three
+    # launches per step: e4m3 stage codecs (cvt.rn.satfinite) on the TMA-fed streaming kernels
+    # (MfSpec) and, beside, on the lane-8 kernels (fc_l8.cuh, FC_OPT_STREAM_MASK bit 10); INT4
+    # g128 with the Hadamard rotation (block 128, seeded signs) fused into the lane-8 kernels'
+    # prologue / epilogue
     lane8 = {}
-    for name, lcfg in (("e4m3_g128", fc.FlashConfig.uniform(fc.CodecConfig(number_format="e4m3"))),
-                       ("int4_g128_rot128", fc.FlashConfig(fc.CodecConfig(bits=4), fc.CodecConfig(bits=4),
-                                                           rotation=fc.HadamardBlock(128, sign_seed=1)))):
+    e4 = fc.FlashConfig.uniform(fc.CodecConfig(number_format="e4m3"))
+    for name, lcfg, lmask, kern in (
+            ("e4m3_g128", e4, 0, "k_qstream_gpl | k_rstream_gpl | k_dstream <MfSpec e4m3>"),
+            ("e4m3_g128_lane8", e4, 1024, "k_l8_scatter | k_l8_reduce | k_l8_gather"),
+            ("int4_g128_rot128", fc.FlashConfig(fc.CodecConfig(bits=4), fc.CodecConfig(bits=4),
+                                                rotation=fc.HadamardBlock(128, sign_seed=1)), 0,
+             "k_l8_scatter | k_l8_reduce | k_l8_gather")):
         lcomm = FlashComm.local([0] * tp, slot_bytes_for(seg, lcfg.stage1_codec, lcfg.stage2_codec))
+        if lmask:
+            lcomm.set_option(_lib.OPT_STREAM_MASK, lmask)
         louts = [torch.empty(m, device=dev, dtype=dt) for _ in range(tp)]
         signs = None
         if lcfg.rotation is not None:
@@ -635,7 +643,7 @@ def bench_local(args, cfg, peaks):
         lane8[name] = {"ms_per_step": lms, "value_gbs": tp * e * m / (lms * 1e-3) / 1e9,
                        "hbm_alg_bytes": lb, "frac": lb / (lms * 1e-3) / 1e9 / peaks["hbm_gbs"],
                        "launches_per_step": lcomm.get_option(_lib.OPT_LAST_LAUNCHES),
-                       "kernels": "k_l8_scatter | k_l8_reduce | k_l8_gather"}
+                       "kernels": kern}
         lcomm.set_rotation(None)
         lcomm.close()
         del louts, signs

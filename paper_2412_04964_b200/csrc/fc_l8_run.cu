@@ -79,12 +79,78 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
     ++g_launch_count;
     return FC_OK;
   };
+  // one minifloat format in both stages, g = 128, 16-bit inputs and outputs, no rotation: the
+  // TMA-fed streaming kernels (k_qstream_gpl / k_rstream_gpl / k_dstream on MfSpec) take every
+  // round of whole tiles; the lane-8 kernels the rest (bit 10 of FC_OPT_STREAM_MASK: A/B off)
+  bool stream_ok = false;
+  if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {
+    stream_ok = c->fast == 1 && c->rot_dim == 0 && !(c->stream_mask & 1024);
+    for (int r = 0; r < N && stream_ok; ++r) {
+      if (only_rank >= 0 && r != only_rank) continue;
+      stream_ok = (uintptr_t)ins[r] % 16 == 0 && (uintptr_t)outs[r] % 16 == 0;
+    }
+    a.stage_hint = (int)c->reduce_stages;
+    a.q_hint = (int)c->q_stages;
+    a.d_hint = (int)c->d_stages;
+    a.cta_cap = (int)c->ctas_per_sm;
+    a.dbg = (int)c->stream_mask;
+  }
+  // the three streaming phase launches for ranks [lo, hi) on device dev (ownq: the scatter
+  // stage-1 quantizes the own piece into the receive slot too, the reduce reads it there)
+  auto stream_phase = [&](int ph, int lo, int hi, int dev, cudaStream_t s) -> fc_status {
+    if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {
+      using MS = MfSpec<F - 1>;
+      FlashArgs b = a;
+      b.rank_lo = lo;
+      b.rank_hi = hi;
+      b.ownq = 1;
+      const int64_t nr = hi - lo;
+      if (ph == 0) return launch_qstream<Tin, MS>(b, dev, s, nr * N * b.tiles);
+      if (ph == 1) return launch_rstream<Tin, Tout, MS, MS>(b, dev, s, nr * b.tiles);
+      return launch_dstream<Tout, MS>(b, dev, s, nr * (N - 1) * b.tiles);
+    } else {
+      return fail(FC_ERR_CONFIG, "internal: minifloat streaming phase without a compile-time format");
+    }
+  };
   for (int64_t k = 0; k < rounds; ++k) {
     a.sub_off = span_lo + k * p.R;
     a.sub_len = std::min(p.R, span_hi - a.sub_off);
     a.tiles = (int)ceil_div(a.sub_len, kTileElems);
     a.epoch = ++c->epoch;
     a.epoch_dev = nullptr;
+    bool strm = false;
+    if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {
+      FlashArgs t = a;  // every rank decides alike: the last owner's segment bounds the round
+      t.rank_lo = 0;
+      t.rank_hi = N;
+      strm = stream_ok && rgpl_ok<Tin, Tout, MfSpec<F - 1>, MfSpec<F - 1>>(t);
+    }
+    if (strm) {
+      if (only_rank >= 0) {
+        const int r = only_rank, dev = c->devices[r];
+        FC_CUDA_TRY(cudaSetDevice(dev));
+        FC_TRY(bump_epoch(c, a, r, st[r]));
+        FC_TRY(stream_phase(0, r, r + 1, dev, st[r]));
+        FC_TRY(ipc_barrier(c, a, r, 0, st[r]));
+        FC_TRY(stream_phase(1, r, r + 1, dev, st[r]));
+        FC_TRY(ipc_barrier(c, a, r, 1, st[r]));
+        FC_TRY(stream_phase(2, r, r + 1, dev, st[r]));
+      } else if (single_dev) {
+        const int dev = c->devices[0];
+        FC_CUDA_TRY(cudaSetDevice(dev));
+        for (int ph = 0; ph < 3; ++ph) FC_TRY(stream_phase(ph, 0, N, dev, st[0]));
+      } else {
+        for (int ph = 0; ph < 3; ++ph) {
+          if (ph) FC_TRY(cross_sync(c, st));
+          for (int r = 0; r < N; ++r) {
+            FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+            FC_TRY(stream_phase(ph, r, r + 1, c->devices[r], st[r]));
+          }
+        }
+      }
+      FC_CUDA_TRY(cudaGetLastError());
+      continue;
+    }
     if (only_rank >= 0) {
       const int r = only_rank, dev = c->devices[r];
       FC_CUDA_TRY(cudaSetDevice(dev));

@@ -1142,6 +1142,35 @@ __device__ __forceinline__ void decode_words(const uint32_t* cw, float s, float 
     decode_words8<NW>(cw, s, mz, acc);
 }
 
+// acc (+)= grid * s for NW minifloat code words into the pairing of the storage width (e4m3 /
+// e5m2 bytes: (4i+a, 4i+a+2); e2m1 nibbles: (8i+a, 8i+a+4)). grid * s is exact (a few-bit
+// grid value times an fp16 scale), so the FFMA2 rounds once like the reference's add
+template <class Spec, int NW>
+__device__ __forceinline__ void decode_words_mf(const uint32_t* cw, float s, uint64_t* acc) {
+  const uint64_t S2 = f2_splat(s);
+  auto emit = [&](int idx, uint32_t two) {
+    float v0, v1;
+    mf_dec2(Spec::FMT, two, v0, v1);
+    uint64_t M;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(M) : "f"(v0), "f"(v1));
+    acc[idx] = f2_fma(M, S2, acc[idx]);
+  };
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    if constexpr (Spec::SB == 8) {
+      emit(2 * i + 0, __byte_perm(cw[i], 0u, 0x0020u) & 0xFFFFu);  // elements 4i, 4i+2
+      emit(2 * i + 1, __byte_perm(cw[i], 0u, 0x0031u) & 0xFFFFu);  // 4i+1, 4i+3
+    } else {
+      const uint32_t lo = cw[i] & 0x0F0F0F0Fu, hi = (cw[i] >> 4) & 0x0F0F0F0Fu;
+      const uint32_t t = lo | (lo >> 12), u = hi | (hi >> 12);  // byte 0: (a, a+4), byte 1: (a+2, a+6)
+      emit(4 * i + 0, t & 0xFFu);
+      emit(4 * i + 2, (t >> 8) & 0xFFu);
+      emit(4 * i + 1, u & 0xFFu);
+      emit(4 * i + 3, (u >> 8) & 0xFFu);
+    }
+  }
+}
+
 // element e of accumulators held in the pairing of storage width SB
 template <int SB = 4>
 __device__ __forceinline__ float acc_get(const uint64_t* acc, int e) {
@@ -1304,7 +1333,7 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
   const int li = warp * 32 + lane;         // lane slice of the tile: elements [li*64, li*64+64)
   const int gt = li / kRgLpg;              // tile-local group
   const bool lead = (li & (kRgLpg - 1)) == 0;
-  const uint32_t xr1 = rep_xor(a.c1), xr2 = rep_xor(a.c2);
+  const uint32_t xr1 = S1::MF ? 0u : rep_xor(a.c1), xr2 = S2::MF ? 0u : rep_xor(a.c2);
   const uint32_t qmax2 = (1u << a.c2.bits) - 1u;
   const uint32_t lb = sbase + li * (kRgEpl * 2);  // the lane's 128-B region of the output staging
   const uint32_t dep_zero = (uint32_t)a.tiles >> 31;  // 0 at run time, opaque to the compiler
@@ -1333,7 +1362,9 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
       unsigned short sh;
       asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sh) : "r"(src + PC + 2 * gt) : "memory");
       float zf;
-      if constexpr (S1::SYM) {
+      if constexpr (S1::MF) {  // minifloat codes: no zero point, stored as is
+        zf = 0.0f;
+      } else if constexpr (S1::SYM) {
         zf = (float)(1 << (a.c1.bits - 1));
 #pragma unroll
         for (int w = 0; w < NW; ++w) cw[w] ^= xr1;
@@ -1351,7 +1382,10 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
 #pragma unroll
       for (int v = 0; v < NW / 4; ++v) dep ^= cw[4 * v];
       mbar_arrive_dep(empty0 + 8 * csl, dep, dep_zero);
-      decode_words<SB, NW>(cw, __half2float(__ushort_as_half(sh)), 8388608.0f + zf, acc);
+      if constexpr (S1::MF)
+        decode_words_mf<S1, NW>(cw, __half2float(__ushort_as_half(sh)), acc);
+      else
+        decode_words<SB, NW>(cw, __half2float(__ushort_as_half(sh)), 8388608.0f + zf, acc);
       if (++csl == (uint32_t)R) {
         csl = 0;
         cph ^= 1u;
@@ -1378,10 +1412,40 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     }
     const bool bad = !(fabsf(lo2) <= 3.402823466e38f && fabsf(hi2) <= 3.402823466e38f);
     GroupQ g2;
-    group_params<S2>(a.c2, lo2, hi2, g2);
-    if (bad) g2.z = S2::SYM ? g2.z : 0u;
+    if constexpr (S2::MF) {  // scale = absmax / max_finite (codec.py:345), no zero point
+      g2.s16 = __half_as_ushort(snap_scale((double)hi2 / a.c2.qdiv, a.c2.floor));
+      g2.s = __half2float(__ushort_as_half(g2.s16));
+      g2.r = __frcp_rn(g2.s);
+      g2.z = 0u;
+      g2.normal = true;
+    } else {
+      group_params<S2>(a.c2, lo2, hi2, g2);
+      if (bad) g2.z = S2::SYM ? g2.z : 0u;
+    }
     uint32_t w2[NW];
-    if (g2.normal) {
+    if constexpr (S2::MF) {
+      // RN32(x / s) by reciprocal + one FMA correction (pairwise), then cvt.rn.satfinite
+      const uint64_t R2 = f2_splat(g2.r), NS2 = f2_splat(-g2.s);
+      auto quo = [&](uint64_t X, float& qa, float& qb) {
+        const uint64_t T = f2_mul(X, R2);
+        f2_unpack(f2_fma(f2_fma(T, NS2, X), R2, T), qa, qb);
+      };
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        if constexpr (SB == 8) {
+          float q0, q1, q2, q3;
+          quo(acc[2 * i], q0, q2);
+          quo(acc[2 * i + 1], q1, q3);
+          w2[i] = mf_enc2(S2::FMT, q0, q1) | (mf_enc2(S2::FMT, q2, q3) << 16);
+        } else {
+          float q[8];
+#pragma unroll
+          for (int aa = 0; aa < 4; ++aa) quo(acc[4 * i + aa], q[aa], q[aa + 4]);
+          w2[i] = mf_enc2(S2::FMT, q[0], q[1]) | (mf_enc2(S2::FMT, q[2], q[3]) << 8) |
+                  (mf_enc2(S2::FMT, q[4], q[5]) << 16) | (mf_enc2(S2::FMT, q[6], q[7]) << 24);
+        }
+      }
+    } else if (g2.normal) {
       const uint64_t R2 = f2_splat(g2.r), NS2 = f2_splat(-g2.s), C2 = f2_splat(12582912.0f);
       const uint32_t Z2 = g2.z * 0x00010001u, Q2 = qmax2 * 0x00010001u;
       auto code_pair = [&](uint64_t X) -> uint32_t {
@@ -1453,7 +1517,10 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
     {
 #pragma unroll
       for (int e = 0; e < 4 * NC; ++e) acc[e] = 0ull;
-      decode_words<SB, NW>(w2, g2.s, 8388608.0f + (float)g2.z, acc);  // 0 + (c - z) s: exact, never -0
+      if constexpr (S2::MF)
+        decode_words_mf<S2, NW>(w2, g2.s, acc);  // 0 + grid s: exact, +0 for the +0 code
+      else
+        decode_words<SB, NW>(w2, g2.s, 8388608.0f + (float)g2.z, acc);  // 0 + (c - z) s: exact, never -0
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         uint32_t h[4];

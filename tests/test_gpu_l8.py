@@ -160,3 +160,40 @@ def test_minifloat_streaming_codec_vs_oracle(fmt, g, dt):
         d = fc.dequantize(q, dtype=odt).float().cpu().numpy()
         want = torch.from_numpy(orc.dequantize(oq)).to(odt).float().numpy()
         assert np.array_equal(d.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("slot_tiles", [0, 1])
+def test_flash_minifloat_streaming_vs_oracle(fmt, dt, slot_tiles):
+    """One minifloat format in both stages, g = 128, 16-bit in and out: the TMA-fed streaming
+    kernels (k_qstream_gpl / k_rstream_gpl / k_dstream on MfSpec) -- one round, or three
+    rounds of one tile (slots sized for one tile) -- bit-exact against the oracle, stage
+    buffers included, and equal to the lane-8 kernels (FC_OPT_STREAM_MASK bit 10)."""
+    n, tiles = 8, 3
+    m = n * 8192 * tiles
+    rng = np.random.default_rng(7)
+    xs = [(rng.standard_normal(m) * np.exp(rng.uniform(-3, 3, m))).astype(np.float32) for _ in range(n)]
+    ts = [torch.from_numpy(x).to(dt) for x in xs]
+    xs = [t.float().numpy() for t in ts]
+    oc = orc.Codec(kind=fmt, group_size=128)
+    res = orc.flash_all_reduce(xs, oc, oc)
+    cc = fc.CodecConfig(number_format=fmt, group_size=128)
+    cfg = fc.FlashConfig.uniform(cc)
+    seg = m // n
+    comm = FlashComm.local([0] * n, slot_bytes_for(8192 if slot_tiles else seg, cc, cc))
+    dts = [t.cuda() for t in ts]
+    want = torch.from_numpy(res.outputs[0]).to(dt).view(torch.int16).numpy()
+    run = fc.flash_all_reduce(dts, cfg, comm=comm, out_dtype=dt)
+    launches = comm.get_option(_lib.OPT_LAST_LAUNCHES)  # three per round
+    assert launches == 3 if not slot_tiles else (launches % 3 == 0 and launches >= 6)
+    for o in run.outputs:
+        assert np.array_equal(o.view(torch.int16).cpu().numpy(), want)
+    if not slot_tiles:
+        assert comm.slot(1, 1, 0, cc).to_bytes() == res.stage1[1][0].wire_bytes()
+        assert comm.slot(0, 2, 3, cc).to_bytes() == res.stage2[3].wire_bytes()
+    comm.set_option(_lib.OPT_STREAM_MASK, 1024)
+    run2 = fc.flash_all_reduce(dts, cfg, comm=comm, out_dtype=dt)
+    for o, o2 in zip(run.outputs, run2.outputs):
+        assert torch.equal(o.view(torch.int16), o2.view(torch.int16))
+    comm.close()
