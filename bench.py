@@ -503,6 +503,10 @@ def bench_local(args, cfg, peaks):
     clk = clocks.stop()
     comm.check()
     value = tp * e * m / (ms * 1e-3) / 1e9
+    # beside (not the value): the same K steps captured in one CUDA graph, as a serving engine
+    # replays them -- no per-call host launch cost (it bounds the small C1 / C4 steps)
+    gms = graph_time(step, args.steps, stream)
+    comm.check()
 
     # ---- per-phase kernels (measurement option: one phase per call), CUDA events on the launch stream
     b1 = wire_len(cfg["bits"], cfg["group"], seg) / seg
@@ -519,7 +523,8 @@ def bench_local(args, cfg, peaks):
     # per rank: input read + output write (2 e M) + the N-1 peer pieces of both stages written and read once
     alg_step = tp * (2 * e * m + 2 * (tp - 1) * seg * (b1 + b2))
     # INT4 g = 128 runs the group-per-lane scatter (q_role_gpl)
-    gpl = cfg["group"] == 128 and cfg["bits"] == 4
+    # (INT8 too for rounds up to 256 tiles per segment, fc_run.cuh launch_qstream)
+    gpl = cfg["group"] == 128 and (cfg["bits"] == 4 or seg <= 256 * 8192)
     phase_kernel = {"scatter": "k_qstream_gpl" if gpl else "k_qstream",
                     "reduce": "k_rstream_gpl" if cfg["group"] == 128 else "k_rstream", "gather": "k_dstream"}
     phases = {}
@@ -550,7 +555,8 @@ def bench_local(args, cfg, peaks):
                 "kernel_us": phases[dom]["us"], "peak_source": peaks["source"],
                 "step": {"alg_bytes": alg_step, "achieved": alg_step / (ms * 1e-3) / 1e9,
                          "frac": alg_step / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-                         "t_roof_us": alg_step / peaks["hbm_gbs"] / 1e3}}
+                         "t_roof_us": alg_step / peaks["hbm_gbs"] / 1e3,
+                         "ms_graph": gms, "frac_graph": alg_step / (gms * 1e-3) / 1e9 / peaks["hbm_gbs"]}}
 
     # ---- e2e: the reference-facing call with HOST buffers (pinned): every rank's host array
     # in, a new host array out for EVERY rank (the reference returns all N outputs), one

@@ -1763,6 +1763,7 @@ __device__ __forceinline__ void decode8(uint2 cw, float s, float mz, float v[8])
 // from a single CTA: more CTAs / deeper rings put more concurrent read streams against
 // its output writes (C2: 198-201 µs at 1 CTA x 6-7 stages vs 222 µs at 3 x 6; tools/gather_sweep.sh)
 constexpr int kDCtasPerSm = 1;
+constexpr int64_t kDSmallItems = 4096;  // gather items (tiles) at most for the small-round CTA count
 template <class S2>
 constexpr int dstream_stages() { return S2::SB == 4 ? 7 : 5; }
 
@@ -1983,51 +1984,73 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
 
 // ------------------------------------------------------------------ phase-split kernels
 
+// Programmatic dependent launch (the phase kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a CTA waits for the previous kernel's
+// completion (and the visibility of its memory) before its first global access, and lets the
+// next kernel launch once its own work is issued -- the next phase's launch and CTA
+// scheduling overlap this phase's last CTAs. (Triggering at entry instead placed the next
+// kernel's CTAs on the SMs that drained first, unbalancing its persistent grid:
+// tools/pdl_probe.py.) Both are no-ops for plain launches.
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_exit() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 template <typename Tin, class S1>
 __global__ void __launch_bounds__(kStreamThreads) k_qstream(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  pdl_enter();
   const int njobs = a.mode == 1 ? 1 : q_jobs(a);
   q_role<Tin, S1, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+  pdl_exit();
 }
 
 // g = 128 scatter / codec quantize, one lane per group (q_role_gpl)
 template <typename Tin, class S1, int G = 128>
 __global__ void __launch_bounds__(kGplThreads, 3) k_qstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  pdl_enter();
   const int njobs = a.mode == 1 ? 1 : q_jobs(a);
   q_role_gpl<Tin, S1, false, RangeIter, G>(a, smem_u32(smem), a.stages,
                                           RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+  pdl_exit();
 }
 
 // any g in {32, 64, 128, 256}, INT4 or INT8, one lane per 128-element slice (q_role_gq)
 template <typename Tin, class S1, int G>
 __global__ void __launch_bounds__(kGplThreads, 4) k_qstream_gq(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  pdl_enter();
   const int njobs = a.mode == 1 ? 1 : q_jobs(a);
   q_role_gq<Tin, S1, G, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+  pdl_exit();
 }
 
 template <typename Tin, typename Tout, class S1, class S2>
 __global__ void __launch_bounds__(kStreamThreads, 2) k_rstream(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  pdl_enter();
   r_role<Tin, Tout, S1, S2, false>(a, smem_u32(smem), a.stages,
                                    RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+  pdl_exit();
 }
 
 // g = 128 reduce, two lanes per group (r_role_gpl, a.stages piece slots); one storage width, whole tiles only
 template <typename Tin, typename Tout, class S1, class S2>
 __global__ void __launch_bounds__(kGplThreads, 4) k_rstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  pdl_enter();
   if constexpr (sizeof(Tout) == 2 && S1::SB == S2::SB)
     r_role_gpl<Tin, Tout, S1, S2, false>(a, smem_u32(smem), a.stages,
                                   RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+  pdl_exit();
 }
 
 template <typename Tout, class S2>
 __global__ void __launch_bounds__(kStreamThreads) k_dstream(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  pdl_enter();
   const int njobs = a.mode == 1 ? 1 : (a.rank_hi - a.rank_lo) * (a.world - 1);
   d_role<Tout, S2, false>(a, smem_u32(smem), a.stages, RangeIter(njobs * a.tiles, a.tiles, blockIdx.x, gridDim.x));
+  pdl_exit();
 }
 
 // ------------------------------------------------------------------ fused kernel
