@@ -48,9 +48,6 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
     L8Rot rot{c->rot_dim, c->rot_normalize, c->rot_dim ? c->rot_signs[r] : nullptr};
     return rot;
   };
-  const int64_t span_lo = c->span_hi >= 0 ? c->span_lo : 0;
-  const int64_t span_hi = c->span_hi >= 0 ? std::min(c->span_hi, p.seg) : p.seg;
-  const int64_t rounds = ceil_div(span_hi - span_lo, p.R);
   // one launch per phase for ranks [lo, hi) on device dev
   auto scatter = [&](int lo, int hi, int dev, cudaStream_t s) -> fc_status {
     FlashArgs b = a;
@@ -89,12 +86,25 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
       if (only_rank >= 0 && r != only_rank) continue;
       stream_ok = (uintptr_t)ins[r] % 16 == 0 && (uintptr_t)outs[r] % 16 == 0;
     }
+    // rounds of whole tiles: the plan unit of a minifloat codec is its group, so round the
+    // round size down to a tile multiple when a segment spans several rounds
+    if (stream_ok && p.R > kTileElems && p.R % kTileElems) {
+      p.R = p.R / kTileElems * kTileElems;
+      p.rounds = ceil_div(p.seg, p.R);
+      p.L1 = layout_of(cfg->stage1, p.R);
+      p.L2 = layout_of(cfg->stage2, p.R);
+      a.c1 = dev_codec(cfg->stage1, p.L1);
+      a.c2 = dev_codec(cfg->stage2, p.L2);
+    }
     a.stage_hint = (int)c->reduce_stages;
     a.q_hint = (int)c->q_stages;
     a.d_hint = (int)c->d_stages;
     a.cta_cap = (int)c->ctas_per_sm;
     a.dbg = (int)c->stream_mask;
   }
+  const int64_t span_lo = c->span_hi >= 0 ? c->span_lo : 0;
+  const int64_t span_hi = c->span_hi >= 0 ? std::min(c->span_hi, p.seg) : p.seg;
+  const int64_t rounds = ceil_div(span_hi - span_lo, p.R);
   // the three streaming phase launches for ranks [lo, hi) on device dev (ownq: the scatter
   // stage-1 quantizes the own piece into the receive slot too, the reduce reads it there)
   auto stream_phase = [&](int ph, int lo, int hi, int dev, cudaStream_t s) -> fc_status {
@@ -124,6 +134,33 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
       t.rank_lo = 0;
       t.rank_hi = N;
       strm = stream_ok && rgpl_ok<Tin, Tout, MfSpec<F - 1>, MfSpec<F - 1>>(t);
+    }
+    // across GPUs / processes (FC_OPT_FUSED -1) or when forced (1): the single-launch fused
+    // streaming kernel (k_fstream on MfSpec), like the integer codecs' default there
+    const bool fused = strm && (c->fused == 1 || (c->fused < 0 && (!single_dev || only_rank >= 0))) &&
+                       fused_eligible(a);
+    if (fused) {
+      if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {
+        using MS = MfSpec<F - 1>;
+        if (only_rank >= 0) {
+          const int r = only_rank, dev = c->devices[r];
+          FC_CUDA_TRY(cudaSetDevice(dev));
+          FC_TRY(bump_epoch(c, a, r, st[r]));
+          FC_TRY((launch_fstream<Tin, Tout, MS, MS>(c, a, r, r + 1, dev, st[r])));
+        } else if (single_dev) {
+          FC_CUDA_TRY(cudaSetDevice(c->devices[0]));
+          FC_TRY(bump_epoch(c, a, 0, st[0]));
+          FC_TRY((launch_fstream<Tin, Tout, MS, MS>(c, a, 0, N, c->devices[0], st[0])));
+        } else {
+          for (int r = 0; r < N; ++r) {
+            FC_CUDA_TRY(cudaSetDevice(c->devices[r]));
+            FC_TRY(bump_epoch(c, a, r, st[r]));
+            FC_TRY((launch_fstream<Tin, Tout, MS, MS>(c, a, r, r + 1, c->devices[r], st[r])));
+          }
+        }
+      }
+      FC_CUDA_TRY(cudaGetLastError());
+      continue;
     }
     if (strm) {
       if (only_rank >= 0) {

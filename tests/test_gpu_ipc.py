@@ -46,7 +46,7 @@ def _worker(rank, world, port, q, mode):
         comm.set_timeout(20.0)
         if mode == "fused":
             comm.set_option(_lib.OPT_FUSED, 1)
-        if mode == "split":
+        if mode in ("split", "mfsplit"):
             comm.set_option(_lib.OPT_FUSED, 0)
             comm.set_option(_lib.OPT_ONESHOT, 0)
         if mode == "generic":
@@ -56,9 +56,10 @@ def _worker(rank, world, port, q, mode):
         m = 8192 * world * 3 + (0 if mode != "generic" else 100)
         xs = orc.gen_rank_activations(8192, -(-m // 8192), 21, world)
         xs = [orc.round_to_bf16(x.ravel()[:m]) for x in xs]
-        if mode in ("minifloat", "mfstream"):
-            # e4m3 stages: float32 outputs take the lane-8 kernels, bf16 outputs the TMA-fed
-            # streaming kernels on MfSpec, both with IPC barriers
+        if mode in ("minifloat", "mfstream", "mfsplit"):
+            # e4m3 stages: float32 outputs take the lane-8 kernels with IPC barriers, bf16 outputs
+            # the fused streaming kernel on MfSpec (flag-synchronised across the processes), or
+            # ("mfsplit") the three streaming phase kernels with IPC barriers
             cfg = fc.FlashConfig.uniform(fc.CodecConfig(number_format="e4m3"))
             oc = orc.Codec(kind="e4m3")
         else:
@@ -67,7 +68,7 @@ def _worker(rank, world, port, q, mode):
         want = orc.flash_all_reduce(xs, oc, oc).outputs[0]
         for it in range(3):
             x = torch.from_numpy(xs[rank]).cuda().to(torch.bfloat16)
-            if mode == "mfstream":
+            if mode in ("mfstream", "mfsplit"):
                 out = comm.all_reduce(x, cfg, out_dtype=torch.bfloat16, check=True)
                 got = out.view(torch.int16).cpu().numpy()
                 assert np.array_equal(got, orc.f32_to_bf16_bits(want).view(np.int16)), f"iteration {it}"
@@ -141,7 +142,7 @@ def _run(world, mode):
 
 @pytest.mark.parametrize("world,mode", [(2, "fused"), (4, "fused"), (8, "fused"), (2, "split"), (4, "split"),
                                         (8, "split"), (2, "small"), (4, "small"), (8, "small"), (3, "generic"),
-                                        (4, "minifloat"), (8, "mfstream")])
+                                        (4, "minifloat"), (8, "mfstream"), (4, "mfsplit")])
 def test_ipc_parity(world, mode):
     _run(world, mode)
 

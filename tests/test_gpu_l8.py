@@ -169,7 +169,8 @@ def test_flash_minifloat_streaming_vs_oracle(fmt, dt, slot_tiles):
     """One minifloat format in both stages, g = 128, 16-bit in and out: the TMA-fed streaming
     kernels (k_qstream_gpl / k_rstream_gpl / k_dstream on MfSpec) -- one round, or three
     rounds of one tile (slots sized for one tile) -- bit-exact against the oracle, stage
-    buffers included, and equal to the lane-8 kernels (FC_OPT_STREAM_MASK bit 10)."""
+    buffers included, and equal to the fused kernel and the lane-8 kernels (FC_OPT_STREAM_MASK
+    bit 10)."""
     n, tiles = 8, 3
     m = n * 8192 * tiles
     rng = np.random.default_rng(7)
@@ -192,8 +193,14 @@ def test_flash_minifloat_streaming_vs_oracle(fmt, dt, slot_tiles):
     if not slot_tiles:
         assert comm.slot(1, 1, 0, cc).to_bytes() == res.stage1[1][0].wire_bytes()
         assert comm.slot(0, 2, 3, cc).to_bytes() == res.stage2[3].wire_bytes()
+    comm.set_option(_lib.OPT_FUSED, 1)  # the single-launch fused kernel on MfSpec (cross-GPU default)
+    runf = fc.flash_all_reduce(dts, cfg, comm=comm, out_dtype=dt)
+    fl = comm.get_option(_lib.OPT_LAST_LAUNCHES)
+    assert fl == 2 * launches // 3, (fl, launches)  # epoch bump + k_fstream per round
+    comm.set_option(_lib.OPT_FUSED, -1)
     comm.set_option(_lib.OPT_STREAM_MASK, 1024)
     run2 = fc.flash_all_reduce(dts, cfg, comm=comm, out_dtype=dt)
-    for o, o2 in zip(run.outputs, run2.outputs):
+    for o, o2, o3 in zip(run.outputs, run2.outputs, runf.outputs):
         assert torch.equal(o.view(torch.int16), o2.view(torch.int16))
+        assert torch.equal(o.view(torch.int16), o3.view(torch.int16))
     comm.close()

@@ -148,8 +148,10 @@ def fused_tune():
     comm.set_option(_lib.OPT_FUSED, 1)
     tiles = seg // 8192
     for chunk in (0, tiles // 4):
-        for qs, ds, cap, gc in ((0, 0, 0, 0), (4, 4, 0, 0), (4, 8, 0, 0), (6, 0, 0, 0), (0, 0, 0, 1), (0, 6, 0, 1),
-                                (0, 0, 0, 2), (4, 0, 2, 0)):
+        for qs, ds, cap, gc, rs in ((0, 0, 0, 0, 0), (4, 4, 0, 0, 0), (4, 8, 0, 0, 0), (6, 0, 0, 0, 0),
+                                    (0, 0, 0, 1, 0), (0, 6, 0, 1, 0), (0, 0, 0, 2, 0), (4, 0, 2, 0, 0),
+                                    (0, 0, 0, 0, 6), (0, 0, 0, 0, 12), (0, 0, 0, 0, 16), (8, 0, 0, 0, 16)):
+            comm.set_option(_lib.OPT_REDUCE_STAGES, rs)
             comm.set_option(_lib.OPT_FUSED_CHUNK, chunk)
             comm.set_option(_lib.OPT_SCATTER_STAGES, qs)
             comm.set_option(_lib.OPT_GATHER_STAGES, ds)
@@ -158,7 +160,7 @@ def fused_tune():
             t = timeit(lambda: comm.all_reduce_local(ins, cfg, outs=outs, check=False), iters=10, warm=3)
             comm.check()
             print(json.dumps({"kernel": "flash_fused_tune", "chunk": chunk, "q_stages": qs, "d_stages": ds,
-                              "cta_cap": cap, "gather_ctas_per_sm": gc, "ms": t, "frac": alg / t / 1e6 / PEAK}),
+                              "cta_cap": cap, "gather_ctas_per_sm": gc, "r_ring": rs, "ms": t, "frac": alg / t / 1e6 / PEAK}),
                   flush=True)
     comm.close()
 

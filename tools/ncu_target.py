@@ -26,7 +26,11 @@ if mode in ("fused", "split") or mode.startswith("c4"):
     comm.check()
 else:
     x = torch.randn(M, device="cuda").to(torch.bfloat16)
-    cc = fc.CodecConfig(number_format=mode[6:]) if mode.startswith("codec_") else fc.CodecConfig(bits=4)
+    if mode.startswith("codec_int"):  # codec_int<bits>_g<group>
+        b, g = mode[9:].split("_g")
+        cc = fc.CodecConfig(bits=int(b), group_size=int(g))
+    else:
+        cc = fc.CodecConfig(number_format=mode[6:]) if mode.startswith("codec_") else fc.CodecConfig(bits=4)
     for _ in range(3):
         q = fc.quantize(x, cc)
         fc.dequantize(q, dtype=torch.bfloat16, validate=False)

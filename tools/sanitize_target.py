@@ -2,7 +2,7 @@
 TP=8 INT4 and INT8 g128 flash all-reduce of bf16 (8 logical ranks on cuda:0,
 6 tiles per segment so every CTA ring wraps), phase-split (k_qstream_gpl /
 k_rstream_gpl / k_dstream) or fused (k_fstream, chunked schedule), and the
-single-GPU codec. Checks the result against the split path bit for bit.
+single-GPU codec; lane8: the minifloat / rotation paths. Checks the result against the split path bit for bit.
 usage: python tools/sanitize_target.py split|fused|codec|small|lane8"""
 import os
 import sys
@@ -51,7 +51,18 @@ elif mode == "lane8":  # minifloat stages and the fused rotation (k_l8_*), plus 
                 fc.FlashConfig(fc.CodecConfig(bits=4), fc.CodecConfig(bits=4), rotation=fc.HadamardBlock(128, sign_seed=3))):
         comm = FlashComm.local([0] * tp, slot_bytes_for(M // tp, cfg.stage1_codec, cfg.stage2_codec))
         for _ in range(2):
-            fc.flash_all_reduce(ins, cfg, comm=comm)
+            fc.flash_all_reduce(ins, cfg, comm=comm, out_dtype=torch.float32)
+        comm.close()
+    # minifloat stages with bf16 outputs: the streaming kernels on MfSpec, against the lane-8 ones
+    for f in ("e4m3", "e2m1"):
+        cfg = fc.FlashConfig.uniform(fc.CodecConfig(number_format=f))
+        comm = FlashComm.local([0] * tp, slot_bytes_for(M // tp, cfg.stage1_codec, cfg.stage2_codec))
+        comm.set_option(_lib.OPT_STREAM_MASK, 1024)
+        ref = [o.clone() for o in comm.all_reduce_local(ins, cfg)]
+        comm.set_option(_lib.OPT_STREAM_MASK, 0)
+        for _ in range(2):
+            outs = comm.all_reduce_local(ins, cfg)
+        assert all(torch.equal(a.view(torch.int16), b.view(torch.int16)) for a, b in zip(outs, ref)), f
         comm.close()
     for f in ("e4m3", "e2m1"):
         q = fc.quantize(ins[0], fc.CodecConfig(number_format=f))
