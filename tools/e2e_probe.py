@@ -61,7 +61,7 @@ def main():
             for h, d in zip(ho, ds):
                 h.copy_(d, non_blocking=True)
     print(f"H2D + D2H concurrently: {wall(both):.2f} ms")
-    for mib in (2, 4, 6, 8, 12, 16):
+    for mib in (4, 8, 12, 16, 24, 32):
         comm.set_option(_lib.OPT_HOST_CHUNK_BYTES, mib << 20)
         comm.all_reduce_host(hs, fcfg)
         t_all = wall(lambda: comm.all_reduce_host(hs, fcfg))
