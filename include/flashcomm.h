@@ -191,7 +191,9 @@ FC_API fc_status fc_flash_all_reduce_host(fc_comm* comm, const void* const* host
 FC_API fc_status fc_flash_all_reduce_host_rank(fc_comm* comm, const void* host_in, void* host_out, int64_t n,
                                                int32_t in_dtype, int32_t out_dtype, const fc_flash_cfg* cfg);
 /* flash_all_reduce, per-rank form (IPC world): every rank calls it with the
- * same n/cfg in the same order. in may alias out. */
+ * same n/cfg in the same order. in may alias out; both 16-byte aligned
+ * (FC_ERR_DOMAIN otherwise: the kernel path, which every rank must share,
+ * depends on it). */
 FC_API fc_status fc_flash_all_reduce(fc_comm* comm, const void* in, void* out, int64_t n, int32_t in_dtype,
                               int32_t out_dtype, const fc_flash_cfg* cfg, void* stream);
 

@@ -435,6 +435,10 @@ fc_status fc_flash_all_reduce(fc_comm* c, const void* in, void* out, int64_t n, 
   FC_TRY(check_call(c, n, in_dtype, out_dtype, cfg));
   if (!c->ipc) return fail(FC_ERR_CONFIG, "fc_flash_all_reduce needs an IPC communicator");
   if (!in || !out) return fail(FC_ERR_DOMAIN, "NULL buffer");
+  // every rank must take the same kernel path (flags / barriers, slot layouts); the path
+  // depends on buffer alignment, which one process cannot see for its peers
+  if ((uintptr_t)in % 16 || (uintptr_t)out % 16)
+    return fail(FC_ERR_DOMAIN, "IPC all-reduce buffers must be 16-byte aligned");
   const int r = c->my_rank;
   if (c->world == 1) return FC_DISPATCH2(in_dtype, out_dtype, identity_typed, in, out, n, c->devices[r], (cudaStream_t)stream);
   for (int p = 0; p < c->world; ++p)

@@ -82,12 +82,10 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
   bool stream_ok = false;
   if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {
     stream_ok = c->fast == 1 && c->rot_dim == 0 && !(c->stream_mask & 1024);
-    for (int r = 0; r < N && stream_ok; ++r) {
-      if (only_rank >= 0 && r != only_rank) continue;
-      stream_ok = (uintptr_t)ins[r] % 16 == 0 && (uintptr_t)outs[r] % 16 == 0;
-    }
     // rounds of whole tiles: the plan unit of a minifloat codec is its group, so round the
-    // round size down to a tile multiple when a segment spans several rounds
+    // round size down to a tile multiple when a segment spans several rounds (decided before
+    // the buffers' alignment, which may differ between IPC ranks: every rank keeps one slot
+    // layout)
     if (stream_ok && p.R > kTileElems && p.R % kTileElems) {
       p.R = p.R / kTileElems * kTileElems;
       p.rounds = ceil_div(p.seg, p.R);
@@ -95,6 +93,10 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
       p.L2 = layout_of(cfg->stage2, p.R);
       a.c1 = dev_codec(cfg->stage1, p.L1);
       a.c2 = dev_codec(cfg->stage2, p.L2);
+    }
+    for (int r = 0; r < N && stream_ok; ++r) {
+      if (only_rank >= 0 && r != only_rank) continue;
+      stream_ok = (uintptr_t)ins[r] % 16 == 0 && (uintptr_t)outs[r] % 16 == 0;
     }
     a.stage_hint = (int)c->reduce_stages;
     a.q_hint = (int)c->q_stages;

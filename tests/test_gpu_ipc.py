@@ -95,6 +95,16 @@ def _worker(rank, world, port, q, mode):
                 raise AssertionError("expected ProtocolError")
             except fc.ProtocolError as e:
                 assert "unconsumed" in str(e), str(e)
+        if mode == "unaligned":
+            # a view 2 bytes into its storage: refused before any launch (the kernel path every
+            # rank must share depends on alignment), so no rank waits on a peer
+            base = torch.zeros(8 * 8192 * world + 8, device="cuda", dtype=torch.bfloat16)
+            try:
+                comm.all_reduce(base[1:1 + 8 * 8192 * world], cfg)
+                raise AssertionError("expected DomainError")
+            except fc.DomainError as e:
+                assert "aligned" in str(e), str(e)
+            dist.barrier()
         if mode == "abort":
             # ranks 0 and 1 call, rank 2 never does; rank 0 (2 s timeout) gives up first and its
             # abort reaches rank 1 (60 s timeout) at once (fabric.py:168-172, 203-205)
@@ -145,6 +155,10 @@ def _run(world, mode):
                                         (4, "minifloat"), (8, "mfstream"), (4, "mfsplit")])
 def test_ipc_parity(world, mode):
     _run(world, mode)
+
+
+def test_ipc_unaligned_buffer_refused():
+    _run(2, "unaligned")
 
 
 def test_ipc_timeout_names_peer():
