@@ -153,7 +153,7 @@ typedef enum {
   FC_OPT_SCATTER_STAGES = 7,/* ring depth of the streaming scatter / quantize kernel (0 = auto) */
   FC_OPT_GATHER_STAGES = 8, /* ring depth of the streaming gather / dequantize kernel (0 = auto) */
   FC_OPT_CTAS_PER_SM = 9,   /* cap on resident CTAs per SM of the streaming kernels (0 = occupancy) */
-  FC_OPT_STREAM_MASK = 10,  /* A/B testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels; bit 4: INT8 g=128 scatter on the group-per-lane kernel; bit 5: its code stores direct (not staged); bits 6/7: g=128 scatter/reduce on the 32-element lane layout; bit 10: minifloat flash rounds on the lane-8 kernels instead of the streaming ones; bit 11: small-message kernel as a plain launch; bit 12: group-lane reduce consumers in lockstep; bit 13: phase kernels as plain launches (no programmatic dependent launch); measurement only (results invalid): bit 8 skips the fused kernel's flag waits, bit 9 its flag publications */
+  FC_OPT_STREAM_MASK = 10,  /* A/B testing: bit 0/1/2 runs scatter/reduce/gather on the cp.async-staged kernels; bit 4: INT8 g=128 scatter on the group-per-lane kernel; bit 5: its code stores direct (not staged); bits 6/7: g=128 scatter/reduce on the 32-element lane layout; bit 10: minifloat flash rounds on the lane-8 kernels instead of the streaming ones; bit 11: small-message kernel as a plain launch; bit 12: group-lane reduce consumers in lockstep; bit 13: phase kernels as plain launches (no programmatic dependent launch, A/B); measurement only (results invalid): bit 8 skips the fused kernel's flag waits, bit 9 its flag publications */
   FC_OPT_PHASES = 11,       /* measurement only: run just these phases (bit 0/1/2) of a one-GPU split call */
   FC_OPT_FUSED_CHUNK = 12,  /* fused kernel schedule: tiles per chunk (step s scatters chunk s, reduces s-1,
                                gathers s-2); 0 = auto: the whole round on one GPU, a quarter across GPUs */

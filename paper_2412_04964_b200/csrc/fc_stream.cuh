@@ -1987,12 +1987,16 @@ __device__ __forceinline__ void d_role(const FlashArgs& a, uint32_t sbase, int S
 // Programmatic dependent launch (the phase kernels are launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization): a CTA waits for the previous kernel's
 // completion (and the visibility of its memory) before its first global access, and lets the
-// next kernel launch once its own work is issued -- the next phase's launch and CTA
-// scheduling overlap this phase's last CTAs. (Triggering at entry instead placed the next
-// kernel's CTAs on the SMs that drained first, unbalancing its persistent grid:
-// tools/pdl_probe.py.) Both are no-ops for plain launches.
+// next kernel launch once all its warps are done -- the next phase's launch and CTA
+// scheduling overlap this phase's last CTAs. (Triggering earlier -- at entry, or from the
+// producer warp, which finishes issuing long before the consumers -- placed the next
+// kernel's CTAs on the SMs that drained first and unbalanced its persistent grid: C2
+// 535 -> 617-742 us, tools/pdl_probe.py.) Both are no-ops for plain launches.
 __device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_exit() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_exit() {
+  __syncthreads();  // one trigger per CTA, after every warp's work (the producer warp ends early)
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 template <typename Tin, class S1>
 __global__ void __launch_bounds__(kStreamThreads) k_qstream(FlashArgs a) {
