@@ -479,6 +479,35 @@ __device__ __forceinline__ uint32_t mf_enc2(int fmt, float x0, float x1) {
   return r;
 }
 
+// mf_enc2 without the +0 fix-up (cvt.rn.satfinite only): the streaming kernels pack the codes
+// into words first and fix a whole word at once (mf_fix_zero)
+__device__ __forceinline__ uint32_t mf_enc2_raw(int fmt, float x0, float x1) {
+  uint32_t r;
+  if (fmt == FC_FMT_E4M3) {
+    unsigned short h;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(h) : "f"(x1), "f"(x0));
+    r = h;
+  } else if (fmt == FC_FMT_E5M2) {
+    unsigned short h;
+    asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(h) : "f"(x1), "f"(x0));
+    r = h;
+  } else {
+    asm("{\n .reg .b8 t;\n cvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n cvt.u32.u8 %0, t;\n}" : "=r"(r) : "f"(x1), "f"(x0));
+  }
+  return r;
+}
+
+// a word of minifloat codes (4 bytes e4m3 / e5m2, 8 nibbles e2m1): every code whose magnitude
+// bits are zero becomes +0 (encode() stores zero magnitudes as +0). Per code, magnitude +
+// all-ones-magnitude carries into the sign position iff the magnitude is non-zero (no carry
+// crosses a code), so the sign survives exactly there
+template <int FMT>
+__device__ __forceinline__ uint32_t mf_fix_zero(uint32_t w) {
+  constexpr uint32_t MAG = FMT == FC_FMT_E2M1 ? 0x77777777u : 0x7F7F7F7Fu;
+  const uint32_t mag = w & MAG;
+  return mag | (w & (mag + MAG) & ~MAG);
+}
+
 // two codes (as packed by mf_enc2) -> two exact fp32 grid values
 __device__ __forceinline__ void mf_dec2(int fmt, uint32_t code2, float& v0, float& v1) {
   uint32_t h2;

@@ -556,18 +556,21 @@ __device__ __forceinline__ void chunk_codes_clamped(const uint32_t x[4], float s
 // e5m2: w[0] = elements 0..3, w[1] = 4..7) or nibbles little-nibble-first (e2m1: w[0])
 template <class Spec, typename Tin>
 __device__ __forceinline__ void chunk_codes_mf(const uint32_t x[4], const GroupQ& g, uint32_t* w) {
+  const uint64_t R2 = f2_splat(g.r), NS2 = f2_splat(-g.s);
   uint32_t two[4];
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const float x0 = __uint_as_float(chunk_elem<Tin>(x, 2 * p)), x1 = __uint_as_float(chunk_elem<Tin>(x, 2 * p + 1));
-    const float t0 = x0 * g.r, t1 = x1 * g.r;
-    two[p] = mf_enc2(Spec::FMT, fmaf(fmaf(-t0, g.s, x0), g.r, t0), fmaf(fmaf(-t1, g.s, x1), g.r, t1));
+  for (int p = 0; p < 4; ++p) {  // the quotient pairwise (FMUL2 / FFMA2: the same roundings as fmaf)
+    const uint64_t X = chunk_pair<Tin>(x, 2 * p, 2 * p + 1);
+    const uint64_t T = f2_mul(X, R2);
+    float q0, q1;
+    f2_unpack(f2_fma(f2_fma(T, NS2, X), R2, T), q0, q1);
+    two[p] = mf_enc2_raw(Spec::FMT, q0, q1);
   }
   if constexpr (Spec::SB == 8) {
-    w[0] = two[0] | (two[1] << 16);
-    w[1] = two[2] | (two[3] << 16);
+    w[0] = mf_fix_zero<Spec::FMT>(two[0] | (two[1] << 16));
+    w[1] = mf_fix_zero<Spec::FMT>(two[2] | (two[3] << 16));
   } else {
-    w[0] = two[0] | (two[1] << 8) | (two[2] << 16) | (two[3] << 24);
+    w[0] = mf_fix_zero<Spec::FMT>(two[0] | (two[1] << 8) | (two[2] << 16) | (two[3] << 24));
   }
 }
 
@@ -1436,13 +1439,14 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
           float q0, q1, q2, q3;
           quo(acc[2 * i], q0, q2);
           quo(acc[2 * i + 1], q1, q3);
-          w2[i] = mf_enc2(S2::FMT, q0, q1) | (mf_enc2(S2::FMT, q2, q3) << 16);
+          w2[i] = mf_fix_zero<S2::FMT>(mf_enc2_raw(S2::FMT, q0, q1) | (mf_enc2_raw(S2::FMT, q2, q3) << 16));
         } else {
           float q[8];
 #pragma unroll
           for (int aa = 0; aa < 4; ++aa) quo(acc[4 * i + aa], q[aa], q[aa + 4]);
-          w2[i] = mf_enc2(S2::FMT, q[0], q[1]) | (mf_enc2(S2::FMT, q[2], q[3]) << 8) |
-                  (mf_enc2(S2::FMT, q[4], q[5]) << 16) | (mf_enc2(S2::FMT, q[6], q[7]) << 24);
+          w2[i] = mf_fix_zero<S2::FMT>(mf_enc2_raw(S2::FMT, q[0], q[1]) | (mf_enc2_raw(S2::FMT, q[2], q[3]) << 8) |
+                                       (mf_enc2_raw(S2::FMT, q[4], q[5]) << 16) |
+                                       (mf_enc2_raw(S2::FMT, q[6], q[7]) << 24));
         }
       }
     } else if (g2.normal) {
