@@ -12,6 +12,7 @@ from paper_2412_04964_b200 import _lib  # noqa: E402
 from bench import graph_time  # noqa: E402
 
 M = 8 * 1024 * 8192
+torch.manual_seed(0)
 x = torch.randn(M, device="cuda").to(torch.bfloat16)
 st = torch.cuda.current_stream()
 for bits in (4, 8):
@@ -20,7 +21,7 @@ for bits in (4, 8):
     buf = torch.empty(L.total_bytes, dtype=torch.uint8, device="cuda")
     c = cc.to_fc()
     qf = lambda: _lib.check(_lib.lib().fc_quantize(x.data_ptr(), _lib.DTYPE_BF16, M, C.byref(c), buf.data_ptr(),  # noqa: E731
-                                                   None, st.cuda_stream))
+                                                   None, torch.cuda.current_stream().cuda_stream))
     qf()
     torch.cuda.synchronize()
     ref = torch.load("/tmp/g32_%d.pt" % bits) if os.path.exists("/tmp/g32_%d.pt" % bits) else None
