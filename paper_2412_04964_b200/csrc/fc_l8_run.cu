@@ -76,11 +76,11 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
     ++g_launch_count;
     return FC_OK;
   };
-  // one minifloat format in both stages, g = 128, 16-bit inputs and outputs, no rotation: the
+  // one minifloat format in both stages, g = 128, 16-bit inputs, 16-bit or fp32 outputs, no rotation: the
   // TMA-fed streaming kernels (k_qstream_gpl / k_rstream_gpl / k_dstream on MfSpec) take every
   // round of whole tiles; the lane-8 kernels the rest (bit 10 of FC_OPT_STREAM_MASK: A/B off)
   bool stream_ok = false;
-  if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {
+  if constexpr (F != 0 && sizeof(Tin) == 2 && (sizeof(Tout) == 2 || sizeof(Tout) == 4)) {
     stream_ok = c->fast == 1 && c->rot_dim == 0 && !(c->stream_mask & 1024);
     // rounds of whole tiles: the plan unit of a minifloat codec is its group, so round the
     // round size down to a tile multiple when a segment spans several rounds (decided before
@@ -110,7 +110,7 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
   // the three streaming phase launches for ranks [lo, hi) on device dev (ownq: the scatter
   // stage-1 quantizes the own piece into the receive slot too, the reduce reads it there)
   auto stream_phase = [&](int ph, int lo, int hi, int dev, cudaStream_t s) -> fc_status {
-    if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {
+    if constexpr (F != 0 && sizeof(Tin) == 2 && (sizeof(Tout) == 2 || sizeof(Tout) == 4)) {
       using MS = MfSpec<F - 1>;
       FlashArgs b = a;
       b.rank_lo = lo;
@@ -131,7 +131,7 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
     a.epoch = ++c->epoch;
     a.epoch_dev = nullptr;
     bool strm = false;
-    if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {
+    if constexpr (F != 0 && sizeof(Tin) == 2 && (sizeof(Tout) == 2 || sizeof(Tout) == 4)) {
       FlashArgs t = a;  // every rank decides alike: the last owner's segment bounds the round
       t.rank_lo = 0;
       t.rank_hi = N;
@@ -139,7 +139,7 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
     }
     // across GPUs / processes (FC_OPT_FUSED -1) or when forced (1): the single-launch fused
     // streaming kernel (k_fstream on MfSpec), like the integer codecs' default there
-    const bool fused = strm && (c->fused == 1 || (c->fused < 0 && (!single_dev || only_rank >= 0))) &&
+    const bool fused = strm && sizeof(Tout) == 2 && (c->fused == 1 || (c->fused < 0 && (!single_dev || only_rank >= 0))) &&
                        fused_eligible(a);
     if (fused) {
       if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {

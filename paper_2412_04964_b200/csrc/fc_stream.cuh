@@ -1233,7 +1233,7 @@ __host__ __device__ inline int rg_ring_for(const DevCodec& c1, uint32_t budget) 
 
 template <typename Tin, typename Tout, class S1, class S2, bool FUSED, class Iter>
 __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, int R, Iter it0, uint32_t bars_in = 0) {
-  static_assert(sizeof(Tin) == 2 && sizeof(Tout) == 2, "16-bit inputs and outputs");
+  static_assert(sizeof(Tin) == 2 && (sizeof(Tout) == 2 || sizeof(Tout) == 4), "16-bit inputs, 16/32-bit outputs");
   static_assert(S1::SB == S2::SB, "one storage width for both stages");
   static_assert(kGplWarps == kRgWpt, "one tile per pass of the consumer warps");
   constexpr int SB = S1::SB;
@@ -1525,27 +1525,38 @@ __device__ __forceinline__ void r_role_gpl(const FlashArgs& a, uint32_t sbase, i
         decode_words_mf<S2, NW>(w2, g2.s, acc);  // 0 + grid s: exact, +0 for the +0 code
       else
         decode_words<SB, NW>(w2, g2.s, 8388608.0f + (float)g2.z, acc);  // 0 + (c - z) s: exact, never -0
+      if constexpr (sizeof(Tout) == 4) {
+        // fp32 outputs: the lane's 64 elements (256 contiguous bytes) as 16-B stores; a warp
+        // instruction covers half of 32 sectors, the next one the other half (merged in L2)
+        float* ob = reinterpret_cast<float*>(a.out[j]) + seg0 + p0;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        uint32_t h[4];
+        for (int c = 0; c < 2 * NC; ++c)
+          st_v4(ob + 4 * c, make_uint4(__float_as_uint(acc_get<SB>(acc, 4 * c)), __float_as_uint(acc_get<SB>(acc, 4 * c + 1)),
+                                       __float_as_uint(acc_get<SB>(acc, 4 * c + 2)),
+                                       __float_as_uint(acc_get<SB>(acc, 4 * c + 3))));
+      } else {
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq)
-          h[qq] = pack2(acc_get<SB>(acc, 8 * c + 2 * qq), acc_get<SB>(acc, 8 * c + 2 * qq + 1), (Tout*)nullptr);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(lb + 16 * (c ^ m)), "r"(h[0]), "r"(h[1]),
-                     "r"(h[2]), "r"(h[3])
-                     : "memory");
+        for (int c = 0; c < NC; ++c) {
+          uint32_t h[4];
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            h[qq] = pack2(acc_get<SB>(acc, 8 * c + 2 * qq), acc_get<SB>(acc, 8 * c + 2 * qq + 1), (Tout*)nullptr);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(lb + 16 * (c ^ m)), "r"(h[0]), "r"(h[1]),
+                       "r"(h[2]), "r"(h[3])
+                       : "memory");
+        }
+        __syncwarp();
+        const uint32_t wbase = sbase + warp * (32 * kRgEpl * 2);
+        uint8_t* ob = reinterpret_cast<uint8_t*>(reinterpret_cast<Tout*>(a.out[j]) + seg0 + e0 + warp * (32 * kRgEpl));
+        // byte 512 v + 16 lane of the warp's output = chunk qq = lane % 8 of slice l = 4 v + lane / 8,
+        // stored at l * 128 + 16 (qq ^ (l & 7)) (conflict-free for each 8-lane phase)
+#pragma unroll
+        for (int v = 0; v < NC; ++v) {
+          const int l = 4 * v + (lane >> 3), qq = lane & 7;
+          st_v4(ob + 512 * v + 16 * lane, lds128_(wbase + l * (kRgEpl * 2) + 16 * (qq ^ (l & 7))));
+        }
+        __syncwarp();  // the staging buffer's loads are complete before the next item rewrites it
       }
-      __syncwarp();
-      const uint32_t wbase = sbase + warp * (32 * kRgEpl * 2);
-      uint8_t* ob = reinterpret_cast<uint8_t*>(reinterpret_cast<Tout*>(a.out[j]) + seg0 + e0 + warp * (32 * kRgEpl));
-      // byte 512 v + 16 lane of the warp's output = chunk qq = lane % 8 of slice l = 4 v + lane / 8,
-      // stored at l * 128 + 16 (qq ^ (l & 7)) (conflict-free for each 8-lane phase)
-#pragma unroll
-      for (int v = 0; v < NC; ++v) {
-        const int l = 4 * v + (lane >> 3), qq = lane & 7;
-        st_v4(ob + 512 * v + 16 * lane, lds128_(wbase + l * (kRgEpl * 2) + 16 * (qq ^ (l & 7))));
-      }
-      __syncwarp();  // the staging buffer's loads are complete before the next item rewrites it
     }
     if (bad) atomicOr(errw(a, j), make_err(kErrNonFinite, kPhReduce, j, j));
     if (a.dbg & 4096) consumers_sync<kRgWpt * 32>();  // A/B: consumer warps in lockstep per tile
@@ -2046,7 +2057,7 @@ template <typename Tin, typename Tout, class S1, class S2>
 __global__ void __launch_bounds__(kGplThreads, 4) k_rstream_gpl(FlashArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   pdl_enter();
-  if constexpr (sizeof(Tout) == 2 && S1::SB == S2::SB)
+  if constexpr ((sizeof(Tout) == 2 || sizeof(Tout) == 4) && S1::SB == S2::SB)
     r_role_gpl<Tin, Tout, S1, S2, false>(a, smem_u32(smem), a.stages,
                                   RangeIter((a.rank_hi - a.rank_lo) * a.tiles, a.tiles, blockIdx.x, gridDim.x));
   pdl_exit();
