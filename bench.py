@@ -9,8 +9,10 @@ all-reduce of bf16 [8,1024,8192] per rank at TP=8 — with all 8 TP ranks
 emulated on one B200 (8 logical ranks, the reference's list-of-tensors call;
 peer stores land in local HBM instead of crossing NVLink). One step = one
 all-reduce of all 8 ranks' tensors = three launches (scatter k_qstream_gpl,
-reduce k_rstream_gpl, gather k_dstream); the fused single-launch kernel is
-timed beside it.
+reduce k_rstream_gpl, gather k_dstream, launched with programmatic dependent
+launch); the fused single-launch kernel is timed beside it, and the same K
+steps replayed from one CUDA graph (`roofline.step.ms_graph`: no per-call host
+cost) beside the eager `value`.
 
 N>1: one process per GPU (the driver's torchrun launch; `--gpus N` outside
 torchrun re-executes itself under torch.distributed.run), TP = N, CUDA IPC
