@@ -139,10 +139,10 @@ fc_status run_l8_typed(fc_comm* c, const void* const* ins, void* const* outs, in
     }
     // across GPUs / processes (FC_OPT_FUSED -1) or when forced (1): the single-launch fused
     // streaming kernel (k_fstream on MfSpec), like the integer codecs' default there
-    const bool fused = strm && sizeof(Tout) == 2 && (c->fused == 1 || (c->fused < 0 && (!single_dev || only_rank >= 0))) &&
+    const bool fused = strm && (c->fused == 1 || (c->fused < 0 && (!single_dev || only_rank >= 0))) &&
                        fused_eligible(a);
     if (fused) {
-      if constexpr (F != 0 && sizeof(Tin) == 2 && sizeof(Tout) == 2) {
+      if constexpr (F != 0 && sizeof(Tin) == 2 && (sizeof(Tout) == 2 || sizeof(Tout) == 4)) {
         using MS = MfSpec<F - 1>;
         if (only_rank >= 0) {
           const int r = only_rank, dev = c->devices[r];

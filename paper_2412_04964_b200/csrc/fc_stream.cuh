@@ -2128,7 +2128,7 @@ __device__ __forceinline__ void fused_role_switch(uint32_t bars, int nb) {
 // launch's last CTA zeroes the counters for the next launch.
 template <typename Tin, typename Tout, class S1, class S2>
 __global__ void __launch_bounds__(kGplThreads, 3) k_fstream(const __grid_constant__ FlashArgs a) {
-  if constexpr (sizeof(Tin) == 2 && sizeof(Tout) == 2 && S1::SB == S2::SB) {
+  if constexpr (sizeof(Tin) == 2 && (sizeof(Tout) == 2 || sizeof(Tout) == 4) && S1::SB == S2::SB) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ int s_last;
     const uint32_t sb = smem_u32(smem);

@@ -70,10 +70,14 @@ def _worker(rank, world, port, q, mode):
             x = torch.from_numpy(xs[rank]).cuda().to(torch.bfloat16)
             if mode in ("mfstream", "mfsplit"):
                 out = comm.all_reduce(x, cfg, out_dtype=torch.bfloat16, check=True)
+                launches = comm.get_option(_lib.OPT_LAST_LAUNCHES)
+                assert launches == (2 if mode == "mfstream" else 6), launches  # fused / split + 2 barriers
                 got = out.view(torch.int16).cpu().numpy()
                 assert np.array_equal(got, orc.f32_to_bf16_bits(want).view(np.int16)), f"iteration {it}"
                 continue
             out = comm.all_reduce(x, cfg, out_dtype=torch.float32, check=True)
+            if mode == "fused":  # the fused kernel itself ran (fp32 outputs): epoch bump + k_fstream
+                assert comm.get_option(_lib.OPT_LAST_LAUNCHES) == 2, comm.get_option(_lib.OPT_LAST_LAUNCHES)
             got = out.cpu().numpy()
             assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), f"iteration {it}"
         dist.barrier()
