@@ -20,18 +20,18 @@ tp, M = 8, 8 * 8192 * 6
 g = torch.Generator(device="cuda").manual_seed(5)
 ins = [torch.randn(M, device="cuda", generator=g).to(torch.bfloat16) for _ in range(tp)]
 if mode in ("split", "fused"):
-    for bits in (4, 8):
+    for bits, odt in ((4, torch.bfloat16), (8, torch.bfloat16), (4, torch.float32)):  # fp32: the register-direct reduce output
         cfg = fc.FlashConfig.from_bits(bits)
         comm = FlashComm.local([0] * tp, slot_bytes_for(M // tp, cfg.stage1_codec, cfg.stage2_codec))
         comm.set_timeout(1200.0)  # racecheck slows the flag-synchronised kernels by 100-1000x
         comm.set_option(_lib.OPT_FUSED, 0)
-        ref = [o.clone() for o in comm.all_reduce_local(ins, cfg)]
+        ref = [o.clone() for o in comm.all_reduce_local(ins, cfg, out_dtype=odt)]
         comm.set_option(_lib.OPT_FUSED, int(mode == "fused"))
         if mode == "fused":
             comm.set_option(_lib.OPT_FUSED_CHUNK, 2)
         for _ in range(2):
-            outs = comm.all_reduce_local(ins, cfg)
-        assert all(torch.equal(a.view(torch.int16), b.view(torch.int16)) for a, b in zip(outs, ref)), mode
+            outs = comm.all_reduce_local(ins, cfg, out_dtype=odt)
+        assert all(torch.equal(a, b) for a, b in zip(outs, ref)), mode
         comm.close()
 elif mode == "small":  # decode-sized rounds: the one-launch k_small (vs the split kernels)
     for bits in (4, 8):
