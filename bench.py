@@ -123,11 +123,6 @@ class NvmlClockSampler:
                         pass
                     time.sleep(0.001)
 
-            # the launching thread holds the GIL almost continuously; a 0.5-ms switch interval
-            # (default 5 ms) lets the sampler in ~every ms of a ~11-ms timed region (the device-
-            # bound step keeps its queue full either way)
-            self.switch = sys.getswitchinterval()
-            sys.setswitchinterval(0.0005)
             self.thread = threading.Thread(target=run, daemon=True)
             self.thread.start()
         except Exception:
@@ -139,7 +134,6 @@ class NvmlClockSampler:
             return self.fallback.stop()
         self.stop_flag.set()
         self.thread.join(timeout=2)
-        sys.setswitchinterval(self.switch)
         sms = [sm for sm, _ in self.samples]
         reasons = sorted({r for _, rs in self.samples for r in rs})
         return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": self.max_sm,
